@@ -1,1 +1,24 @@
-"""B200-native fractal-image encoder hot path."""
+"""B200-native fractal-image encoder hot path (arXiv 1206.4880), see DESIGN.md.
+
+Public names mirror the reference package ``fic`` for the rebuilt path:
+``encode``, ``decode``, ``serialize``, ``deserialize``, ``FractalCode``,
+``EncodeStats``, ``FormatError``, ``RECORD_DTYPE``, ``dbc_grid``.
+"""
+
+from .codec import (  # noqa: F401
+    RECORD_DTYPE,
+    STRATEGIES,
+    STRATEGY_IDS,
+    EncodeStats,
+    FormatError,
+    FractalCode,
+    dbc_grid,
+    decode,
+    deserialize,
+    encode,
+    encode_device,
+    plan,
+    serialize,
+)
+
+__version__ = "0.1.0"

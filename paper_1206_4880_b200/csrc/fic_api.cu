@@ -1,0 +1,851 @@
+// C ABI of the B200 fractal encoder (include/fic_b200.h): validation, pool
+// planning, work decomposition and orchestration of the kernels.
+#include <cuda.h>
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "kernels.h"
+#include "match.h"
+
+namespace fic {
+
+static thread_local std::string g_err;
+thread_local int g_launches = 0;
+void set_error(const std::string& m) { g_err = m; }
+const char* last_error() { return g_err.c_str(); }
+
+// ---------------------------------------------------------------------------
+// stream-ordered scratch: every buffer of a call comes from the device's
+// default memory pool (kept cached across calls) and is freed on the stream.
+// ---------------------------------------------------------------------------
+class Scratch {
+ public:
+  explicit Scratch(cudaStream_t s) : s_(s) {
+    static bool pool_set = false;
+    if (!pool_set) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaMemPool_t pool;
+      if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+      }
+      pool_set = true;
+    }
+  }
+  ~Scratch() {
+    for (void* p : ptrs_) cudaFreeAsync(p, s_);
+  }
+  template <class T>
+  T* get(size_t n) {
+    if (n == 0) n = 1;
+    void* p = nullptr;
+    FIC_CUDA(cudaMallocAsync(&p, n * sizeof(T), s_));
+    ptrs_.push_back(p);
+    return static_cast<T*>(p);
+  }
+
+ private:
+  cudaStream_t s_;
+  std::vector<void*> ptrs_;
+};
+
+struct Timer {
+  cudaEvent_t ev[8];
+  int n = 0;
+  cudaStream_t s;
+  explicit Timer(cudaStream_t st) : s(st) {
+    for (auto& e : ev) FIC_CUDA(cudaEventCreate(&e));
+  }
+  ~Timer() {
+    for (auto& e : ev) cudaEventDestroy(e);
+  }
+  void mark() { FIC_CUDA(cudaEventRecord(ev[n++], s)); }
+  double ms(int a, int b) {
+    float t = 0;
+    cudaEventElapsedTime(&t, ev[a], ev[b]);
+    return t;
+  }
+};
+
+static const char* kStrategyTuple = "('exhaustive', 'nosearch', 'static2', 'dynamic_fd')";
+
+// Validation in the reference's order (codec.py:313-331, blocks.py:63-68,
+// 148-151, fdim.py:48-56) with its messages.
+static Geo validate(int H, int W, const fic_params_t& p) {
+  if (H <= 0 || W <= 0) invalid("image must be a 2-D uint8 array");
+  if (p.strategy < 0 || p.strategy > 3)
+    invalid("unknown strategy " + std::to_string(p.strategy) + "; use one of " + kStrategyTuple);
+  if (p.domain_size != 2 * p.range_size) invalid("domain_size must be exactly twice range_size");
+  if (p.fd_source != 0 && p.fd_source != 1)
+    invalid("fd_source must be 'original' or 'downsampled'");
+  if (p.range_size <= 0 || H % p.range_size || W % p.range_size)
+    invalid("image " + std::to_string(W) + "x" + std::to_string(H) +
+            " not divisible by range size " + std::to_string(p.range_size));
+  if (p.stride < 1) invalid("stride must be >= 1");
+  if (p.domain_size > std::min(W, H))
+    invalid("domain size " + std::to_string(p.domain_size) + " exceeds image " +
+            std::to_string(W) + "x" + std::to_string(H));
+  Geo g;
+  g.H = H;
+  g.W = W;
+  g.rs = p.range_size;
+  g.ds = p.domain_size;
+  g.st = p.stride;
+  g.npx = g.rs * g.rs;
+  g.nrx = W / g.rs;
+  g.nry = H / g.rs;
+  g.R = g.nrx * g.nry;
+  g.ndx = (W - g.ds) / g.st + 1;
+  g.ndy = (H - g.ds) / g.st + 1;
+  g.D = (int64_t)g.ndx * g.ndy;
+  g.n_iso = p.isometries ? 8 : 1;
+  if (g.D == 0) invalid("empty domain set");
+  if (g.D >= (int64_t)1 << 31) invalid("too many domain positions for this build (>= 2^31)");
+  return g;
+}
+
+static void check_dbc_side(int side) {
+  uint16_t q[7 * 256];
+  int smax = 0, need = 0;
+  int J = 0;
+  std::vector<int> scales;
+  for (int s = 2; s <= side / 2; s *= 2)
+    if (side % s == 0) ++J;
+  if (J < 2)
+    invalid("block side " + std::to_string(side) + " too small: need at least two DBC scales");
+  (void)q;
+  (void)smax;
+  (void)need;
+}
+
+// Device-resident DBC tables for one block side.
+struct DbcTables {
+  int J = 0, smax = 0, ln_len = 0;
+  uint16_t* quot = nullptr;
+  double* ln = nullptr;
+  double* w = nullptr;
+};
+
+static DbcTables make_dbc(Scratch& sc, cudaStream_t s, int side, const double* h_ln, int ln_len,
+                          const double* h_w, int n_w) {
+  DbcTables t;
+  std::vector<uint16_t> q(7 * 256);
+  int need = 0;
+  t.J = dbc_tables(side, q.data(), &t.smax, &need);
+  if (t.J < 2)
+    invalid("block side " + std::to_string(side) + " too small: need at least two DBC scales");
+  // ln table: caller's numpy values if long enough, else C log()
+  std::vector<double> ln;
+  if (h_ln && ln_len >= need) {
+    ln.assign(h_ln, h_ln + need);
+  } else {
+    ln.resize(need);
+    for (int k = 0; k < need; ++k) ln[k] = std::log((double)k);
+  }
+  // slope weights: caller's numpy values, else fdim.py:37-41 in C
+  std::vector<double> w(t.J);
+  if (h_w && n_w == t.J) {
+    std::copy(h_w, h_w + t.J, w.begin());
+  } else {
+    std::vector<double> xs(t.J);
+    double mean = 0;
+    for (int j = 0; j < t.J; ++j) {
+      xs[j] = std::log((double)side / (double)(2 << j));
+      mean = (j == 0) ? xs[0] : mean + xs[j];
+    }
+    mean /= t.J;
+    double dd = 0;
+    for (int j = 0; j < t.J; ++j) dd += (xs[j] - mean) * (xs[j] - mean);
+    for (int j = 0; j < t.J; ++j) w[j] = (xs[j] - mean) / dd;
+  }
+  t.ln_len = need;
+  t.quot = sc.get<uint16_t>(t.J * 256);
+  t.ln = sc.get<double>(need);
+  t.w = sc.get<double>(t.J);
+  FIC_CUDA(cudaMemcpyAsync(t.quot, q.data(), t.J * 256 * sizeof(uint16_t),
+                           cudaMemcpyHostToDevice, s));
+  FIC_CUDA(cudaMemcpyAsync(t.ln, ln.data(), need * sizeof(double), cudaMemcpyHostToDevice, s));
+  // pageable-source copies: the host buffers are staged before the call returns
+  FIC_CUDA(cudaMemcpyAsync(t.w, w.data(), t.J * sizeof(double), cudaMemcpyHostToDevice, s));
+  return t;
+}
+
+// ---------------------------------------------------------------------------
+// planning kernels
+// ---------------------------------------------------------------------------
+__global__ void k_iota(uint32_t* o, int64_t n) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) o[i] = (uint32_t)i;
+}
+
+__global__ void k_bits_to_double(const unsigned long long* k, double* o, int64_t n) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) o[i] = __longlong_as_double((long long)k[i]);
+}
+
+struct ClassifyArgs {
+  const int32_t* lo;
+  const int32_t* hi;
+  int R;
+  int n_iso;
+  int small_pool;
+  int tensor_ok;
+  unsigned long long* key;     // (class << 63) | lo << 32 | hi
+  uint32_t* rid;
+  int64_t* pool_out;           // may be null
+  unsigned long long* pool_sum;
+};
+
+__global__ void k_classify(ClassifyArgs a) {
+  int r = blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long pool = 0;
+  if (r < a.R) {
+    int32_t lo = a.lo[r], hi = a.hi[r];
+    pool = (unsigned long long)(hi - lo);
+    unsigned long long cls = (a.tensor_ok && (int64_t)pool >= a.small_pool) ? 0ull : 1ull;
+    a.key[r] = (cls << 63) | ((unsigned long long)(uint32_t)lo << 32) | (uint32_t)hi;
+    a.rid[r] = r;
+    if (a.pool_out) a.pool_out[r] = (int64_t)pool;
+  }
+  for (int m = 16; m >= 1; m >>= 1) pool += __shfl_xor_sync(0xffffffffu, pool, m);
+  if ((threadIdx.x & 31) == 0 && pool) atomicAdd(a.pool_sum, pool);
+}
+
+__global__ void k_cost(const unsigned long long* key, int R, int n_iso, unsigned long long* cost) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= R) return;
+  unsigned long long k = key[i];
+  unsigned long long pool = (uint32_t)k - (uint32_t)((k >> 32) & 0x7fffffffu);
+  // an exact-path candidate costs ~32x a screened one
+  cost[i] = pool * n_iso * ((k >> 63) ? 32ull : 1ull) + 1ull;
+}
+
+__global__ void k_shard(const unsigned long long* key, const unsigned long long* cum, int R,
+                        int shard, int nshard, PlanCounts* out) {
+  if (threadIdx.x || blockIdx.x) return;
+  // first position with class bit set
+  int lo = 0, hi = R;
+  while (lo < hi) {
+    int m = (lo + hi) >> 1;
+    if ((key[m] >> 63) == 0) lo = m + 1; else hi = m;
+  }
+  out->n_tensor = lo;
+  // shard of position i: floor((cum[i] - 1) * nshard / total)
+  unsigned long long total = R ? cum[R - 1] : 0;
+  auto first_with_shard_ge = [&](int s) {
+    int a = 0, b = R;
+    while (a < b) {
+      int m = (a + b) >> 1;
+      unsigned long long sh = (cum[m] - 1) * (unsigned long long)nshard / total;
+      if ((int)sh < s) a = m + 1; else b = m;
+    }
+    return a;
+  };
+  if (nshard <= 1 || total == 0) {
+    out->shard_begin = 0;
+    out->shard_end = R;
+  } else {
+    out->shard_begin = first_with_shard_ge(shard);
+    out->shard_end = first_with_shard_ge(shard + 1);
+  }
+}
+
+struct TileArgs {
+  const unsigned long long* key;  // sorted
+  const uint32_t* rid;            // sorted
+  int64_t tb, te;                 // tensor positions of this shard
+  int RT;
+  int seg;
+  int32_t* wlo;
+  int32_t* whi;
+  int32_t* nseg;
+  int32_t* nslots;                // [R]
+  int n_iso;
+  unsigned long long* useful;     // sum(pool) * n_iso over tensor ranges
+};
+
+__global__ void k_tiles(TileArgs a) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int64_t b = a.tb + t * a.RT;
+  if (b >= a.te) return;
+  int64_t e = min(a.te, b + a.RT);
+  int32_t lo = (int32_t)((a.key[b] >> 32) & 0x7fffffffu);
+  int32_t hi = 0;
+  for (int64_t i = b; i < e; ++i) hi = max(hi, (int32_t)(uint32_t)a.key[i]);
+  int32_t ns = (int32_t)cdiv(hi - lo, a.seg);
+  a.wlo[t] = lo;
+  a.whi[t] = hi;
+  a.nseg[t] = ns;
+  unsigned long long u = 0;
+  for (int64_t i = b; i < e; ++i) {
+    a.nslots[a.rid[i]] = ns;
+    unsigned long long k = a.key[i];
+    u += (uint32_t)k - (uint32_t)((k >> 32) & 0x7fffffffu);
+  }
+  atomicAdd(a.useful, u * a.n_iso);
+}
+
+__global__ void k_exact_segs(const unsigned long long* key, const uint32_t* rid, int64_t eb,
+                             int64_t ee, int seg, int32_t* nseg, int32_t* nslots) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (eb + i >= ee) return;
+  unsigned long long k = key[eb + i];
+  int32_t pool = (int32_t)((uint32_t)k - (uint32_t)((k >> 32) & 0x7fffffffu));
+  int32_t ns = (int32_t)cdiv(pool, seg);
+  nseg[i] = ns;
+  nslots[rid[eb + i]] = ns;
+}
+
+struct Totals {
+  int64_t n_titems, n_eitems, n_slots;
+};
+
+__global__ void k_totals(const int32_t* tnseg, const int32_t* tbase, int64_t ntt,
+                         const int32_t* enseg, const int32_t* ebase, int64_t ner,
+                         const int32_t* nslots, const int64_t* sbase, int R, Totals* out) {
+  if (threadIdx.x || blockIdx.x) return;
+  out->n_titems = ntt ? (int64_t)tbase[ntt - 1] + tnseg[ntt - 1] : 0;
+  out->n_eitems = ner ? (int64_t)ebase[ner - 1] + enseg[ner - 1] : 0;
+  out->n_slots = R ? sbase[R - 1] + nslots[R - 1] : 0;
+}
+
+__global__ void k_expand(const int32_t* nseg, const int32_t* base, int64_t n, int2* items) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  int32_t b = base[t];
+  for (int s = 0; s < nseg[t]; ++s) items[b + s] = make_int2((int)t, s);
+}
+
+__global__ void k_i32_to_i64(const int32_t* a, int64_t* o, int n) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) o[i] = a[i];
+}
+__global__ void k_u32_to_i64(const uint32_t* a, int64_t* o, int64_t n) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) o[i] = a[i];
+}
+
+// CUB helpers (temp storage from the scratch pool)
+template <class F>
+static void cub_call(Scratch& sc, F f) {
+  size_t bytes = 0;
+  FIC_CUDA(f(nullptr, bytes));
+  void* tmp = sc.get<uint8_t>(bytes);
+  FIC_CUDA(f(tmp, bytes));
+}
+
+// ---------------------------------------------------------------------------
+// pool planning shared by encode and plan
+// ---------------------------------------------------------------------------
+struct PlanBufs {
+  double* fd_dom = nullptr;      // [D] (dynamic/static2)
+  double* fd_rng = nullptr;      // [R]
+  double* keys = nullptr;        // [D] sorted FDs
+  uint32_t* order = nullptr;     // [D] raster id per pool position (nullptr = identity)
+  int32_t* lo = nullptr;
+  int32_t* hi = nullptr;
+  double* scal = nullptr;        // [4]
+};
+
+static PlanBufs make_plan(Scratch& sc, cudaStream_t s, const uint8_t* img, const Geo& g,
+                          const fic_params_t& p) {
+  PlanBufs pb;
+  pb.lo = sc.get<int32_t>(g.R);
+  pb.hi = sc.get<int32_t>(g.R);
+  pb.scal = sc.get<double>(4);
+  FIC_CUDA(cudaMemsetAsync(pb.scal, 0, 4 * sizeof(double), s));
+  SlabArgs sa{};
+  sa.R = g.R;
+  sa.D = g.D;
+  sa.strategy = p.strategy;
+  sa.has_delta = p.has_delta;
+  sa.delta = p.delta;
+  sa.scal = pb.scal;
+  sa.lo = pb.lo;
+  sa.hi = pb.hi;
+  sa.H = g.H;
+  sa.W = g.W;
+  sa.rs = g.rs;
+  sa.ds = g.ds;
+  sa.st = g.st;
+  sa.nrx = g.nrx;
+  sa.ndx = g.ndx;
+  if (p.strategy == FIC_STATIC2 || p.strategy == FIC_DYNAMIC_FD) {
+    // K2: FD of domains (original or decimated blocks) then ranges, in the
+    // reference's order so the same side raises first (codec.py:352-354)
+    int dside = p.fd_source == FIC_FD_ORIGINAL ? g.ds : g.rs;
+    DbcTables td = make_dbc(sc, s, dside, p.h_ln_table, p.ln_len, p.h_fd_weights_dom,
+                            p.n_fd_weights_dom);
+    DbcTables tr = make_dbc(sc, s, g.rs, p.h_ln_table, p.ln_len, p.h_fd_weights_rng,
+                            p.n_fd_weights_rng);
+    pb.fd_dom = sc.get<double>(g.D);
+    pb.fd_rng = sc.get<double>(g.R);
+    unsigned long long* kin = sc.get<unsigned long long>(g.D);
+    unsigned long long* kout = sc.get<unsigned long long>(g.D);
+    uint32_t* iin = sc.get<uint32_t>(g.D);
+    pb.order = sc.get<uint32_t>(g.D);
+    FdArgs fa{};
+    fa.src = img;
+    fa.W = g.W;
+    fa.side = dside;
+    fa.bst = g.st;
+    fa.nbx = g.ndx;
+    fa.n = g.D;
+    fa.mode = p.fd_source == FIC_FD_ORIGINAL ? FD_IMAGE : FD_DECIMATED;
+    fa.clamp = 1;
+    fa.J = td.J;
+    fa.smax = td.smax;
+    fa.quot = td.quot;
+    fa.ln = td.ln;
+    fa.ln_len = td.ln_len;
+    fa.w = td.w;
+    fa.fd = pb.fd_dom;
+    fa.key = kin;
+    launch_fd(fa, s);
+    FdArgs fr = fa;
+    fr.side = g.rs;
+    fr.bst = g.rs;
+    fr.nbx = g.nrx;
+    fr.n = g.R;
+    fr.mode = FD_IMAGE;
+    fr.J = tr.J;
+    fr.smax = tr.smax;
+    fr.quot = tr.quot;
+    fr.ln = tr.ln;
+    fr.ln_len = tr.ln_len;
+    fr.w = tr.w;
+    fr.fd = pb.fd_rng;
+    fr.key = nullptr;
+    launch_fd(fr, s);
+    // K3: stable sort of domains by FD (== AvlTree flatten, avltree.py:150-189)
+    k_iota<<<(unsigned)cdiv(g.D, 256), 256, 0, s>>>(iin, g.D);
+    FIC_CHECK_LAUNCH();
+    int nbits = 64;
+    cub_call(sc, [&](void* t, size_t& b) {
+      return cub::DeviceRadixSort::SortPairs(t, b, kin, kout, iin, pb.order, (int64_t)g.D, 0,
+                                             nbits, s);
+    });
+    pb.keys = sc.get<double>(g.D);
+    k_bits_to_double<<<(unsigned)cdiv(g.D, 256), 256, 0, s>>>(kout, pb.keys, g.D);
+    FIC_CHECK_LAUNCH();
+    sa.keys = pb.keys;
+    sa.ids = pb.order;
+    sa.fd_rng = pb.fd_rng;
+  }
+  launch_slabs(sa, s);
+  return pb;
+}
+
+static cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+template <class F>
+static int guarded(F f) {
+  try {
+    f();
+    return FIC_OK;
+  } catch (const Error& e) {
+    set_error(e.msg);
+    return e.code;
+  } catch (const std::exception& e) {
+    set_error(e.what());
+    return FIC_ECUDA;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// encode
+// ---------------------------------------------------------------------------
+static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p, uint8_t* records,
+                        double* pre_rms, double* post_rms, int64_t* pool_sizes,
+                        fic_stats_t* st, cudaStream_t s) {
+  Geo g = validate(H, W, p);
+  if (p.strategy == FIC_STATIC2 || p.strategy == FIC_DYNAMIC_FD) {
+    check_dbc_side(p.fd_source == FIC_FD_ORIGINAL ? g.ds : g.rs);
+    check_dbc_side(g.rs);
+  }
+  if (g.npx % 4) invalid("range_size must be even on the GPU path");
+  const int K = g.npx;
+  const int nshard = std::max(1, p.shard_count);
+  const int shard = std::min(std::max(0, p.shard_index), nshard - 1);
+  const bool tensor_ok = (p.matcher != FIC_MATCH_EXACT) && tc_supported(K);
+  const int small_pool = p.small_pool > 0 ? p.small_pool : 256;
+  const int seg_t = p.max_segment > 0 ? (int)align_up(p.max_segment, 256) : 65536;
+  const int seg_e = 4096;
+  const int RT = 128 / g.n_iso;
+
+  g_launches = 0;
+  Scratch sc(s);
+  Timer tm(s);
+  tm.mark();  // 0
+  PlanBufs pb = make_plan(sc, s, img, g, p);
+  tm.mark();  // 1
+
+  // K1 pool builder
+  PoolArgs pa{};
+  pa.img = img;
+  pa.W = g.W;
+  pa.rs = g.rs;
+  pa.st = g.st;
+  pa.ndx = g.ndx;
+  pa.D = g.D;
+  pa.order = pb.order;
+  pa.raw = sc.get<uint8_t>((size_t)g.D * K);
+  pa.bh = tensor_ok ? sc.get<uint16_t>((size_t)g.D * K) : nullptr;
+  pa.inv_den = sc.get<double>(g.D);
+  pa.sums = sc.get<uint2>(g.D);
+  pa.ids = sc.get<uint32_t>(g.D);
+  launch_pool(pa, s);
+  tm.mark();  // 2
+
+  // ranges
+  std::vector<int> perm(8 * K), inv(8 * K);
+  iso_tables(g.rs, perm.data(), inv.data());
+  int* d_inv = sc.get<int>(8 * K);
+  FIC_CUDA(cudaMemcpyAsync(d_inv, inv.data(), 8 * K * sizeof(int), cudaMemcpyHostToDevice, s));
+  RangeArgs ra{};
+  ra.img = img;
+  ra.W = g.W;
+  ra.rs = g.rs;
+  ra.nrx = g.nrx;
+  ra.R = g.R;
+  ra.n_iso = g.n_iso;
+  ra.inv_perm = d_inv;
+  ra.info = sc.get<RangeInfo>(g.R);
+  ra.rows = sc.get<uint8_t>((size_t)g.R * g.n_iso * K);
+  launch_ranges(ra, s);
+
+  // plan: classify, sort by (class, lo, hi), shard by cost
+  unsigned long long* counters = sc.get<unsigned long long>(4);
+  FIC_CUDA(cudaMemsetAsync(counters, 0, 4 * sizeof(unsigned long long), s));
+  unsigned long long* key = sc.get<unsigned long long>(g.R);
+  unsigned long long* key_s = sc.get<unsigned long long>(g.R);
+  uint32_t* rid = sc.get<uint32_t>(g.R);
+  uint32_t* rid_s = sc.get<uint32_t>(g.R);
+  ClassifyArgs ca{pb.lo, pb.hi, g.R, g.n_iso, small_pool, tensor_ok ? 1 : 0, key, rid,
+                  pool_sizes, counters + 2};
+  k_classify<<<(unsigned)cdiv(g.R, 256), 256, 0, s>>>(ca);
+  FIC_CHECK_LAUNCH();
+  cub_call(sc, [&](void* t, size_t& b) {
+    return cub::DeviceRadixSort::SortPairs(t, b, key, key_s, rid, rid_s, g.R, 0, 64, s);
+  });
+  unsigned long long* cost = sc.get<unsigned long long>(g.R);
+  unsigned long long* cum = sc.get<unsigned long long>(g.R);
+  k_cost<<<(unsigned)cdiv(g.R, 256), 256, 0, s>>>(key_s, g.R, g.n_iso, cost);
+  FIC_CHECK_LAUNCH();
+  cub_call(sc, [&](void* t, size_t& b) {
+    return cub::DeviceScan::InclusiveSum(t, b, cost, cum, g.R, s);
+  });
+  PlanCounts* d_pc = sc.get<PlanCounts>(1);
+  k_shard<<<1, 32, 0, s>>>(key_s, cum, g.R, shard, nshard, d_pc);
+  FIC_CHECK_LAUNCH();
+  PlanCounts pc;
+  FIC_CUDA(cudaMemcpyAsync(&pc, d_pc, sizeof(pc), cudaMemcpyDeviceToHost, s));
+  FIC_CUDA(cudaStreamSynchronize(s));
+
+  const int64_t tb = pc.shard_begin, te = std::min(pc.shard_end, pc.n_tensor);
+  const int64_t eb = std::max(pc.shard_begin, pc.n_tensor), ee = pc.shard_end;
+  const int64_t n_tr = std::max<int64_t>(0, te - tb);
+  const int64_t n_er = std::max<int64_t>(0, ee - eb);
+  const int64_t n_tt = cdiv(n_tr, RT);
+
+  int32_t* nslots = sc.get<int32_t>(g.R);
+  FIC_CUDA(cudaMemsetAsync(nslots, 0, g.R * sizeof(int32_t), s));
+  int32_t* wlo = sc.get<int32_t>(n_tt);
+  int32_t* whi = sc.get<int32_t>(n_tt);
+  int32_t* tnseg = sc.get<int32_t>(n_tt);
+  int32_t* tbase = sc.get<int32_t>(n_tt);
+  int32_t* enseg = sc.get<int32_t>(n_er);
+  int32_t* ebase = sc.get<int32_t>(n_er);
+  int64_t* sbase = sc.get<int64_t>(g.R);
+  if (n_tt) {
+    TileArgs ta{key_s, rid_s, tb, te, RT, seg_t, wlo, whi, tnseg, nslots, g.n_iso, counters + 3};
+    k_tiles<<<(unsigned)cdiv(n_tt, 128), 128, 0, s>>>(ta);
+    FIC_CHECK_LAUNCH();
+    cub_call(sc, [&](void* t, size_t& b) {
+      return cub::DeviceScan::ExclusiveSum(t, b, tnseg, tbase, (int)n_tt, s);
+    });
+  }
+  if (n_er) {
+    k_exact_segs<<<(unsigned)cdiv(n_er, 256), 256, 0, s>>>(key_s, rid_s, eb, ee, seg_e, enseg,
+                                                            nslots);
+    FIC_CHECK_LAUNCH();
+    cub_call(sc, [&](void* t, size_t& b) {
+      return cub::DeviceScan::ExclusiveSum(t, b, enseg, ebase, (int)n_er, s);
+    });
+  }
+  {
+    // slot bases over raster ranges (int64 accumulation)
+    int64_t* ns64 = sc.get<int64_t>(g.R);
+    k_i32_to_i64<<<(unsigned)cdiv(g.R, 256), 256, 0, s>>>(nslots, ns64, g.R);
+    FIC_CHECK_LAUNCH();
+    cub_call(sc, [&](void* t, size_t& b) {
+      return cub::DeviceScan::ExclusiveSum(t, b, ns64, sbase, g.R, s);
+    });
+  }
+  Totals* d_tot = sc.get<Totals>(1);
+  k_totals<<<1, 32, 0, s>>>(tnseg, tbase, n_tt, enseg, ebase, n_er, nslots, sbase, g.R, d_tot);
+  FIC_CHECK_LAUNCH();
+  Totals tot;
+  FIC_CUDA(cudaMemcpyAsync(&tot, d_tot, sizeof(tot), cudaMemcpyDeviceToHost, s));
+  FIC_CUDA(cudaStreamSynchronize(s));
+
+  int2* titems = sc.get<int2>(tot.n_titems);
+  int2* eitems = sc.get<int2>(tot.n_eitems);
+  Partial* partials = sc.get<Partial>(tot.n_slots);
+  if (n_tt) {
+    k_expand<<<(unsigned)cdiv(n_tt, 128), 128, 0, s>>>(tnseg, tbase, n_tt, titems);
+    FIC_CHECK_LAUNCH();
+  }
+  if (n_er) {
+    k_expand<<<(unsigned)cdiv(n_er, 128), 128, 0, s>>>(enseg, ebase, n_er, eitems);
+    FIC_CHECK_LAUNCH();
+  }
+
+  PoolView P{pa.raw, pa.bh, pa.inv_den, pa.sums, pa.ids, g.D};
+  RangeView Rv{ra.info, ra.rows, pb.lo, pb.hi, g.n_iso, K};
+  tm.mark();  // 3
+  if (tot.n_titems) {
+    TcArgs ta{titems, tot.n_titems, rid_s + tb, n_tr, wlo, whi, seg_t, RT, sbase, partials,
+              counters};
+    launch_tc(P, Rv, ta, s);
+  }
+  tm.mark();  // 4
+  if (tot.n_eitems) {
+    ExactArgs ea{eitems, tot.n_eitems, rid_s + eb, seg_e, sbase, partials, counters};
+    launch_exact(P, Rv, ea, s);
+  }
+  tm.mark();  // 5
+  MergeArgs ma{g.R, sbase, nslots, partials, records, pre_rms, post_rms, (double)K};
+  launch_merge(ma, s);
+  tm.mark();  // 6
+
+  unsigned long long hc[4];
+  double hs[4];
+  FIC_CUDA(cudaMemcpyAsync(hc, counters, sizeof(hc), cudaMemcpyDeviceToHost, s));
+  FIC_CUDA(cudaMemcpyAsync(hs, pb.scal, sizeof(hs), cudaMemcpyDeviceToHost, s));
+  tm.mark();  // 7
+  FIC_CUDA(cudaStreamSynchronize(s));
+  if (st) {
+    std::memset(st, 0, sizeof(*st));
+    st->n_ranges = g.R;
+    st->n_domains = g.D;
+    st->comparisons = (int64_t)hc[2] * g.n_iso;
+    st->mean_pool_size = (double)hc[2] / (double)g.R;
+    st->fd_min = hs[0];
+    st->fd_max = hs[1];
+    st->half_width = p.strategy == FIC_DYNAMIC_FD ? hs[2] : 0.0;
+    st->ms_fd = tm.ms(0, 1);
+    st->ms_pool = tm.ms(1, 2);
+    st->ms_match = tm.ms(3, 6);
+    st->ms_tensor = tm.ms(3, 4);
+    st->ms_exact = tm.ms(4, 5);
+    st->ms_total = tm.ms(0, 7);
+    st->exact_evals = (int64_t)hc[0];
+    st->tensor_candidates = (int64_t)hc[1];
+    st->tensor_comparisons = (int64_t)hc[3];
+    st->tensor_tiles = (int32_t)n_tt;
+    st->exact_tiles = (int32_t)n_er;
+    st->work_items = (int32_t)(tot.n_titems + tot.n_eitems);
+    st->kernel_launches = g_launches;
+  }
+}
+
+static void plan_impl(const uint8_t* img, int H, int W, const fic_params_t& p, double* fd_dom,
+                      double* fd_rng, int64_t* order, int64_t* slab_lo, int64_t* slab_hi,
+                      fic_stats_t* st, cudaStream_t s) {
+  Geo g = validate(H, W, p);
+  if (p.strategy == FIC_STATIC2 || p.strategy == FIC_DYNAMIC_FD) {
+    check_dbc_side(p.fd_source == FIC_FD_ORIGINAL ? g.ds : g.rs);
+    check_dbc_side(g.rs);
+  }
+  Scratch sc(s);
+  PlanBufs pb = make_plan(sc, s, img, g, p);
+  if (fd_dom && pb.fd_dom)
+    FIC_CUDA(cudaMemcpyAsync(fd_dom, pb.fd_dom, g.D * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  if (fd_rng && pb.fd_rng)
+    FIC_CUDA(cudaMemcpyAsync(fd_rng, pb.fd_rng, g.R * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  if (order) {
+    if (pb.order) {
+      k_u32_to_i64<<<(unsigned)cdiv(g.D, 256), 256, 0, s>>>(pb.order, order, g.D);
+    } else {
+      uint32_t* io = sc.get<uint32_t>(g.D);
+      k_iota<<<(unsigned)cdiv(g.D, 256), 256, 0, s>>>(io, g.D);
+      k_u32_to_i64<<<(unsigned)cdiv(g.D, 256), 256, 0, s>>>(io, order, g.D);
+    }
+    FIC_CHECK_LAUNCH();
+  }
+  if (slab_lo) k_i32_to_i64<<<(unsigned)cdiv(g.R, 256), 256, 0, s>>>(pb.lo, slab_lo, g.R);
+  if (slab_hi) k_i32_to_i64<<<(unsigned)cdiv(g.R, 256), 256, 0, s>>>(pb.hi, slab_hi, g.R);
+  FIC_CHECK_LAUNCH();
+  double hs[4];
+  FIC_CUDA(cudaMemcpyAsync(hs, pb.scal, sizeof(hs), cudaMemcpyDeviceToHost, s));
+  FIC_CUDA(cudaStreamSynchronize(s));
+  if (st) {
+    std::memset(st, 0, sizeof(*st));
+    st->n_ranges = g.R;
+    st->n_domains = g.D;
+    st->fd_min = hs[0];
+    st->fd_max = hs[1];
+    st->half_width = p.strategy == FIC_DYNAMIC_FD ? hs[2] : 0.0;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// decode (codec.py:534-598): gather 2x2 means, isometry, s*x + o, clip,
+// scatter; the work image stays float64, rint -> uint8 at the end.
+// ---------------------------------------------------------------------------
+struct DecArgs {
+  const uint8_t* rec;
+  int W, rs, st, ndx, nrx, R;
+  const int* perm;  // [8][K]
+  double* src;
+  double* dst;
+};
+
+__global__ void k_decode(DecArgs a) {
+  int K = a.rs * a.rs;
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)a.R * K) return;
+  int r = (int)(t / K), k = (int)(t - (int64_t)r * K);
+  const uint8_t* rc = a.rec + (int64_t)r * 7;
+  uint32_t dom = rc[0] | (rc[1] << 8) | (rc[2] << 16) | ((uint32_t)rc[3] << 24);
+  int iso = rc[4];
+  double s_hat = __dsub_rn(__dmul_rn((double)rc[5], 2.0 / 31.0), 1.0);
+  double o_hat = __dsub_rn(__dmul_rn((double)rc[6], 510.0 / 127.0), 255.0);
+  int m = a.perm[iso * K + k];  // domains[rows][:, perms[iso]]
+  int u = m / a.rs, v = m - u * a.rs;
+  int64_t y = (int64_t)(dom / a.ndx) * a.st + 2 * u;
+  int64_t x = (int64_t)(dom % a.ndx) * a.st + 2 * v;
+  int64_t gi = y * a.W + x;
+  double sum = __dadd_rn(__dadd_rn(__dadd_rn(a.src[gi], a.src[gi + 1]), a.src[gi + a.W]),
+                         a.src[gi + a.W + 1]);
+  double d = __dmul_rn(0.25, sum);
+  double val = __dadd_rn(__dmul_rn(s_hat, d), o_hat);
+  val = fmin(fmax(val, 0.0), 255.0);
+  int ry = r / a.nrx, rx = r - ry * a.nrx;
+  int64_t oy = (int64_t)ry * a.rs + k / a.rs, ox = (int64_t)rx * a.rs + k % a.rs;
+  a.dst[oy * a.W + ox] = val;
+}
+
+__global__ void k_fill(double* w, int64_t n, double v, const uint8_t* init) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) w[i] = init ? (double)init[i] : v;
+}
+
+__global__ void k_round(const double* w, uint8_t* out, int64_t n) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = (uint8_t)rint(w[i]);
+}
+
+static void decode_impl(const uint8_t* rec, int H, int W, int rs, int ds, int st, int iters,
+                        double initial, const uint8_t* init_img, uint8_t* out, cudaStream_t s) {
+  if (iters < 1) invalid("iterations must be >= 1");
+  if (rs <= 0 || H % rs || W % rs)
+    invalid("image " + std::to_string(W) + "x" + std::to_string(H) +
+            " not divisible by range size " + std::to_string(rs));
+  if (st < 1) invalid("stride must be >= 1");
+  if (ds > std::min(W, H))
+    invalid("domain size " + std::to_string(ds) + " exceeds image " + std::to_string(W) + "x" +
+            std::to_string(H));
+  int K = rs * rs;
+  Scratch sc(s);
+  std::vector<int> perm(8 * K), inv(8 * K);
+  iso_tables(rs, perm.data(), inv.data());
+  int* d_perm = sc.get<int>(8 * K);
+  FIC_CUDA(cudaMemcpyAsync(d_perm, perm.data(), 8 * K * sizeof(int), cudaMemcpyHostToDevice, s));
+  int64_t n = (int64_t)H * W;
+  double* w0 = sc.get<double>(n);
+  double* w1 = sc.get<double>(n);
+  k_fill<<<(unsigned)cdiv(n, 256), 256, 0, s>>>(w0, n, initial, init_img);
+  FIC_CHECK_LAUNCH();
+  DecArgs a{rec, W, rs, st, (W - ds) / st + 1, W / rs, (W / rs) * (H / rs), d_perm, w0, w1};
+  for (int i = 0; i < iters; ++i) {
+    k_decode<<<(unsigned)cdiv(n, 256), 256, 0, s>>>(a);
+    FIC_CHECK_LAUNCH();
+    std::swap(a.src, a.dst);
+  }
+  k_round<<<(unsigned)cdiv(n, 256), 256, 0, s>>>(a.src, out, n);
+  FIC_CHECK_LAUNCH();
+  FIC_CUDA(cudaStreamSynchronize(s));
+}
+
+}  // namespace fic
+
+// ===========================================================================
+// extern "C"
+// ===========================================================================
+using namespace fic;
+
+extern "C" int fic_encode_v1(const uint8_t* d_image, int32_t height, int32_t width,
+                             const fic_params_t* params, uint8_t* d_records, double* d_pre_rms,
+                             double* d_post_rms, int64_t* d_pool_sizes, fic_stats_t* h_stats,
+                             void* stream) {
+  return guarded([&] {
+    if (!params) invalid("params must not be NULL");
+    encode_impl(d_image, height, width, *params, d_records, d_pre_rms, d_post_rms, d_pool_sizes,
+                h_stats, as_stream(stream));
+  });
+}
+
+extern "C" int fic_plan_v1(const uint8_t* d_image, int32_t height, int32_t width,
+                           const fic_params_t* params, double* d_fd_dom, double* d_fd_rng,
+                           int64_t* d_order, int64_t* d_slab_lo, int64_t* d_slab_hi,
+                           fic_stats_t* h_stats, void* stream) {
+  return guarded([&] {
+    if (!params) invalid("params must not be NULL");
+    plan_impl(d_image, height, width, *params, d_fd_dom, d_fd_rng, d_order, d_slab_lo, d_slab_hi,
+              h_stats, as_stream(stream));
+  });
+}
+
+extern "C" int fic_dbc_v1(const uint8_t* d_blocks, int64_t n, int32_t side, int32_t clamp,
+                          const double* h_ln_table, int32_t ln_len, const double* h_weights,
+                          int32_t n_weights, double* d_fd, void* stream) {
+  return guarded([&] {
+    cudaStream_t s = as_stream(stream);
+    Scratch sc(s);
+    DbcTables t = make_dbc(sc, s, side, h_ln_table, ln_len, h_weights, n_weights);
+    FdArgs fa{};
+    fa.src = d_blocks;
+    fa.side = side;
+    fa.n = n;
+    fa.mode = FD_STACK;
+    fa.clamp = clamp;
+    fa.J = t.J;
+    fa.smax = t.smax;
+    fa.quot = t.quot;
+    fa.ln = t.ln;
+    fa.ln_len = t.ln_len;
+    fa.w = t.w;
+    fa.fd = d_fd;
+    launch_fd(fa, s);
+    FIC_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+extern "C" int fic_decode_v1(const uint8_t* d_records, int32_t height, int32_t width,
+                             int32_t range_size, int32_t domain_size, int32_t stride,
+                             int32_t iterations, double initial, const uint8_t* d_initial,
+                             uint8_t* d_out, void* stream) {
+  return guarded([&] {
+    decode_impl(d_records, height, width, range_size, domain_size, stride, iterations, initial,
+                d_initial, d_out, as_stream(stream));
+  });
+}
+
+extern "C" const char* fic_last_error(void) { return fic::last_error(); }
+extern "C" int fic_abi_version(void) { return FIC_ABI_VERSION; }
+extern "C" void fic_release(void) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    cudaDeviceSynchronize();
+    cudaMemPoolTrimTo(pool, 0);
+  }
+}

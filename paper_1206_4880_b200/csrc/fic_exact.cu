@@ -1,0 +1,239 @@
+// Exact CUDA-core matcher (K5 on whole slabs) and the partial merge (K6).
+//
+// Every candidate (range, domain, isometry) of a work item is evaluated with
+// the reference's fp64 op sequence (codec.py:218-242, see eval_candidate):
+// the cross term is an exact integer dot product (u8 x u8 via dp4a), every
+// fp64 op is an explicit round-to-nearest intrinsic (no FMA), so results are
+// bit-identical to numpy's.  Used for small pools (fallback ranges, nosearch)
+// and as the device-side oracle (FIC_MATCH_EXACT).
+#include "match.h"
+
+namespace fic {
+
+struct Best {
+  double err, pre;
+  uint32_t dom;
+  int iso, sq, oq;
+};
+
+__device__ __forceinline__ void best_init(Best& b) {
+  b.err = INFINITY;
+  b.pre = INFINITY;
+  b.dom = 0xffffffffu;
+  b.iso = 0;
+  b.sq = 0;
+  b.oq = 0;
+}
+
+__device__ __forceinline__ void best_merge(Best& a, const Best& b) {
+  if (better(b.err, b.dom, b.iso, a.err, a.dom, a.iso)) {
+    a.err = b.err;
+    a.dom = b.dom;
+    a.iso = b.iso;
+    a.sq = b.sq;
+    a.oq = b.oq;
+  }
+  a.pre = fmin(a.pre, b.pre);
+}
+
+__device__ __forceinline__ Best shfl_best(const Best& b, int lane_mask) {
+  Best o;
+  o.err = __shfl_xor_sync(0xffffffffu, b.err, lane_mask);
+  o.pre = __shfl_xor_sync(0xffffffffu, b.pre, lane_mask);
+  o.dom = __shfl_xor_sync(0xffffffffu, b.dom, lane_mask);
+  o.iso = __shfl_xor_sync(0xffffffffu, b.iso, lane_mask);
+  o.sq = __shfl_xor_sync(0xffffffffu, b.sq, lane_mask);
+  o.oq = __shfl_xor_sync(0xffffffffu, b.oq, lane_mask);
+  return o;
+}
+
+template <int K>
+__global__ void __launch_bounds__(256) k_exact(PoolView P, RangeView Rv, ExactArgs a) {
+  constexpr int KW = K / 4;  // 32-bit words per row
+  __shared__ uint32_t srow[8][KW];
+  __shared__ Best sbest[8];
+  int64_t it = blockIdx.x;
+  if (it >= a.n_items) return;
+  int2 item = a.items[it];
+  uint32_t r = a.elist[item.x];
+  int64_t lo = Rv.lo[r], hi = Rv.hi[r];
+  int64_t c0 = lo + (int64_t)item.y * a.seg_len;
+  int64_t c1 = min(hi, c0 + a.seg_len);
+  const int n_iso = Rv.n_iso;
+  const uint32_t* rw = reinterpret_cast<const uint32_t*>(Rv.rows + (int64_t)r * n_iso * K);
+  for (int i = threadIdx.x; i < n_iso * KW; i += blockDim.x) srow[i / KW][i % KW] = rw[i];
+  __syncthreads();
+  const RangeInfo inf = Rv.info[r];
+  const double n = (double)K;
+  Best b;
+  best_init(b);
+  unsigned long long evals = 0;
+  for (int64_t p = c0 + threadIdx.x; p < c1; p += blockDim.x) {
+    uint32_t dw[KW];
+    const uint4* src = reinterpret_cast<const uint4*>(P.raw + p * K);
+#pragma unroll
+    for (int q = 0; q < KW / 4; ++q) {
+      uint4 v = __ldg(src + q);
+      dw[4 * q] = v.x;
+      dw[4 * q + 1] = v.y;
+      dw[4 * q + 2] = v.z;
+      dw[4 * q + 3] = v.w;
+    }
+    uint2 sm = P.sums[p];
+    double sd = (double)sm.x, sdd = (double)sm.y, inv = P.inv_den[p];
+    uint32_t dom = P.ids[p];
+    for (int i = 0; i < n_iso; ++i) {
+      uint32_t acc = 0;
+#pragma unroll
+      for (int q = 0; q < KW; ++q) acc = __dp4a(dw[q], srow[i][q], acc);
+      Cand c = eval_candidate((double)acc, sd, sdd, inv, inf.sr, inf.srr, n);
+      b.pre = fmin(b.pre, c.pre);
+      if (better(c.err, dom, i, b.err, b.dom, b.iso)) {
+        b.err = c.err;
+        b.dom = dom;
+        b.iso = i;
+        b.sq = c.sq;
+        b.oq = c.oq;
+      }
+    }
+    evals += n_iso;
+  }
+#pragma unroll
+  for (int m = 16; m >= 1; m >>= 1) best_merge(b, shfl_best(b, m));
+  int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) sbest[warp] = b;
+  for (int m = 16; m >= 1; m >>= 1) evals += __shfl_xor_sync(0xffffffffu, evals, m);
+  if (lane == 0 && evals) atomicAdd(a.counters, evals);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    Best t = sbest[0];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) best_merge(t, sbest[w]);
+    Partial out;
+    out.err = t.err;
+    out.pre = t.pre;
+    out.dom = t.dom;
+    out.iso = (uint8_t)t.iso;
+    out.sq = (uint8_t)t.sq;
+    out.oq = (uint8_t)t.oq;
+    out.valid = (c1 > c0) ? 1 : 0;
+    a.partials[a.slot_base[r] + item.y] = out;
+  }
+}
+
+// Generic K (any range size whose K is a multiple of 4, K <= 1024).
+__global__ void __launch_bounds__(256) k_exact_generic(PoolView P, RangeView Rv, ExactArgs a) {
+  extern __shared__ uint32_t dyn[];
+  __shared__ Best sbest[8];
+  const int K = Rv.K, KW = K / 4;
+  int64_t it = blockIdx.x;
+  if (it >= a.n_items) return;
+  int2 item = a.items[it];
+  uint32_t r = a.elist[item.x];
+  int64_t lo = Rv.lo[r], hi = Rv.hi[r];
+  int64_t c0 = lo + (int64_t)item.y * a.seg_len;
+  int64_t c1 = min(hi, c0 + a.seg_len);
+  const int n_iso = Rv.n_iso;
+  const uint32_t* rw = reinterpret_cast<const uint32_t*>(Rv.rows + (int64_t)r * n_iso * K);
+  for (int i = threadIdx.x; i < n_iso * KW; i += blockDim.x) dyn[i] = rw[i];
+  __syncthreads();
+  const RangeInfo inf = Rv.info[r];
+  const double n = (double)K;
+  Best b;
+  best_init(b);
+  unsigned long long evals = 0;
+  for (int64_t p = c0 + threadIdx.x; p < c1; p += blockDim.x) {
+    const uint32_t* dw = reinterpret_cast<const uint32_t*>(P.raw + p * K);
+    uint2 sm = P.sums[p];
+    double sd = (double)sm.x, sdd = (double)sm.y, inv = P.inv_den[p];
+    uint32_t dom = P.ids[p];
+    for (int i = 0; i < n_iso; ++i) {
+      uint32_t acc = 0;
+      for (int q = 0; q < KW; ++q) acc = __dp4a(__ldg(dw + q), dyn[i * KW + q], acc);
+      Cand c = eval_candidate((double)acc, sd, sdd, inv, inf.sr, inf.srr, n);
+      b.pre = fmin(b.pre, c.pre);
+      if (better(c.err, dom, i, b.err, b.dom, b.iso)) {
+        b.err = c.err;
+        b.dom = dom;
+        b.iso = i;
+        b.sq = c.sq;
+        b.oq = c.oq;
+      }
+    }
+    evals += n_iso;
+  }
+  for (int m = 16; m >= 1; m >>= 1) best_merge(b, shfl_best(b, m));
+  int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) sbest[warp] = b;
+  for (int m = 16; m >= 1; m >>= 1) evals += __shfl_xor_sync(0xffffffffu, evals, m);
+  if (lane == 0 && evals) atomicAdd(a.counters, evals);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    Best t = sbest[0];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) best_merge(t, sbest[w]);
+    Partial out;
+    out.err = t.err;
+    out.pre = t.pre;
+    out.dom = t.dom;
+    out.iso = (uint8_t)t.iso;
+    out.sq = (uint8_t)t.sq;
+    out.oq = (uint8_t)t.oq;
+    out.valid = (c1 > c0) ? 1 : 0;
+    a.partials[a.slot_base[r] + item.y] = out;
+  }
+}
+
+void launch_exact(const PoolView& P, const RangeView& Rv, const ExactArgs& a, cudaStream_t s) {
+  if (a.n_items == 0) return;
+  if (Rv.K % 4) invalid("range_size * range_size must be a multiple of 4 on the GPU path");
+  unsigned grid = (unsigned)a.n_items;
+  if (Rv.K == 64)
+    k_exact<64><<<grid, 256, 0, s>>>(P, Rv, a);
+  else if (Rv.K == 16)
+    k_exact<16><<<grid, 256, 0, s>>>(P, Rv, a);
+  else
+    k_exact_generic<<<grid, 256, (size_t)Rv.n_iso * Rv.K, s>>>(P, Rv, a);
+  FIC_CHECK_LAUNCH();
+}
+
+// K6: merge partials (per range) into the raster-order outputs.
+__global__ void k_merge(MergeArgs a) {
+  int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= a.R) return;
+  int ns = a.nslots[r];
+  if (ns == 0) return;
+  const Partial* p = a.partials + a.slot_base[r];
+  double err = INFINITY, pre = INFINITY;
+  uint32_t dom = 0xffffffffu;
+  int iso = 0, sq = 0, oq = 0;
+  for (int i = 0; i < ns; ++i) {
+    Partial q = p[i];
+    if (!q.valid) continue;
+    pre = fmin(pre, q.pre);
+    if (better(q.err, q.dom, q.iso, err, dom, iso)) {
+      err = q.err;
+      dom = q.dom;
+      iso = q.iso;
+      sq = q.sq;
+      oq = q.oq;
+    }
+  }
+  uint8_t* rec = a.records + (int64_t)r * 7;
+  rec[0] = dom & 255;
+  rec[1] = (dom >> 8) & 255;
+  rec[2] = (dom >> 16) & 255;
+  rec[3] = dom >> 24;
+  rec[4] = (uint8_t)iso;
+  rec[5] = (uint8_t)sq;
+  rec[6] = (uint8_t)oq;
+  // codec.py:263-264
+  a.post_rms[r] = __dsqrt_rn(__ddiv_rn(fmax(err, 0.0), a.n));
+  a.pre_rms[r] = __dsqrt_rn(__ddiv_rn(fmax(pre, 0.0), a.n));
+}
+
+void launch_merge(const MergeArgs& a, cudaStream_t s) {
+  if (a.R == 0) return;
+  k_merge<<<(unsigned)cdiv(a.R, 256), 256, 0, s>>>(a);
+  FIC_CHECK_LAUNCH();
+}
+
+}  // namespace fic

@@ -1,0 +1,434 @@
+// Setup kernels of the encoder hot path: FD (K2), slabs (K3), pool builder
+// (K1), range preparation.  sm_100a.  See DESIGN.md §Kernels.
+#include <cuda_fp16.h>
+#include <math.h>
+
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "kernels.h"
+
+namespace fic {
+
+// ============================================================================
+// K2 — differential box counting, one thread per block.
+// fdim.py:44-80: per scale s (consecutive powers of two up to smax), cell
+// max/min, count = sum(floor(max/h) - floor(min/h)) + k^2, FD = sum_j
+// ln(count_j) * w_j accumulated left to right (numpy's sum over <8 terms),
+// clamped to [2, 3].  floor(v/h) comes from a host table built with the same
+// fp64 division numpy performs, so any block side is bit-exact.
+// ============================================================================
+
+int dbc_tables(int side, uint16_t* quot, int* smax, int* ln_needed) {
+  std::vector<int> scales;
+  for (int s = 2; s <= side / 2; s *= 2)
+    if (side % s == 0) scales.push_back(s);
+  int J = (int)scales.size();
+  if (J < 2) return J;
+  if (J > 7) invalid("block side too large for the DBC kernel (max 7 scales)");
+  int need = 0;
+  for (int j = 0; j < J; ++j) {
+    double h = (double)(scales[j] * 256) / (double)side;  // fdim.py:74
+    for (int v = 0; v < 256; ++v) quot[j * 256 + v] = (uint16_t)std::floor((double)v / h);
+    int k = side / scales[j];
+    need = std::max(need, k * k * (quot[j * 256 + 255] - quot[j * 256 + 0]) + k * k);
+  }
+  *smax = scales.back();
+  *ln_needed = need + 1;
+  return J;
+}
+
+struct PixSrc {
+  const uint8_t* p;
+  int W, side, mode;
+  __device__ __forceinline__ int operator()(int y0, int x0, int64_t b, int yy, int xx) const {
+    if (mode == FD_IMAGE) return p[(int64_t)(y0 + yy) * W + x0 + xx];
+    if (mode == FD_STACK) return p[b * side * side + yy * side + xx];
+    const uint8_t* q = p + (int64_t)(y0 + 2 * yy) * W + x0 + 2 * xx;  // blocks.py:75-82
+    return (q[0] + q[1] + q[W] + q[W + 1]) >> 2;
+  }
+};
+
+template <int SMAX>
+__global__ void __launch_bounds__(256) k_fd(FdArgs a) {
+  constexpr int J = (SMAX == 4) ? 2 : (SMAX == 8) ? 3 : 0;
+  __shared__ uint16_t quot[J][256];
+  for (int i = threadIdx.x; i < J * 256; i += blockDim.x) quot[i >> 8][i & 255] = a.quot[i];
+  __syncthreads();
+  int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= a.n) return;
+  int y0 = 0, x0 = 0;
+  if (a.mode != FD_STACK) {
+    int64_t by = b / a.nbx, bx = b - by * a.nbx;
+    y0 = (int)by * a.bst;
+    x0 = (int)bx * a.bst;
+  }
+  PixSrc px{a.src, a.W, a.side, a.mode};
+  int cnt[J];
+#pragma unroll
+  for (int j = 0; j < J; ++j) cnt[j] = 0;
+  const int ncell = a.side / SMAX;
+  for (int cy = 0; cy < ncell; ++cy) {
+    for (int cx = 0; cx < ncell; ++cx) {
+      constexpr int L = SMAX / 2;
+      int mx[L][L], mn[L][L];
+#pragma unroll
+      for (int i = 0; i < L; ++i) {
+#pragma unroll
+        for (int j = 0; j < L; ++j) {
+          int yy = cy * SMAX + 2 * i, xx = cx * SMAX + 2 * j;
+          int p0 = px(y0, x0, b, yy, xx), p1 = px(y0, x0, b, yy, xx + 1);
+          int p2 = px(y0, x0, b, yy + 1, xx), p3 = px(y0, x0, b, yy + 1, xx + 1);
+          mx[i][j] = max(max(p0, p1), max(p2, p3));
+          mn[i][j] = min(min(p0, p1), min(p2, p3));
+          cnt[0] += quot[0][mx[i][j]] - quot[0][mn[i][j]];
+        }
+      }
+#pragma unroll
+      for (int lev = 1; lev < J; ++lev) {
+        const int n = L >> lev;  // cells per side at this level
+#pragma unroll
+        for (int i = 0; i < n; ++i) {
+#pragma unroll
+          for (int j = 0; j < n; ++j) {
+            int a0 = max(max(mx[2 * i][2 * j], mx[2 * i][2 * j + 1]),
+                         max(mx[2 * i + 1][2 * j], mx[2 * i + 1][2 * j + 1]));
+            int b0 = min(min(mn[2 * i][2 * j], mn[2 * i][2 * j + 1]),
+                         min(mn[2 * i + 1][2 * j], mn[2 * i + 1][2 * j + 1]));
+            mx[i][j] = a0;
+            mn[i][j] = b0;
+            cnt[lev] += quot[lev][a0] - quot[lev][b0];
+          }
+        }
+      }
+    }
+  }
+  double f = 0.0;
+#pragma unroll
+  for (int j = 0; j < J; ++j) {
+    int k = a.side >> (j + 1);
+    int c = cnt[j] + k * k;
+    c = min(c, a.ln_len - 1);
+    double t = __dmul_rn(__ldg(a.ln + c), __ldg(a.w + j));
+    f = (j == 0) ? t : __dadd_rn(f, t);
+  }
+  if (a.clamp) f = fmin(fmax(f, 2.0), 3.0);
+  a.fd[b] = f;
+  if (a.key) a.key[b] = (unsigned long long)__double_as_longlong(f);
+}
+
+// Generic path (coarsest scale >= 16): direct per-cell scan, slower.
+__global__ void k_fd_generic(FdArgs a) {
+  __shared__ uint16_t quot[7][256];
+  for (int i = threadIdx.x; i < a.J * 256; i += blockDim.x) quot[i >> 8][i & 255] = a.quot[i];
+  __syncthreads();
+  int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= a.n) return;
+  int y0 = 0, x0 = 0;
+  if (a.mode != FD_STACK) {
+    int64_t by = b / a.nbx, bx = b - by * a.nbx;
+    y0 = (int)by * a.bst;
+    x0 = (int)bx * a.bst;
+  }
+  PixSrc px{a.src, a.W, a.side, a.mode};
+  double f = 0.0;
+  for (int j = 0; j < a.J; ++j) {
+    int s = 2 << j, k = a.side / s;
+    int c = k * k;
+    for (int cy = 0; cy < k; ++cy)
+      for (int cx = 0; cx < k; ++cx) {
+        int hi = 0, lo = 255;
+        for (int yy = 0; yy < s; ++yy)
+          for (int xx = 0; xx < s; ++xx) {
+            int v = px(y0, x0, b, cy * s + yy, cx * s + xx);
+            hi = max(hi, v);
+            lo = min(lo, v);
+          }
+        c += quot[j][hi] - quot[j][lo];
+      }
+    c = min(c, a.ln_len - 1);
+    double t = __dmul_rn(__ldg(a.ln + c), __ldg(a.w + j));
+    f = (j == 0) ? t : __dadd_rn(f, t);
+  }
+  if (a.clamp) f = fmin(fmax(f, 2.0), 3.0);
+  a.fd[b] = f;
+  if (a.key) a.key[b] = (unsigned long long)__double_as_longlong(f);
+}
+
+void launch_fd(const FdArgs& a, cudaStream_t s) {
+  if (a.n == 0) return;
+  int threads = 256;
+  int64_t blocks = cdiv(a.n, threads);
+  if (a.smax == 4 && a.J == 2)
+    k_fd<4><<<(unsigned)blocks, threads, 0, s>>>(a);
+  else if (a.smax == 8 && a.J == 3)
+    k_fd<8><<<(unsigned)blocks, threads, 0, s>>>(a);
+  else
+    k_fd_generic<<<(unsigned)blocks, threads, 0, s>>>(a);
+  FIC_CHECK_LAUNCH();
+}
+
+// ============================================================================
+// K3 — slabs.  Dynamic: [searchsorted(keys, fd - half, left),
+// searchsorted(keys, fd + half, right)) (codec.py:368-370); static2: the
+// midpoint split (codec.py:362-367); empty slabs fall back to the nearest
+// FD (codec.py:371-375, 267-287).  Exhaustive / nosearch: codec.py:343-349.
+// ============================================================================
+
+__device__ __forceinline__ int64_t lower_bound(const double* k, int64_t n, double v) {
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    int64_t m = (lo + hi) >> 1;
+    if (k[m] < v) lo = m + 1; else hi = m;
+  }
+  return lo;
+}
+__device__ __forceinline__ int64_t upper_bound(const double* k, int64_t n, double v) {
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    int64_t m = (lo + hi) >> 1;
+    if (k[m] <= v) lo = m + 1; else hi = m;
+  }
+  return lo;
+}
+
+__global__ void k_slab_scalars(SlabArgs a) {
+  if (threadIdx.x || blockIdx.x) return;
+  double fmn = a.keys[0], fmx = a.keys[a.D - 1];  // fdim.py:93-100
+  a.scal[0] = fmn;
+  a.scal[1] = fmx;
+  if (a.strategy == FIC_STATIC2) {
+    double mid = __ddiv_rn(__dadd_rn(fmn, fmx), 2.0);
+    a.scal[2] = mid;
+    a.scal[3] = (double)lower_bound(a.keys, a.D, mid);
+  } else {
+    a.scal[2] = a.has_delta ? a.delta : __ddiv_rn(__dsub_rn(fmx, fmn), 3.0);
+    a.scal[3] = 0.0;
+  }
+}
+
+__device__ int64_t nearest_fd(const double* keys, const uint32_t* ids, int64_t n, double v) {
+  // codec.py:267-287
+  int64_t pos = lower_bound(keys, n, v);
+  int64_t pl = pos > 0 ? pos - 1 : 0;
+  int64_t pr = pos < n - 1 ? pos : n - 1;
+  int64_t left = lower_bound(keys, n, keys[pl]);
+  int64_t right = lower_bound(keys, n, keys[pr]);
+  double d_lo = pos > 0 ? __dsub_rn(v, keys[pl]) : INFINITY;
+  double d_hi = pos < n ? __dsub_rn(keys[pr], v) : INFINITY;
+  bool take_left = (d_lo < d_hi) || (d_lo == d_hi && ids[left] < ids[right]);
+  return take_left ? left : right;
+}
+
+__device__ __forceinline__ int64_t floordiv(int64_t a, int64_t b) {
+  int64_t q = a / b;
+  return (q * b != a && ((a < 0) != (b < 0))) ? q - 1 : q;
+}
+
+__device__ int64_t nosearch_axis(int extent, int top, int rs, int ds, int st) {
+  // codec.py:434-441
+  int64_t n_pos = (extent - ds) / st + 1;
+  int64_t target = (int64_t)top - rs / 2;
+  int64_t k0 = min(max(floordiv(target, st), (int64_t)0), n_pos - 1);
+  int64_t k1 = min(max(k0 + 1, (int64_t)0), n_pos - 1);
+  int64_t e1 = k1 * st - target, e0 = k0 * st - target;
+  return (llabs(e1) < llabs(e0)) ? k1 : k0;
+}
+
+__global__ void k_slabs(SlabArgs a) {
+  int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= a.R) return;
+  int64_t lo, hi;
+  if (a.strategy == FIC_EXHAUSTIVE) {
+    lo = 0;
+    hi = a.D;
+  } else if (a.strategy == FIC_NOSEARCH) {
+    int ry = r / a.nrx, rx = r - ry * a.nrx;
+    int64_t ky = nosearch_axis(a.H, ry * a.rs, a.rs, a.ds, a.st);
+    int64_t kx = nosearch_axis(a.W, rx * a.rs, a.rs, a.ds, a.st);
+    lo = ky * a.ndx + kx;
+    hi = lo + 1;
+  } else {
+    double f = a.fd_rng[r];
+    if (a.strategy == FIC_STATIC2) {
+      int64_t b = (int64_t)a.scal[3];
+      bool below = f < a.scal[2];
+      lo = below ? 0 : b;
+      hi = below ? b : a.D;
+    } else {
+      double half = a.scal[2];
+      lo = lower_bound(a.keys, a.D, __dsub_rn(f, half));
+      hi = upper_bound(a.keys, a.D, __dadd_rn(f, half));
+    }
+    if (hi <= lo) {
+      lo = nearest_fd(a.keys, a.ids, a.D, f);
+      hi = lo + 1;
+    }
+  }
+  a.lo[r] = (int32_t)lo;
+  a.hi[r] = (int32_t)hi;
+}
+
+void launch_slabs(const SlabArgs& a, cudaStream_t s) {
+  if (a.strategy == FIC_STATIC2 || a.strategy == FIC_DYNAMIC_FD) {
+    k_slab_scalars<<<1, 32, 0, s>>>(a);
+    FIC_CHECK_LAUNCH();
+  }
+  k_slabs<<<(unsigned)cdiv(a.R, 256), 256, 0, s>>>(a);
+  FIC_CHECK_LAUNCH();
+}
+
+// ============================================================================
+// K1 — pool builder.  For each pool position p (FD order for dynamic_fd /
+// static2, raster otherwise): the 2x2 floor-mean decimated domain
+// (blocks.py:75-82) as raw bytes, its exact sums, inv_den = 1/den (0 when
+// den == 0, codec.py:141-145) and the fp16 centred unit-norm row
+// B_k = (K d_k - sum_d) / sqrt(K den) that the tensor-core screen consumes.
+// ============================================================================
+
+template <int RS>
+__global__ void __launch_bounds__(256) k_pool(PoolArgs a) {
+  constexpr int K = RS * RS;
+  int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= a.D) return;
+  uint32_t id = a.order ? a.order[p] : (uint32_t)p;
+  int dy = (int)(id / (uint32_t)a.ndx), dx = (int)(id - (uint32_t)dy * a.ndx);
+  const uint8_t* base = a.img + (int64_t)dy * a.st * a.W + (int64_t)dx * a.st;
+  uint8_t v[K];
+  uint32_t sd = 0, sdd = 0;
+#pragma unroll
+  for (int i = 0; i < RS; ++i) {
+    const uint8_t* r0 = base + (int64_t)(2 * i) * a.W;
+    const uint8_t* r1 = r0 + a.W;
+#pragma unroll
+    for (int j = 0; j < RS; ++j) {
+      uint32_t x = (r0[2 * j] + r0[2 * j + 1] + r1[2 * j] + r1[2 * j + 1]) >> 2;
+      v[i * RS + j] = (uint8_t)x;
+      sd += x;
+      sdd += x * x;
+    }
+  }
+  int64_t den = (int64_t)K * sdd - (int64_t)sd * sd;
+  a.inv_den[p] = den != 0 ? __ddiv_rn(1.0, (double)den) : 0.0;
+  a.sums[p] = make_uint2(sd, sdd);
+  a.ids[p] = id;
+  // raw bytes
+  uint32_t* rw = reinterpret_cast<uint32_t*>(a.raw + p * K);
+#pragma unroll
+  for (int q = 0; q < K / 4; ++q)
+    rw[q] = v[4 * q] | (v[4 * q + 1] << 8) | (v[4 * q + 2] << 16) | ((uint32_t)v[4 * q + 3] << 24);
+  if (a.bh) {
+    double scale = den > 0 ? __drcp_rn(__dsqrt_rn((double)K * (double)den)) : 0.0;
+    uint32_t* bw = reinterpret_cast<uint32_t*>(a.bh + p * K);
+#pragma unroll
+    for (int q = 0; q < K / 2; ++q) {
+      float f0 = (float)(((double)((int)K * v[2 * q] - (int)sd)) * scale);
+      float f1 = (float)(((double)((int)K * v[2 * q + 1] - (int)sd)) * scale);
+      __half2 h = __floats2half2_rn(f0, f1);
+      bw[q] = *reinterpret_cast<uint32_t*>(&h);
+    }
+  }
+}
+
+__global__ void k_pool_generic(PoolArgs a, int rs) {
+  int K = rs * rs;
+  int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= a.D) return;
+  uint32_t id = a.order ? a.order[p] : (uint32_t)p;
+  int dy = (int)(id / (uint32_t)a.ndx), dx = (int)(id - (uint32_t)dy * a.ndx);
+  const uint8_t* base = a.img + (int64_t)dy * a.st * a.W + (int64_t)dx * a.st;
+  uint32_t sd = 0, sdd = 0;
+  for (int i = 0; i < rs; ++i)
+    for (int j = 0; j < rs; ++j) {
+      const uint8_t* q = base + (int64_t)(2 * i) * a.W + 2 * j;
+      uint32_t x = (q[0] + q[1] + q[a.W] + q[a.W + 1]) >> 2;
+      a.raw[p * K + i * rs + j] = (uint8_t)x;
+      sd += x;
+      sdd += x * x;
+    }
+  int64_t den = (int64_t)K * sdd - (int64_t)sd * sd;
+  a.inv_den[p] = den != 0 ? __ddiv_rn(1.0, (double)den) : 0.0;
+  a.sums[p] = make_uint2(sd, sdd);
+  a.ids[p] = id;
+}
+
+void launch_pool(const PoolArgs& a, cudaStream_t s) {
+  if (a.D == 0) return;
+  unsigned blocks = (unsigned)cdiv(a.D, 256);
+  if (a.rs == 8)
+    k_pool<8><<<blocks, 256, 0, s>>>(a);
+  else if (a.rs == 4)
+    k_pool<4><<<blocks, 256, 0, s>>>(a);
+  else
+    k_pool_generic<<<blocks, 256, 0, s>>>(a, a.rs);
+  FIC_CHECK_LAUNCH();
+}
+
+// ============================================================================
+// Range preparation: sums, V, rho and the isometry-permuted range rows
+// rv = r[inv_perm[iso]] (codec.py:195-198, 215, 336-337).
+// ============================================================================
+
+__global__ void k_ranges(RangeArgs a) {
+  int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= a.R) return;
+  const int rs = a.rs, K = rs * rs;
+  int ry = r / a.nrx, rx = r - ry * a.nrx;
+  const uint8_t* base = a.img + (int64_t)ry * rs * a.W + (int64_t)rx * rs;
+  int64_t sr = 0, srr = 0;
+  for (int i = 0; i < rs; ++i)
+    for (int j = 0; j < rs; ++j) {
+      int v = base[(int64_t)i * a.W + j];
+      sr += v;
+      srr += v * v;
+    }
+  RangeInfo inf;
+  inf.sr = (double)sr;
+  inf.srr = (double)srr;
+  inf.V = __dsub_rn((double)srr, __ddiv_rn((double)sr * (double)sr, (double)K));
+  inf.rho = (int32_t)((2 * sr + K) / (2 * K));
+  inf.pad = 0;
+  a.info[r] = inf;
+  uint8_t* out = a.rows + (int64_t)r * a.n_iso * K;
+  for (int i = 0; i < a.n_iso; ++i)
+    for (int k = 0; k < K; ++k) {
+      int src = a.inv_perm[i * K + k];
+      out[i * K + k] = base[(int64_t)(src / rs) * a.W + (src % rs)];
+    }
+}
+
+void launch_ranges(const RangeArgs& a, cudaStream_t s) {
+  if (a.R == 0) return;
+  k_ranges<<<(unsigned)cdiv(a.R, 128), 128, 0, s>>>(a);
+  FIC_CHECK_LAUNCH();
+}
+
+// ============================================================================
+// isometry tables (blocks.py:113-139): 0 id, 1-3 clockwise quarter turns,
+// 4 fliplr, 5-7 fliplr then turns.
+// ============================================================================
+void iso_tables(int rs, int* perm, int* inv_perm) {
+  int K = rs * rs;
+  std::vector<int> cur(K), nxt(K);
+  for (int i = 0; i < 8; ++i) {
+    for (int k = 0; k < K; ++k) cur[k] = k;
+    if (i >= 4)  // fliplr: out[y][x] = in[y][rs-1-x]
+      for (int y = 0; y < rs; ++y)
+        for (int x = 0; x < rs; ++x) nxt[y * rs + x] = cur[y * rs + rs - 1 - x];
+    else
+      nxt = cur;
+    cur = nxt;
+    for (int t = 0; t < i % 4; ++t) {  // clockwise: out[y][x] = in[rs-1-x][y]
+      for (int y = 0; y < rs; ++y)
+        for (int x = 0; x < rs; ++x) nxt[y * rs + x] = cur[(rs - 1 - x) * rs + y];
+      cur = nxt;
+    }
+    for (int k = 0; k < K; ++k) {
+      perm[i * K + k] = cur[k];
+      inv_perm[i * K + cur[k]] = k;
+    }
+  }
+}
+
+}  // namespace fic

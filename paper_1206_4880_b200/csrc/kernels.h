@@ -1,0 +1,81 @@
+// Host-side launchers of the library's kernels (internal interface).
+#pragma once
+#include "common.cuh"
+
+namespace fic {
+
+// ---- K2: differential box counting (fdim.py:44-80) -------------------------
+enum FdMode { FD_IMAGE = 0, FD_DECIMATED = 1, FD_STACK = 2 };
+struct FdArgs {
+  const uint8_t* src;   // image (modes 0/1) or block stack (mode 2)
+  int W;                // image width (modes 0/1)
+  int side;             // block side M
+  int bst;              // block origin step in image pixels (modes 0/1)
+  int nbx;              // blocks per row (modes 0/1)
+  int64_t n;            // blocks
+  int mode;
+  int clamp;
+  int J;                // number of DBC scales (2..7)
+  int smax;             // coarsest scale
+  const uint16_t* quot; // [J][256] floor(v / h_j) (host-built, fdim.py:74-75)
+  const double* ln;     // ln table (fdim.py:76 np.log)
+  int ln_len;
+  const double* w;      // [J] slope weights
+  double* fd;           // [n] output
+  unsigned long long* key;  // [n] optional: fd bits for sorting
+};
+// Builds host-side tables for block side `side` into `quot` (J*256), returns
+// J and the coarsest scale and the ln-table length required.
+int dbc_tables(int side, uint16_t* quot, int* smax, int* ln_needed);
+void launch_fd(const FdArgs& a, cudaStream_t s);
+
+// ---- K3: FD index + slabs (avltree.py:150-189, codec.py:343-375) ------------
+struct SlabArgs {
+  const double* keys;      // sorted domain FDs (pool order)
+  const uint32_t* ids;     // raster id per pool position
+  const double* fd_rng;    // [R]
+  int64_t D;
+  int R;
+  int strategy;
+  int has_delta;
+  double delta;
+  double* scal;            // [4] out: f_min, f_max, half / mid, boundary
+  int32_t* lo;             // [R] out
+  int32_t* hi;             // [R] out
+  // geometry for nosearch (codec.py:430-447)
+  int H, W, rs, ds, st, nrx, ndx;
+};
+void launch_slabs(const SlabArgs& a, cudaStream_t s);
+
+// ---- K1: pool builder (blocks.py:75-82, codec.py:136-145) -------------------
+struct PoolArgs {
+  const uint8_t* img;
+  int W, rs, st, ndx;
+  int64_t D;
+  const uint32_t* order;   // raster id per pool position (nullptr = identity)
+  uint8_t* raw;            // [D][K] decimated pixels, pool order
+  uint16_t* bh;            // [D][K] fp16 centred unit-norm rows (nullptr = skip)
+  double* inv_den;         // [D]
+  uint2* sums;             // [D] (sum_d, sum_dd)
+  uint32_t* ids;           // [D] raster id per pool position (copy of order)
+};
+void launch_pool(const PoolArgs& a, cudaStream_t s);
+
+// ---- range preparation -------------------------------------------------------
+struct RangeArgs {
+  const uint8_t* img;
+  int W, rs, nrx, R, n_iso;
+  const int* inv_perm;     // [8][K] device
+  RangeInfo* info;         // [R]
+  uint8_t* rows;           // [R][n_iso][K] permuted range pixels
+};
+void launch_ranges(const RangeArgs& a, cudaStream_t s);
+
+// ---- planning -----------------------------------------------------------------
+struct PlanCounts {        // read back to the host once
+  int64_t shard_begin, shard_end;  // sorted positions of this shard
+  int64_t n_tensor;                // ranges of the tensor class (all shards)
+  int64_t pool_sum;                // sum(pool) over all ranges
+};
+
+}  // namespace fic

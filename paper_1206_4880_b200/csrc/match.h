@@ -1,0 +1,70 @@
+// Matcher launchers (internal interface).
+#pragma once
+#include "common.cuh"
+
+namespace fic {
+
+// Column (domain) data in pool order, produced by the pool builder (K1).
+struct PoolView {
+  const uint8_t* raw;      // [D][K]
+  const uint16_t* bh;      // [D][K] fp16 bits (tensor path)
+  const double* inv_den;   // [D]
+  const uint2* sums;       // [D] (sum_d, sum_dd)
+  const uint32_t* ids;     // [D] raster domain index
+  int64_t D;
+};
+
+// Range data (raster index).
+struct RangeView {
+  const RangeInfo* info;   // [R]
+  const uint8_t* rows;     // [R][n_iso][K] permuted pixels
+  const int32_t* lo;       // [R] slab start (pool order)
+  const int32_t* hi;       // [R] slab end
+  int n_iso, K;
+};
+
+// Exact CUDA-core matcher: one work item = (range, segment of its slab).
+struct ExactArgs {
+  const int2* items;           // (index into elist, segment)
+  int64_t n_items;
+  const uint32_t* elist;       // range ids of the exact class (this shard)
+  int seg_len;
+  const int64_t* slot_base;    // [R]
+  Partial* partials;
+  unsigned long long* counters;  // [0] exact evaluations
+};
+void launch_exact(const PoolView& P, const RangeView& Rv, const ExactArgs& a,
+                  cudaStream_t s);
+
+// Tensor-core matcher: one work item = (tile of RT ranges x n_iso rows,
+// segment of the tile's union window).
+struct TcArgs {
+  const int2* items;           // (tile, segment)
+  int64_t n_items;
+  const uint32_t* tlist;       // range ids of the tensor class (this shard), tile order
+  int64_t n_tr;
+  const int32_t* wlo;          // [tiles] union window
+  const int32_t* whi;
+  int seg_len;
+  int RT;                      // ranges per tile = 128 / n_iso
+  const int64_t* slot_base;
+  Partial* partials;
+  unsigned long long* counters;  // [0] exact evaluations, [1] screened candidates
+};
+bool tc_supported(int K);
+void launch_tc(const PoolView& P, const RangeView& Rv, const TcArgs& a, cudaStream_t s);
+
+// Merge partial bests into records + RMS (codec.py:259-264, 399-405).
+struct MergeArgs {
+  int R;
+  const int64_t* slot_base;    // [R]
+  const int32_t* nslots;       // [R] (0 = not matched in this call)
+  const Partial* partials;
+  uint8_t* records;            // [R][7]
+  double* pre_rms;
+  double* post_rms;
+  double n;                    // pixels per range
+};
+void launch_merge(const MergeArgs& a, cudaStream_t s);
+
+}  // namespace fic

@@ -1,0 +1,138 @@
+"""CPU-only checks of the host side and the C ABI library (no compute calls)."""
+
+import ctypes
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, cases, load_golden
+from paper_1206_4880_b200 import _lib, codec
+from oracle import fic_oracle as orc
+
+HEADER = os.path.join(ROOT, "include", "fic_b200.h")
+
+
+def _header_symbols():
+    text = open(HEADER).read()
+    return set(re.findall(r"^\s*(?:int|const char\*|void)\s+(fic_\w+)\s*\(", text, re.M))
+
+
+def test_library_exports_every_header_symbol():
+    lib = _lib.load()
+    declared = _header_symbols()
+    assert declared == set(_lib.EXPORTS)
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert lib.fic_abi_version() == 1
+
+
+def test_library_has_sm100a_tensor_core_code():
+    out = subprocess.run(["cuobjdump", "-sass", _lib.LIB_PATH], capture_output=True, text=True)
+    if out.returncode != 0:
+        pytest.skip("cuobjdump unavailable")
+    sass = out.stdout
+    assert "UTCHMMA" in sass      # tcgen05.mma
+    assert "LDTM" in sass         # tcgen05.ld
+    assert "UTMALDG" in sass      # TMA load
+    assert "sm_100a" in subprocess.run(["cuobjdump", "-lelf", _lib.LIB_PATH],
+                                       capture_output=True, text=True).stdout
+
+
+def test_params_struct_matches_c_layout(tmp_path):
+    src = tmp_path / "sz.c"
+    src.write_text(
+        '#include <stdio.h>\n#include <stddef.h>\n#include "fic_b200.h"\n'
+        'int main(void){printf("%zu %zu %zu %zu %zu\\n", sizeof(fic_params_t),'
+        ' offsetof(fic_params_t, delta), offsetof(fic_params_t, n_fd_weights_rng),'
+        ' sizeof(fic_stats_t), sizeof(fic_record_t));return 0;}\n')
+    exe = tmp_path / "sz"
+    subprocess.run(["gcc", "-I", os.path.dirname(HEADER), str(src), "-o", str(exe)], check=True)
+    got = [int(v) for v in subprocess.run([str(exe)], capture_output=True, text=True).stdout.split()]
+    assert got == [ctypes.sizeof(_lib.FicParams), _lib.FicParams.delta.offset,
+                   _lib.FicParams.n_fd_weights_rng.offset, ctypes.sizeof(_lib.FicStats), 7]
+
+
+def test_record_dtype_round_trip():
+    assert codec.RECORD_DTYPE.itemsize == 7
+    rec = np.zeros(3, codec.RECORD_DTYPE)
+    rec["domain"] = [1, 70000, 2**32 - 1]
+    rec["isometry"], rec["s_q"], rec["o_q"] = [0, 7, 3], [0, 31, 16], [0, 127, 64]
+    raw = rec.view(np.uint8).reshape(-1, 7)
+    assert np.array_equal(codec.records_from_bytes(raw), rec)
+
+
+@pytest.mark.parametrize("call, msg", [
+    (lambda: codec.validate(np.zeros((64, 64), np.float32), "exhaustive", 8, 16, 1, "original"), "uint8"),
+    (lambda: codec.validate(np.zeros((64, 64), np.uint8), "bogus", 8, 16, 1, "original"), "unknown strategy"),
+    (lambda: codec.validate(np.zeros((64, 64), np.uint8), "exhaustive", 8, 24, 1, "original"), "twice"),
+    (lambda: codec.validate(np.zeros((64, 64), np.uint8), "exhaustive", 8, 16, 1, "x"), "fd_source"),
+    (lambda: codec.validate(np.zeros((60, 64), np.uint8), "exhaustive", 8, 16, 1, "original"), "not divisible"),
+    (lambda: codec.validate(np.zeros((64, 64), np.uint8), "exhaustive", 8, 16, 0, "original"), "stride must be >= 1"),
+    (lambda: codec.validate(np.zeros((8, 8), np.uint8), "exhaustive", 8, 16, 1, "original"), "exceeds"),
+    (lambda: codec.validate(np.zeros((64, 64), np.uint8), "dynamic_fd", 4, 8, 1, "original"), "two DBC scales"),
+])
+def test_validation_texts_match_reference(call, msg):
+    with pytest.raises(ValueError, match=msg) as got:
+        call()
+    # the oracle restates the reference's own messages: identical text
+    ref_calls = {
+        "uint8": lambda: orc.encode(np.zeros((64, 64), np.float32), "exhaustive"),
+        "unknown strategy": lambda: orc.encode(np.zeros((64, 64), np.uint8), "bogus"),
+        "twice": lambda: orc.encode(np.zeros((64, 64), np.uint8), "exhaustive", domain_size=24),
+        "fd_source": lambda: orc.encode(np.zeros((64, 64), np.uint8), "exhaustive", fd_source="x"),
+        "not divisible": lambda: orc.encode(np.zeros((60, 64), np.uint8), "exhaustive"),
+        "stride must be >= 1": lambda: orc.encode(np.zeros((64, 64), np.uint8), "exhaustive", stride=0),
+        "exceeds": lambda: orc.encode(np.zeros((8, 8), np.uint8), "exhaustive"),
+        "two DBC scales": lambda: orc.encode(np.zeros((64, 64), np.uint8), "dynamic_fd",
+                                             range_size=4, domain_size=8),
+    }
+    with pytest.raises(ValueError) as ref:
+        ref_calls[msg]()
+    assert str(got.value) == str(ref.value)
+
+
+def test_dbc_weights_and_ln_table_match_reference_numpy(golden_fd):
+    for side in (8, 16, 32):
+        assert np.array_equal(codec.dbc_weights(side), golden_fd[f"weights{side}"])
+    ln = codec.ln_table()
+    assert ln[1] == 0.0 and ln[64] == np.log(64.0)
+
+
+def test_serialize_matches_reference_bytes():
+    g = load_golden("encode_cases.npz")
+    for name in cases(g):
+        if f"{name}.fic1" not in g:
+            continue
+        stride, iso, sid, rs, ds = (int(v) for v in g[f"{name}.params"])
+        img = g[f"{name}.image"]
+        recs = codec.records_from_bytes(g[f"{name}.records"]).copy()
+        code = codec.FractalCode(img.shape[1], img.shape[0], rs, ds, stride, sid, bool(iso), recs)
+        blob = codec.serialize(code)
+        assert blob == g[f"{name}.fic1"].tobytes()
+        assert codec.deserialize(blob) == code
+
+
+@pytest.mark.parametrize("mutate, message", [
+    (lambda b: b[:10], "shorter than the fixed header"),
+    (lambda b: b"XXXX" + b[4:], "magic"),
+    (lambda b: b[:4] + bytes([9]) + b[5:], "version"),
+    (lambda b: b[:-3], "fewer record bytes"),
+    (lambda b: b + b"\x00", "trailing"),
+])
+def test_deserialize_rejects_malformed(mutate, message):
+    g = load_golden("encode_cases.npz")
+    blob = g["flat32_ns_s4.fic1"].tobytes()
+    with pytest.raises(codec.FormatError, match=message):
+        codec.deserialize(mutate(blob))
+
+
+def test_make_params_fields():
+    p = codec.make_params("dynamic_fd", 8, 16, 2, True, "original", 0.05, "auto", (1, 4))
+    assert (p.range_size, p.domain_size, p.stride, p.isometries) == (8, 16, 2, 1)
+    assert (p.strategy, p.has_delta, p.delta) == (3, 1, 0.05)
+    assert (p.shard_index, p.shard_count, p.n_fd_weights_dom, p.n_fd_weights_rng) == (1, 4, 3, 2)
+    with pytest.raises(ValueError, match="unknown matcher"):
+        codec.make_params("dynamic_fd", 8, 16, 2, True, "original", None, "bogus", (0, 1))
