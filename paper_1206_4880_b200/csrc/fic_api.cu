@@ -5,6 +5,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -288,6 +290,7 @@ __global__ void k_tiles(TileArgs a) {
     u += (uint32_t)k - (uint32_t)((k >> 32) & 0x7fffffffu);
   }
   atomicAdd(a.useful, u * a.n_iso);
+  atomicAdd(a.useful - 2, (unsigned long long)(hi - lo) * (unsigned long long)((e - b) * a.n_iso));
 }
 
 __global__ void k_exact_segs(const unsigned long long* key, const uint32_t* rid, int64_t eb,
@@ -520,8 +523,8 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
   launch_ranges(ra, s);
 
   // plan: classify, sort by (class, lo, hi), shard by cost
-  unsigned long long* counters = sc.get<unsigned long long>(4);
-  FIC_CUDA(cudaMemsetAsync(counters, 0, 4 * sizeof(unsigned long long), s));
+  unsigned long long* counters = sc.get<unsigned long long>(16);
+  FIC_CUDA(cudaMemsetAsync(counters, 0, 16 * sizeof(unsigned long long), s));
   unsigned long long* key = sc.get<unsigned long long>(g.R);
   unsigned long long* key_s = sc.get<unsigned long long>(g.R);
   uint32_t* rid = sc.get<uint32_t>(g.R);
@@ -611,8 +614,25 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
   tm.mark();  // 3
   if (tot.n_titems) {
     TcArgs ta{titems, tot.n_titems, rid_s + tb, n_tr, wlo, whi, seg_t, RT, sbase, partials,
-              counters};
+              counters, 0, nullptr};
+    const char* dbg_env = getenv("FIC_TC_DEBUG");
+    if (dbg_env && (atoi(dbg_env) & 32)) {
+      ta.dbg = sc.get<unsigned long long>(64 * 24);
+      FIC_CUDA(cudaMemsetAsync(ta.dbg, 0, 64 * 24 * 8, s));
+    }
     launch_tc(P, Rv, ta, s);
+    if (ta.dbg) {
+      std::vector<unsigned long long> h(64 * 24);
+      FIC_CUDA(cudaMemcpyAsync(h.data(), ta.dbg, h.size() * 8, cudaMemcpyDeviceToHost, s));
+      FIC_CUDA(cudaStreamSynchronize(s));
+      unsigned long long t0 = h[0];
+      fprintf(stderr, "tile: tma_issue mma_issue | screener0: full ld_done max_done pre_release arrived\n");
+      for (int j = 0; j < 40; ++j) {
+        fprintf(stderr, "%3d: %7lld %7lld |", j, (long long)(h[j * 24] - t0), (long long)(h[j * 24 + 1] - t0));
+        for (int w = 4; w < 9; ++w) fprintf(stderr, " %7lld", (long long)(h[j * 24 + w] - t0));
+        fprintf(stderr, "\n");
+      }
+    }
   }
   tm.mark();  // 4
   if (tot.n_eitems) {
@@ -624,7 +644,7 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
   launch_merge(ma, s);
   tm.mark();  // 6
 
-  unsigned long long hc[4];
+  unsigned long long hc[16];
   double hs[4];
   FIC_CUDA(cudaMemcpyAsync(hc, counters, sizeof(hc), cudaMemcpyDeviceToHost, s));
   FIC_CUDA(cudaMemcpyAsync(hs, pb.scal, sizeof(hs), cudaMemcpyDeviceToHost, s));
@@ -652,6 +672,9 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
     st->exact_tiles = (int32_t)n_er;
     st->work_items = (int32_t)(tot.n_titems + tot.n_eitems);
     st->kernel_launches = g_launches;
+    if (getenv("FIC_TC_DEBUG") && (atoi(getenv("FIC_TC_DEBUG")) & 4))
+      fprintf(stderr, "tc cycles: producer-empty %.3g  mma-tempty %.3g  mma-full %.3g  epi-tfull %.3g  epi-slow %.3g  epi-total %.3g  arrive->next-full %.3g  full->arrive %.3g\n",
+              (double)hc[4], (double)hc[5], (double)hc[6], (double)hc[7], (double)hc[8], (double)hc[9], (double)hc[10], (double)hc[11]);
   }
 }
 

@@ -24,6 +24,7 @@
 // therefore identical to evaluating every candidate exactly.
 #include <cuda.h>
 #include <cuda_fp16.h>
+#include <cstdlib>
 
 #include "match.h"
 
@@ -32,8 +33,17 @@ namespace fic {
 namespace tc {
 
 constexpr int BM = 128;       // rows per tile (TMEM lanes)
-constexpr int BN = 256;       // columns per N-tile
-constexpr int NTHREADS = 256; // 8 warps: 0 TMA, 1 MMA, 2 TMEM alloc, 3 idle, 4-7 epilogue
+constexpr int BN = 128;       // columns per N-tile (one TMEM accumulator stage)
+constexpr int NACC = 4;       // TMEM accumulator stages (NACC * BN = 512 columns)
+constexpr int NEPI = 16;      // screening warps: 2 groups x 4 lane quarters x 2 slices
+constexpr int NGRP = 2;       // screening groups; group g handles stages j with j % 2 == g
+constexpr int NRES = 2;       // rescoring warps: each thread owns rows t and t + 64
+constexpr int NSLICE = 4;     // survivor queues per row: (group, 64-column slice)
+constexpr int QCAP = 16;      // survivor queue entries per (row, slice)
+constexpr int RES0 = 2;       // first rescoring warp
+constexpr int SCR0 = RES0 + NRES;
+// warps: 0 TMA (+ TMEM alloc), 1 MMA, 2..3 rescorers, 4..19 screeners
+constexpr int NTHREADS = 32 * (SCR0 + NEPI);
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -71,6 +81,14 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map
       " [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(x), "r"(y)
       : "memory");
+}
+
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n .reg .b32 r;\n .reg .pred p;\n elect.sync r|p, 0xffffffff;\n selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(pred));
+  return pred != 0;
 }
 
 __device__ __forceinline__ void fence_after() {
@@ -131,10 +149,14 @@ struct Cfg {
   static constexpr int ROWB = K * 2;                  // bytes per fp16 row
   static constexpr uint32_t LAYOUT = (K == 64) ? 2u : 6u;  // SW128 / SW32
   static constexpr uint32_t SBO = 8 * ROWB;           // bytes per 8-row core group
-  static constexpr int NST = (K == 64) ? 4 : 8;       // B pipeline stages
+  static constexpr int NST = (K == 64) ? 8 : 12;      // B pipeline stages
   static constexpr int A_BYTES = BM * ROWB;
   static constexpr int B_BYTES = BN * ROWB;
-  static constexpr int SMEM = 1024 /*align slack*/ + A_BYTES + NST * B_BYTES + 256;
+  static constexpr int BAR_BYTES = (2 * NST + 2 * NACC + 2) * 8;
+  static constexpr int ROWS_BYTES = BM * K;               // u8 permuted range rows
+  static constexpr int Q_BYTES = BM * NSLICE * QCAP * 4 + BM * NSLICE * 4 * 2 + 16;  // queues + tails/heads
+  static constexpr int RS_BYTES = BM * 40;                // rescorer row state
+  static constexpr int SMEM = 1024 /*align slack*/ + A_BYTES + NST * B_BYTES + BAR_BYTES + BM * 8 + ROWS_BYTES + Q_BYTES + RS_BYTES;
   static constexpr int KW = K / 4;                    // u32 words of a u8 row
 };
 
@@ -149,36 +171,50 @@ __device__ __forceinline__ uint32_t swz(int r, int c) {
 
 using namespace tc;
 
-template <int K>
+template <int K, bool DBG>
 __global__ void __launch_bounds__(NTHREADS, 1)
     k_match_tc(const __grid_constant__ CUtensorMap tmB, PoolView P, RangeView Rv, TcArgs a) {
   using C = Cfg<K>;
+  // timing experiments (FIC_TC_DEBUG) compile into a separate instantiation
+  const int debug = DBG ? a.debug : 0;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte aligned base, derived from smem_raw so accesses stay in the shared window
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;
   uint8_t* sB = smem + C::A_BYTES;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sB + C::NST * C::B_BYTES);
-  // bars: full[NST], empty[NST], tfull[2], tempty[2]
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * C::NST + 4);
+  // bars: full[NST], empty[NST], tfull[NACC], tempty[NACC], tmem holder
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * C::NST + 2 * NACC);
+  // per-range running threshold (bits of a non-negative double)
+  unsigned long long* thr_s = reinterpret_cast<unsigned long long*>(
+      smem + C::A_BYTES + C::NST * C::B_BYTES + C::BAR_BYTES);
+  uint8_t* sRows = reinterpret_cast<uint8_t*>(thr_s + BM);      // [BM][K] u8 rows
+  uint32_t* qbuf = reinterpret_cast<uint32_t*>(sRows + C::ROWS_BYTES);  // [BM][NSLICE][QCAP]
+  volatile uint32_t* qtail = qbuf + BM * NSLICE * QCAP;        // [BM][NSLICE] (screener-owned)
+  volatile uint32_t* qhead = qtail + BM * NSLICE;              // [BM][NSLICE] (rescorer-owned)
+  volatile uint32_t* edone = qhead + BM * NSLICE;              // screening warps done
+  struct RowState { double err, pre, sr, srr; uint32_t dom; uint8_t sq, oq, iso, valid; };
+  RowState* rstate = reinterpret_cast<RowState*>(
+      reinterpret_cast<uint8_t*>(const_cast<uint32_t*>(edone)) + 16);  // [BM]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   auto full_bar = [&](int s) { return smem_u32(bars + s); };
   auto empty_bar = [&](int s) { return smem_u32(bars + C::NST + s); };
   auto tfull_bar = [&](int b) { return smem_u32(bars + 2 * C::NST + b); };
-  auto tempty_bar = [&](int b) { return smem_u32(bars + 2 * C::NST + 2 + b); };
+  auto tempty_bar = [&](int b) { return smem_u32(bars + 2 * C::NST + NACC + b); };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::NST; ++s) {
       mbar_init(full_bar(s), 1);
       mbar_init(empty_bar(s), 1);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < NACC; ++b) {
       mbar_init(tfull_bar(b), 1);
-      mbar_init(tempty_bar(b), 4);
+      mbar_init(tempty_bar(b), NEPI / NGRP);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 2) {
+  if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
                      smem_u32(tmem_holder))
                  : "memory");
@@ -193,17 +229,45 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 
   // pipeline state (each role advances its own copy identically)
   int stage = 0, ph = 0, acc = 0, acc_ph = 0;
+  uint32_t gt = 0;  // N-tiles this CTA processed in earlier items (stage / phase bookkeeping)
   const int n_iso = Rv.n_iso;
   const double nK = (double)K;
 
-  // ---- per-row epilogue state ----
-  const int erow = threadIdx.x - 128;  // row owned by an epilogue thread
-  uint32_t rr[C::KW];
+  // ---- row identity: rescorers own row (tid - 128); screener warp (q, h)
+  // owns TMEM lanes 32q..32q+31 and the h-th 128-column half of each stage
+  const bool is_res = warp >= RES0 && warp < SCR0;
+  const bool is_scr = warp >= SCR0;
+  const int row = is_scr ? 32 * (warp & 3) + lane : 0;
+  const int slice = is_scr ? ((warp - SCR0) >> 2) & 1 : 0;  // 64-column half of a stage
+  const int group = is_scr ? (warp - SCR0) >> 3 : 0;        // stages j % NGRP == group
+  const int rk = row / n_iso;          // range within the tile
+  const int iso = row - rk * n_iso;
   double sr = 0, srr = 0, V = 0, eps = 0;
   int32_t rlo = 0, rhi = 0;
   uint32_t rid = 0;
   bool rvalid = false;
-  unsigned long long evals = 0, screened = 0;
+  unsigned long long evals = 0;
+  long long tw0 = 0, tw1 = 0, tw2 = 0, tw3 = 0, tw4 = 0;  // stall cycles (debug & 4)
+  const long long tstart = (DBG ? clock64() : 0ll);
+
+  // exact rescoring of pool position p (codec.py:218-258 via eval_candidate)
+  auto exact = [&](int64_t p, int erow, double esr, double esrr) -> Cand {
+    uint32_t acc32 = 0;
+    const uint4* src = reinterpret_cast<const uint4*>(P.raw + p * K);
+    const uint4* rrow = reinterpret_cast<const uint4*>(sRows + erow * K);
+#pragma unroll
+    for (int w4 = 0; w4 < C::KW / 4; ++w4) {
+      const uint4 dv = __ldg(src + w4);
+      const uint4 rv = rrow[w4];
+      acc32 = __dp4a(dv.x, rv.x, acc32);
+      acc32 = __dp4a(dv.y, rv.y, acc32);
+      acc32 = __dp4a(dv.z, rv.z, acc32);
+      acc32 = __dp4a(dv.w, rv.w, acc32);
+    }
+    const uint2 sm = __ldg(P.sums + p);
+    return eval_candidate((double)acc32, (double)sm.x, (double)sm.y, __ldg(P.inv_den + p), esr,
+                          esrr, nK);
+  };
 
   int prev_tile = -1;
   for (int64_t it = blockIdx.x; it < a.n_items; it += gridDim.x) {
@@ -221,10 +285,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         int k = j / n_iso, i = j - k * n_iso;
         int64_t g = (int64_t)tile * a.RT + k;
         uint32_t h[4] = {0, 0, 0, 0};
+        uint2 raw8 = make_uint2(0, 0);
         if (k < a.RT && g < a.n_tr) {
           uint32_t r = a.tlist[g];
           int rho = Rv.info[r].rho;
           const uint8_t* src = Rv.rows + ((int64_t)r * n_iso + i) * K + c * 8;
+          raw8 = *reinterpret_cast<const uint2*>(src);
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             __half2 hv = __floats2half2_rn((float)((int)src[2 * e] - rho),
@@ -233,12 +299,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           }
         }
         *reinterpret_cast<uint4*>(sA + swz<K>(j, c)) = make_uint4(h[0], h[1], h[2], h[3]);
+        *reinterpret_cast<uint2*>(sRows + j * K + c * 8) = raw8;
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      if (erow >= 0) {
-        int k = erow / n_iso;
-        int64_t g = (int64_t)tile * a.RT + k;
-        rvalid = (k < a.RT) && (g < a.n_tr);
+      if (is_scr) {
+        int64_t g = (int64_t)tile * a.RT + rk;
+        rvalid = (rk < a.RT) && (g < a.n_tr);
         if (rvalid) {
           rid = a.tlist[g];
           RangeInfo inf = Rv.info[rid];
@@ -251,178 +317,308 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           double an = (double)((int64_t)srr - 2 * (int64_t)inf.rho * (int64_t)sr +
                                (int64_t)K * inf.rho * inf.rho);
           eps = (0x1p-11 + 0x1p-12 + 0x1p-13) * sqrt(an) + (double)K * 510.0 * 0x1p-24 + 1e-6;
-          const uint32_t* src = reinterpret_cast<const uint32_t*>(
-              Rv.rows + ((int64_t)rid * n_iso + (erow - k * n_iso)) * K);
-#pragma unroll
-          for (int q = 0; q < C::KW; ++q) rr[q] = src[q];
         } else {
           rlo = rhi = 0;
         }
       }
       prev_tile = tile;
     }
+    if (threadIdx.x < BM) thr_s[threadIdx.x] = 0x7ff0000000000000ull;  // +inf
+    for (int i = threadIdx.x; i < NSLICE * BM; i += NTHREADS) {
+      qtail[i] = 0;
+      qhead[i] = 0;
+    }
+    if (threadIdx.x == 0) *edone = 0;
     __syncthreads();
 
     if (warp == 0) {
-      if (lane == 0) {
-        for (int j = 0; j < nt; ++j) {
-          mbar_wait(empty_bar(stage), ph ^ 1);
-          mbar_expect_tx(full_bar(stage), C::B_BYTES);
-          tma_load_2d(smem_u32(sB + stage * C::B_BYTES), &tmB, full_bar(stage), 0,
-                      (int)(c0 + (int64_t)j * BN));
-          if (++stage == C::NST) { stage = 0; ph ^= 1; }
+      // TMA producer: the whole warp walks the pipeline, one lane issues
+      for (int j = 0; j < nt; ++j) {
+        { long long t0 = (DBG ? clock64() : 0ll); mbar_wait(empty_bar(stage), ph ^ 1); tw0 += (DBG ? clock64() : 0ll) - t0; }
+        if ((debug & 32) && blockIdx.x == 0 && it == 0 && j < 64 && lane == 0) a.dbg[j * 24] = (DBG ? clock64() : 0ll);
+        if (elect_one()) {
+          if (debug & 16) {
+            mbar_arrive(full_bar(stage));
+          } else {
+            mbar_expect_tx(full_bar(stage), C::B_BYTES);
+            tma_load_2d(smem_u32(sB + stage * C::B_BYTES), &tmB, full_bar(stage), 0,
+                        (int)(c0 + (int64_t)j * BN));
+          }
         }
+        __syncwarp();
+        if (++stage == C::NST) { stage = 0; ph ^= 1; }
       }
     } else if (warp == 1) {
-      if (lane == 0) {
-        const uint32_t a_addr = smem_u32(sA);
-        for (int j = 0; j < nt; ++j) {
-          mbar_wait(tempty_bar(acc), acc_ph ^ 1);
-          mbar_wait(full_bar(stage), ph);
-          fence_after();
-          const uint32_t b_addr = smem_u32(sB + stage * C::B_BYTES);
+      // MMA issuer: descriptors precomputed; per K step +32 B (= +2 in the
+      // 16-byte address field), per stage +B_BYTES
+      const uint64_t adesc = smem_desc(smem_u32(sA), C::SBO, C::LAYOUT);
+      const uint64_t bdesc = smem_desc(smem_u32(sB), C::SBO, C::LAYOUT);
+      for (int j = 0; j < nt; ++j) {
+        { long long t0 = (DBG ? clock64() : 0ll); mbar_wait(tempty_bar(acc), acc_ph ^ 1); tw1 += (DBG ? clock64() : 0ll) - t0; }
+        { long long t0 = (DBG ? clock64() : 0ll); mbar_wait(full_bar(stage), ph); tw2 += (DBG ? clock64() : 0ll) - t0; }
+        fence_after();
+        if ((debug & 32) && blockIdx.x == 0 && it == 0 && j < 64 && lane == 0) a.dbg[j * 24 + 1] = (DBG ? clock64() : 0ll);
+        if (elect_one()) {
           const uint32_t d = tmem_base + acc * BN;
+          const uint64_t bs = bdesc + (uint64_t)((stage * C::B_BYTES) >> 4);
 #pragma unroll
           for (int kk = 0; kk < K / 16; ++kk)
-            mma_f16(d, smem_desc(a_addr + kk * 32, C::SBO, C::LAYOUT),
-                    smem_desc(b_addr + kk * 32, C::SBO, C::LAYOUT), kk > 0 ? 1u : 0u);
+            if (!(debug & 2)) mma_f16(d, adesc + 2 * kk, bs + 2 * kk, kk > 0 ? 1u : 0u);
           mma_commit(empty_bar(stage));
           mma_commit(tfull_bar(acc));
-          if (++stage == C::NST) { stage = 0; ph ^= 1; }
-          if (++acc == 2) { acc = 0; acc_ph ^= 1; }
         }
+        __syncwarp();
+        if (++stage == C::NST) { stage = 0; ph ^= 1; }
+        if (++acc == NACC) { acc = 0; acc_ph ^= 1; }
       }
-    } else if (warp >= 4) {
-      // ------------------------------ epilogue ------------------------------
-      const int q = warp & 3;  // TMEM lane quarter == rows 32q..32q+31
-      const int iso = erow % n_iso;
-      double err = INFINITY, pre = INFINITY, thr = INFINITY;
-      uint32_t dom = 0xffffffffu;
-      int sq = 0, oq = 0;
+    } else if (is_scr) {
+      // ------------------------------ screening ------------------------------
+      // Per stage: 2 x 64 columns (tcgen05.ld x32 twice), |u| max tree, vote.
+      // Chunks whose max reaches the row's threshold push their survivors
+      // (relative positions) to the row's queue; rescoring warps do the
+      // exact evaluation.  A row without an exact error yet first evaluates
+      // its best-|u| candidate itself, so its threshold is finite before any
+      // survivor mask is built.
+      const uint32_t lane_base = tmem_base + ((uint32_t)(32 * (warp & 3)) << 16) + 64 * slice;
+      const uint32_t tfull0 = tfull_bar(0), tempty0 = tempty_bar(0);
+      const int32_t lo32 = rvalid ? (int32_t)(max((int64_t)rlo, c0) - c0) : 0;
+      const int32_t hi32 = rvalid ? (int32_t)(min((int64_t)rhi, c1) - c0) : 0;
+      uint32_t* myq = qbuf + (row * NSLICE + group * 2 + slice) * QCAP;
+      volatile uint32_t* mytail = qtail + row * NSLICE + group * 2 + slice;
+      volatile uint32_t* myhead = qhead + row * NSLICE + group * 2 + slice;
+      uint32_t qt = 0;
+      unsigned long long thr_bits = 0x7ff0000000000000ull;
       float s_r = -1.0f;  // |u| threshold; negative = every candidate survives
+      auto set_threshold = [&](unsigned long long tb) {
+        thr_bits = tb;
+        const double cth = V - __longlong_as_double((long long)tb) - 1e-5;
+        s_r = (cth > 0.0) ? __double2float_rd(sqrt(cth) * (1.0 - 1e-9) - eps) : -1.0f;
+      };
+      auto push = [&](uint32_t rel) {
+        while (qt - *myhead >= (uint32_t)QCAP) __nanosleep(32);
+        myq[qt & (QCAP - 1)] = rel;
+        ++qt;
+        __threadfence_block();
+        *mytail = qt;
+      };
       for (int j = 0; j < nt; ++j) {
-        mbar_wait(tfull_bar(acc), acc_ph);
+        const uint32_t gj = gt + (uint32_t)j;
+        if ((int)(gj % NGRP) != group) continue;
+        const int acc = (int)(gj % NACC), acc_ph = (int)((gj / NACC) & 1);
+        { long long t0 = (DBG ? clock64() : 0ll); mbar_wait(tfull0 + 8 * acc, acc_ph); tw3 += (DBG ? clock64() : 0ll) - t0; }
+        const bool dbgw = (debug & 32) && blockIdx.x == 0 && it == 0 && j < 64 && lane == 0 && warp == SCR0;
+        if (dbgw) a.dbg[j * 24 + 4] = (DBG ? clock64() : 0ll);
         fence_after();
-        const int64_t n0 = c0 + (int64_t)j * BN;
+        {  // thresholds published by the rescorers
+          const unsigned long long tb = thr_s[rk];
+          if (tb < thr_bits) set_threshold(tb);
+        }
 #pragma unroll 1
-        for (int c = 0; c < BN / 32; ++c) {
-          const int64_t p0 = n0 + 32 * c;
-          if (p0 >= c1) break;  // warp-uniform
+        for (int c = 0; c < 2; ++c) {
           float v[32];
-          tmem_ld32(tmem_base + ((uint32_t)(32 * q) << 16) + acc * BN + 32 * c, v);
+          if (!(debug & 1)) tmem_ld32(lane_base + acc * BN + 32 * c, v);
+          const int32_t rel = j * BN + 64 * slice + 32 * c;  // chunk start, relative to c0
+          const int32_t e_lo = lo32 - rel, e_hi = hi32 - rel;
+          const bool overlap = rvalid && e_lo < 32 && e_hi > 0;
           tmem_wait_ld();
-          const bool need = rvalid && p0 < rhi && p0 + 32 > rlo;
-          float m0 = 0.f, m1 = 0.f, m2 = 0.f, m3 = 0.f;
+          if (dbgw && c == 0) a.dbg[j * 24 + 5] = (DBG ? clock64() : 0ll);
+          if (debug & 1) continue;
+          float m0 = fmaxf(fmaxf(fabsf(v[0]), fabsf(v[1])), fabsf(v[2]));
+          float m1 = fmaxf(fmaxf(fabsf(v[3]), fabsf(v[4])), fabsf(v[5]));
+          float m2 = fmaxf(fmaxf(fabsf(v[6]), fabsf(v[7])), fabsf(v[8]));
+          float m3 = fmaxf(fmaxf(fabsf(v[9]), fabsf(v[10])), fabsf(v[11]));
 #pragma unroll
-          for (int e = 0; e < 32; e += 4) {
-            m0 = fmaxf(m0, fabsf(v[e]));
-            m1 = fmaxf(m1, fabsf(v[e + 1]));
-            m2 = fmaxf(m2, fabsf(v[e + 2]));
-            m3 = fmaxf(m3, fabsf(v[e + 3]));
+          for (int e = 12; e < 28; e += 8) {
+            m0 = fmaxf(fmaxf(m0, fabsf(v[e])), fabsf(v[e + 1]));
+            m1 = fmaxf(fmaxf(m1, fabsf(v[e + 2])), fabsf(v[e + 3]));
+            m2 = fmaxf(fmaxf(m2, fabsf(v[e + 4])), fabsf(v[e + 5]));
+            m3 = fmaxf(fmaxf(m3, fabsf(v[e + 6])), fabsf(v[e + 7]));
           }
+          m0 = fmaxf(fmaxf(m0, fabsf(v[28])), fabsf(v[29]));
+          m1 = fmaxf(fmaxf(m1, fabsf(v[30])), fabsf(v[31]));
           const float mx = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3));
-          const bool hit = need && mx >= s_r;
-          if (need) screened += 32;
+          const bool hit = !(debug & 8) && overlap && mx >= s_r;
+          if (dbgw && c == 0) a.dbg[j * 24 + 6] = (DBG ? clock64() : 0ll);
           if (__any_sync(0xffffffffu, hit)) {
-            uint32_t mask = 0;
-            if (hit) {
-              const int64_t lim_lo = max((int64_t)rlo, p0) - p0;
-              const int64_t lim_hi = min(min((int64_t)rhi, c1), p0 + 32) - p0;
+            const long long ts0 = (DBG ? clock64() : 0ll);
+            const int32_t wl = max(e_lo, 0), wh = min(e_hi, 32);
+            uint32_t wmask = 0;
+            if (hit) wmask = ((wh >= 32) ? ~0u : ((1u << wh) - 1u)) & ~((1u << wl) - 1u);
+            const bool seed = hit && thr_bits == 0x7ff0000000000000ull;
+            if (__any_sync(0xffffffffu, seed)) {
+              double tnew = INFINITY;
+              if (seed) {
+                float bv = -1.0f;
 #pragma unroll
-              for (int e = 0; e < 32; ++e)
-                mask |= (fabsf(v[e]) >= s_r && e >= lim_lo && e < lim_hi) ? (1u << e) : 0u;
-            }
-            while (__any_sync(0xffffffffu, mask != 0)) {
-              if (mask) {
-                const int e = __ffs(mask) - 1;
-                mask &= mask - 1;
-                const int64_t p = p0 + e;
-                uint32_t acc32 = 0;
-                const uint4* src = reinterpret_cast<const uint4*>(P.raw + p * K);
+                for (int q = 0; q < 32; ++q) bv = fmaxf(bv, ((wmask >> q) & 1u) ? fabsf(v[q]) : -1.0f);
+                uint32_t eq = 0;
 #pragma unroll
-                for (int w4 = 0; w4 < C::KW / 4; ++w4) {
-                  uint4 dv = __ldg(src + w4);
-                  acc32 = __dp4a(dv.x, rr[4 * w4], acc32);
-                  acc32 = __dp4a(dv.y, rr[4 * w4 + 1], acc32);
-                  acc32 = __dp4a(dv.z, rr[4 * w4 + 2], acc32);
-                  acc32 = __dp4a(dv.w, rr[4 * w4 + 3], acc32);
-                }
-                const uint2 sm = __ldg(P.sums + p);
-                const Cand cd = eval_candidate((double)acc32, (double)sm.x, (double)sm.y,
-                                               __ldg(P.inv_den + p), sr, srr, nK);
-                const uint32_t did = __ldg(P.ids + p);
-                pre = fmin(pre, cd.pre);
-                if (better(cd.err, did, iso, err, dom, iso)) {
-                  err = cd.err;
-                  dom = did;
-                  sq = cd.sq;
-                  oq = cd.oq;
-                }
-                thr = fmin(thr, cd.err);
+                for (int q = 0; q < 32; ++q) eq |= (fabsf(v[q]) == bv) ? (1u << q) : 0u;
+                const int e = __ffs((int)(eq & wmask)) - 1;
+                wmask &= ~(1u << e);
+                tnew = fmax(exact(c0 + rel + e, row, sr, srr).err, 0.0);
                 ++evals;
+                push((uint32_t)(rel + e));  // the rescorer records it
+              }
+              for (int m = 1; m < n_iso; m <<= 1)
+                tnew = fmin(tnew, __shfl_xor_sync(0xffffffffu, tnew, m));
+              const unsigned long long tb = (unsigned long long)__double_as_longlong(tnew);
+              if (tb < thr_bits) {
+                set_threshold(tb);
+                if (iso == 0 && rvalid) atomicMin(thr_s + rk, tb);
               }
             }
-            // share the range's threshold across its isometry lanes
-            for (int m = 1; m < n_iso; m <<= 1) thr = fmin(thr, __shfl_xor_sync(0xffffffffu, thr, m));
-            const double cth = V - thr - 1e-5;
-            if (cth > 0.0) {
-              const double t = sqrt(cth) * (1.0 - 1e-9) - eps;
-              s_r = __double2float_rd(t);
-            } else {
-              s_r = -1.0f;
+            if (hit) {
+              uint32_t m = 0;
+#pragma unroll
+              for (int q = 0; q < 32; ++q) m |= (fabsf(v[q]) >= s_r) ? (1u << q) : 0u;
+              m &= wmask;
+              while (m) {
+                const int e = __ffs((int)m) - 1;
+                m &= m - 1;
+                push((uint32_t)(rel + e));
+              }
             }
+            tw4 += (DBG ? clock64() : 0ll) - ts0;
           }
         }
+      release:
+        if (dbgw) a.dbg[j * 24 + 7] = (DBG ? clock64() : 0ll);
         fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(tempty_bar(acc));
-        if (++acc == 2) { acc = 0; acc_ph ^= 1; }
+        if (lane == 0) mbar_arrive(tempty0 + 8 * acc);
+        if (dbgw) a.dbg[j * 24 + 8] = (DBG ? clock64() : 0ll);
       }
-      // combine the n_iso rows of each range: lexicographic (err, dom, iso)
-      int biso = iso;
-      for (int m = 1; m < n_iso; m <<= 1) {
-        double e2 = __shfl_xor_sync(0xffffffffu, err, m);
-        double p2 = __shfl_xor_sync(0xffffffffu, pre, m);
-        uint32_t d2 = __shfl_xor_sync(0xffffffffu, dom, m);
-        int i2 = __shfl_xor_sync(0xffffffffu, biso, m);
-        int s2 = __shfl_xor_sync(0xffffffffu, sq, m);
-        int o2 = __shfl_xor_sync(0xffffffffu, oq, m);
-        if (better(e2, d2, i2, err, dom, biso)) {
-          err = e2;
-          dom = d2;
-          biso = i2;
-          sq = s2;
-          oq = o2;
+      __threadfence_block();
+      __syncwarp();
+      if (lane == 0) atomicAdd((uint32_t*)edone, 1u);
+    } else if (is_res) {
+      // ------------------------------ rescoring ------------------------------
+      // Thread t owns rows t and t + 64: it drains their survivor queues,
+      // evaluates each candidate exactly (state in shared memory) and
+      // publishes the range's threshold.
+      const int t = (int)threadIdx.x - 32 * RES0;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int r = t + 64 * h, k = r / n_iso;
+        const int64_t g = (int64_t)tile * a.RT + k;
+        RowState st;
+        st.err = INFINITY;
+        st.pre = INFINITY;
+        st.dom = 0xffffffffu;
+        st.sq = st.oq = 0;
+        st.iso = (uint8_t)(r - k * n_iso);
+        st.valid = (k < a.RT && g < a.n_tr) ? 1 : 0;
+        st.sr = st.srr = 0.0;
+        if (st.valid) {
+          const RangeInfo inf = Rv.info[a.tlist[g]];
+          st.sr = inf.sr;
+          st.srr = inf.srr;
         }
-        pre = fmin(pre, p2);
+        rstate[r] = st;
       }
-      if (rvalid && iso == 0) {
-        Partial out;
-        out.err = err;
-        out.pre = pre;
-        out.dom = dom;
-        out.iso = (uint8_t)biso;
-        out.sq = (uint8_t)sq;
-        out.oq = (uint8_t)oq;
-        out.valid = (dom != 0xffffffffu) ? 1 : 0;
-        a.partials[a.slot_base[rid] + item.y] = out;
+      uint32_t hd[2 * NSLICE];
+#pragma unroll
+      for (int q = 0; q < 2 * NSLICE; ++q) hd[q] = 0;
+      while (true) {
+        int got = -1;
+        uint32_t rel = 0;
+#pragma unroll
+        for (int q = 0; q < 2 * NSLICE; ++q) {
+          const int r = t + 64 * (q / NSLICE), qs = q % NSLICE;
+          if (got < 0 && hd[q] != qtail[r * NSLICE + qs]) {
+            __threadfence_block();
+            rel = qbuf[(r * NSLICE + qs) * QCAP + (hd[q] & (QCAP - 1))];
+            qhead[r * NSLICE + qs] = ++hd[q];
+            got = q / NSLICE;
+          }
+        }
+        if (got >= 0) {
+          const int r = t + 64 * got, k = r / n_iso;
+          RowState st = rstate[r];
+          const int64_t p = c0 + rel;
+          const Cand cd = exact(p, r, st.sr, st.srr);
+          const uint32_t did = __ldg(P.ids + p);
+          st.pre = fmin(st.pre, cd.pre);
+          if (better(cd.err, did, st.iso, st.err, st.dom, st.iso)) {
+            st.err = cd.err;
+            st.dom = did;
+            st.sq = (uint8_t)cd.sq;
+            st.oq = (uint8_t)cd.oq;
+          }
+          rstate[r] = st;
+          atomicMin(thr_s + k, (unsigned long long)__double_as_longlong(fmax(cd.err, 0.0)));
+          ++evals;
+        } else if (*edone == (uint32_t)NEPI) {
+          __threadfence_block();
+          bool empty = true;
+#pragma unroll
+          for (int q = 0; q < 2 * NSLICE; ++q)
+            empty = empty && (hd[q] == qtail[(t + 64 * (q / NSLICE)) * NSLICE + q % NSLICE]);
+          if (empty) break;
+        } else {
+          __nanosleep(256);
+        }
+      }
+      __syncwarp();
+      // combine the n_iso rows of each range: lexicographic (err, dom, iso)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int r = t + 64 * h;
+        const RowState st = rstate[r];
+        double err = st.err, pre = st.pre;
+        uint32_t dom = st.dom;
+        int biso = st.iso, sq = st.sq, oq = st.oq;
+        for (int m = 1; m < n_iso; m <<= 1) {
+          double e2 = __shfl_xor_sync(0xffffffffu, err, m);
+          double p2 = __shfl_xor_sync(0xffffffffu, pre, m);
+          uint32_t d2 = __shfl_xor_sync(0xffffffffu, dom, m);
+          int i2 = __shfl_xor_sync(0xffffffffu, biso, m);
+          int s2 = __shfl_xor_sync(0xffffffffu, sq, m);
+          int o2 = __shfl_xor_sync(0xffffffffu, oq, m);
+          if (better(e2, d2, i2, err, dom, biso)) {
+            err = e2;
+            dom = d2;
+            biso = i2;
+            sq = s2;
+            oq = o2;
+          }
+          pre = fmin(pre, p2);
+        }
+        if (st.iso == 0 && st.valid) {
+          const int64_t g = (int64_t)tile * a.RT + r / n_iso;
+          Partial out;
+          out.err = err;
+          out.pre = pre;
+          out.dom = dom;
+          out.iso = (uint8_t)biso;
+          out.sq = (uint8_t)sq;
+          out.oq = (uint8_t)oq;
+          out.valid = (dom != 0xffffffffu) ? 1 : 0;
+          a.partials[a.slot_base[a.tlist[g]] + item.y] = out;
+        }
       }
     }
+    gt += (uint32_t)nt;
     __syncthreads();
   }
 
-  if (erow >= 0) {
-    for (int m = 16; m >= 1; m >>= 1) {
-      evals += __shfl_xor_sync(0xffffffffu, evals, m);
-      screened += __shfl_xor_sync(0xffffffffu, screened, m);
-    }
-    if (lane == 0) {
-      atomicAdd(a.counters, evals);
-      atomicAdd(a.counters + 1, screened);
+  if (is_res || is_scr) {
+    for (int m = 16; m >= 1; m >>= 1) evals += __shfl_xor_sync(0xffffffffu, evals, m);
+    if (lane == 0) atomicAdd(a.counters, evals);
+    if ((debug & 4) && lane == 0 && is_scr) {
+      atomicAdd(a.counters + 7, (unsigned long long)tw3);
+      atomicAdd(a.counters + 8, (unsigned long long)tw4);
+      atomicAdd(a.counters + 9, (unsigned long long)((DBG ? clock64() : 0ll) - tstart));
     }
   }
+  if ((debug & 4) && lane == 0 && warp == 0) atomicAdd(a.counters + 4, (unsigned long long)tw0);
+  if ((debug & 4) && lane == 0 && warp == 1) {
+    atomicAdd(a.counters + 5, (unsigned long long)tw1);
+    atomicAdd(a.counters + 6, (unsigned long long)tw2);
+  }
   __syncthreads();
-  if (warp == 2) {
+  if (warp == 0) {
     fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base)
                  : "memory");
@@ -469,7 +665,9 @@ static void launch_tc_k(const PoolView& P, const RangeView& Rv, const TcArgs& a,
   if (cr != CUDA_SUCCESS) throw Error{FIC_ECUDA, "cuTensorMapEncodeTiled failed"};
   static bool attr_set = false;
   if (!attr_set) {
-    FIC_CUDA(cudaFuncSetAttribute(k_match_tc<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    FIC_CUDA(cudaFuncSetAttribute(k_match_tc<K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  C::SMEM));
+    FIC_CUDA(cudaFuncSetAttribute(k_match_tc<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   C::SMEM));
     attr_set = true;
   }
@@ -477,7 +675,13 @@ static void launch_tc_k(const PoolView& P, const RangeView& Rv, const TcArgs& a,
   FIC_CUDA(cudaGetDevice(&dev));
   FIC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   unsigned grid = (unsigned)std::min<int64_t>(a.n_items, sms);
-  k_match_tc<K><<<grid, NTHREADS, C::SMEM, s>>>(map, P, Rv, a);
+  TcArgs aa = a;
+  const char* dbg = getenv("FIC_TC_DEBUG");
+  aa.debug = dbg ? atoi(dbg) : 0;
+  if (aa.debug)
+    k_match_tc<K, true><<<grid, NTHREADS, C::SMEM, s>>>(map, P, Rv, aa);
+  else
+    k_match_tc<K, false><<<grid, NTHREADS, C::SMEM, s>>>(map, P, Rv, aa);
   FIC_CHECK_LAUNCH();
 }
 

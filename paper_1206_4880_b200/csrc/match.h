@@ -50,6 +50,8 @@ struct TcArgs {
   const int64_t* slot_base;
   Partial* partials;
   unsigned long long* counters;  // [0] exact evaluations, [1] screened candidates
+  int debug;                   // FIC_TC_DEBUG (timing experiments only; results invalid if != 0)
+  unsigned long long* dbg;     // timeline buffer (debug & 32)
 };
 bool tc_supported(int K);
 void launch_tc(const PoolView& P, const RangeView& Rv, const TcArgs& a, cudaStream_t s);
