@@ -65,6 +65,20 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   } while (!ok);
 }
 
+// blocking wait with a suspend-time hint: the warp sleeps in the barrier
+// instead of spinning through the issue slots
+__device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity) {
+  uint32_t ok = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity), "r"(0x100000u)
+        : "memory");
+  } while (!ok);
+}
+
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
@@ -401,11 +415,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         __threadfence_block();
         *mytail = qt;
       };
-      for (int j = 0; j < nt; ++j) {
+      for (int j = (int)((group - (int)(gt % NGRP) + NGRP) % NGRP); j < nt; j += NGRP) {
         const uint32_t gj = gt + (uint32_t)j;
-        if ((int)(gj % NGRP) != group) continue;
         const int acc = (int)(gj % NACC), acc_ph = (int)((gj / NACC) & 1);
-        { long long t0 = (DBG ? clock64() : 0ll); mbar_wait(tfull0 + 8 * acc, acc_ph); tw3 += (DBG ? clock64() : 0ll) - t0; }
+        { long long t0 = (DBG ? clock64() : 0ll); mbar_wait_sleep(tfull0 + 8 * acc, acc_ph); tw3 += (DBG ? clock64() : 0ll) - t0; }
         const bool dbgw = (debug & 32) && blockIdx.x == 0 && it == 0 && j < 64 && lane == 0 && warp == SCR0;
         if (dbgw) a.dbg[j * 24 + 4] = (DBG ? clock64() : 0ll);
         fence_after();
