@@ -479,7 +479,7 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
   const int small_pool = p.small_pool > 0 ? p.small_pool : 256;
   const int seg_t = p.max_segment > 0 ? (int)align_up(p.max_segment, 256) : 65536;
   const int seg_e = 4096;
-  const int RT = 128 / g.n_iso;
+  const int RT = (tensor_ok ? tc_tile_rows(K) : 128) / g.n_iso;
 
   g_launches = 0;
   Scratch sc(s);

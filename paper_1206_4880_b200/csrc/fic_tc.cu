@@ -123,21 +123,85 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t sbo, uint3
   return d;
 }
 
-// kind::f16 instruction descriptor: D f32, A/B f16, both K-major, M=128, N=256.
-constexpr uint32_t IDESC = (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
-
-__device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t acc) {
-  asm volatile(
-      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-      " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
-      "l"(a), "l"(b), "r"(IDESC), "r"(acc)
-      : "memory");
+// kind::f16 instruction descriptor: D f32, A/B f16, both K-major, M = 128*CG, N = BN.
+template <int CG>
+__device__ __forceinline__ constexpr uint32_t idesc() {
+  return (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)((BM * CG) >> 4) << 24);
 }
 
+template <int CG>
+__device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t acc) {
+  if constexpr (CG == 1)
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+        " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc<1>()), "r"(acc)
+        : "memory");
+  else
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+        " tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc<2>()), "r"(acc)
+        : "memory");
+}
+
+// MMA completion -> mbarrier arrive (in both CTAs of the pair for CG == 2)
+template <int CG>
 __device__ __forceinline__ void mma_commit(uint32_t bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                   bar)
+  if constexpr (CG == 1)
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+                 : "memory");
+  else
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+        " [%0], %1;" ::"r"(bar), "h"((uint16_t)3)
+        : "memory");
+}
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+// shared::cluster address of the same smem location in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t map_to_rank(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
                : "memory");
+}
+
+template <int CG>
+__device__ __forceinline__ void cta_sync() {
+  if constexpr (CG == 1) {
+    __syncthreads();
+  } else {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::
+                     : "memory");
+  }
+}
+
+// TMA 2D load; for CG == 2 the completion goes to the leader CTA's barrier
+template <int CG>
+__device__ __forceinline__ void tma_load(uint32_t dst, const CUtensorMap* map, uint32_t bar, int x,
+                                         int y) {
+  if constexpr (CG == 1)
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(x), "r"(y)
+        : "memory");
+  else
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(x), "r"(y)
+        : "memory");
 }
 
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
@@ -158,14 +222,15 @@ __device__ __forceinline__ void tmem_wait_ld() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-template <int K>
+template <int K, int CG>
 struct Cfg {
   static constexpr int ROWB = K * 2;                  // bytes per fp16 row
   static constexpr uint32_t LAYOUT = (K == 64) ? 2u : 6u;  // SW128 / SW32
   static constexpr uint32_t SBO = 8 * ROWB;           // bytes per 8-row core group
-  static constexpr int NST = (K == 64) ? 8 : 12;      // B pipeline stages
+  static constexpr int NST = (K == 64) ? 8 : 12;  // B smem stages
   static constexpr int A_BYTES = BM * ROWB;
-  static constexpr int B_BYTES = BN * ROWB;
+  static constexpr int B_BYTES = (BN / CG) * ROWB;       // this CTA's share of a B stage
+  static constexpr int TX_BYTES = BN * ROWB;              // both shares (leader's barrier)
   static constexpr int BAR_BYTES = (2 * NST + 2 * NACC + 2) * 8;
   static constexpr int ROWS_BYTES = BM * K;               // u8 permuted range rows
   static constexpr int Q_BYTES = BM * NSLICE * QCAP * 4 + BM * NSLICE * 4 * 2 + 16;  // queues + tails/heads
@@ -185,10 +250,15 @@ __device__ __forceinline__ uint32_t swz(int r, int c) {
 
 using namespace tc;
 
-template <int K, bool DBG>
+template <int K, int CG, bool DBG>
 __global__ void __launch_bounds__(NTHREADS, 1)
     k_match_tc(const __grid_constant__ CUtensorMap tmB, PoolView P, RangeView Rv, TcArgs a) {
-  using C = Cfg<K>;
+  using C = Cfg<K, CG>;
+  // CG == 2: a cluster of two CTAs runs one M = 256 tile; CTA `crank` owns
+  // tile rows 128*crank .. +127 and loads columns (BN/2)*crank .. of each B stage.
+  const uint32_t crank = (CG == 2) ? cluster_rank() : 0u;
+  const bool leader = crank == 0;
+  const int rbase = BM * (int)crank;
   // timing experiments (FIC_TC_DEBUG) compile into a separate instantiation
   const int debug = DBG ? a.debug : 0;
   extern __shared__ uint8_t smem_raw[];
@@ -197,7 +267,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   uint8_t* sA = smem;
   uint8_t* sB = smem + C::A_BYTES;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sB + C::NST * C::B_BYTES);
-  // bars: full[NST], empty[NST], tfull[NACC], tempty[NACC], tmem holder
+  // bars: full[NST] (leader: B data landed), empty[NST] (MMA done reading B),
+  // tfull[NACC] (MMA done writing D), tempty[NACC] (leader: all screeners
+  // released the accumulator stage), tmem holder
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * C::NST + 2 * NACC);
   // per-range running threshold (bits of a non-negative double)
   unsigned long long* thr_s = reinterpret_cast<unsigned long long*>(
@@ -224,20 +296,27 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
     for (int b = 0; b < NACC; ++b) {
       mbar_init(tfull_bar(b), 1);
-      mbar_init(tempty_bar(b), NEPI / NGRP);
+      mbar_init(tempty_bar(b), (NEPI / NGRP) * CG);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
-                     smem_u32(tmem_holder))
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    if constexpr (CG == 1) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                       smem_u32(tmem_holder))
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                       smem_u32(tmem_holder))
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    }
   }
   if (warp == 0 && lane == 0)
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
   fence_before();
-  __syncthreads();
+  cta_sync<CG>();
   fence_after();
   const uint32_t tmem_base = *tmem_holder;
 
@@ -254,8 +333,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   const int row = is_scr ? 32 * (warp & 3) + lane : 0;
   const int slice = is_scr ? ((warp - SCR0) >> 2) & 1 : 0;  // 64-column half of a stage
   const int group = is_scr ? (warp - SCR0) >> 3 : 0;        // stages j % NGRP == group
-  const int rk = row / n_iso;          // range within the tile
+  const int rk = row / n_iso;          // range within this CTA's rows (thr_s index)
   const int iso = row - rk * n_iso;
+  const int rk_tile = (row + rbase) / n_iso;  // range within the tile (tlist index)
   double sr = 0, srr = 0, V = 0, eps = 0;
   int32_t rlo = 0, rhi = 0;
   uint32_t rid = 0;
@@ -284,7 +364,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   };
 
   int prev_tile = -1;
-  for (int64_t it = blockIdx.x; it < a.n_items; it += gridDim.x) {
+  for (int64_t it = blockIdx.x / CG; it < a.n_items; it += gridDim.x / CG) {
     const int2 item = a.items[it];
     const int tile = item.x;
     const int64_t wlo = a.wlo[tile], whi = a.whi[tile];
@@ -296,7 +376,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       // A operand: row j = (range k = j / n_iso, iso i = j % n_iso), a = rv - rho
       for (int u = threadIdx.x; u < BM * (K / 8); u += NTHREADS) {
         int j = u / (K / 8), c = u % (K / 8);
-        int k = j / n_iso, i = j - k * n_iso;
+        int k = (j + rbase) / n_iso, i = (j + rbase) - k * n_iso;
         int64_t g = (int64_t)tile * a.RT + k;
         uint32_t h[4] = {0, 0, 0, 0};
         uint2 raw8 = make_uint2(0, 0);
@@ -317,8 +397,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       if (is_scr) {
-        int64_t g = (int64_t)tile * a.RT + rk;
-        rvalid = (rk < a.RT) && (g < a.n_tr);
+        int64_t g = (int64_t)tile * a.RT + rk_tile;
+        rvalid = (rk_tile < a.RT) && (g < a.n_tr);
         if (rvalid) {
           rid = a.tlist[g];
           RangeInfo inf = Rv.info[rid];
@@ -343,7 +423,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       qhead[i] = 0;
     }
     if (threadIdx.x == 0) *edone = 0;
-    __syncthreads();
+    cta_sync<CG>();
 
     if (warp == 0) {
       // TMA producer: the whole warp walks the pipeline, one lane issues
@@ -352,17 +432,19 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         if ((debug & 32) && blockIdx.x == 0 && it == 0 && j < 64 && lane == 0) a.dbg[j * 24] = (DBG ? clock64() : 0ll);
         if (elect_one()) {
           if (debug & 16) {
-            mbar_arrive(full_bar(stage));
+            if (leader) mbar_arrive(full_bar(stage));
           } else {
-            mbar_expect_tx(full_bar(stage), C::B_BYTES);
-            tma_load_2d(smem_u32(sB + stage * C::B_BYTES), &tmB, full_bar(stage), 0,
-                        (int)(c0 + (int64_t)j * BN));
+            // the leader's full barrier expects both CTAs' shares
+            if (leader) mbar_expect_tx(full_bar(stage), C::TX_BYTES);
+            const uint32_t fb = (CG == 2) ? map_to_rank(full_bar(stage), 0) : full_bar(stage);
+            tma_load<CG>(smem_u32(sB + stage * C::B_BYTES), &tmB, fb, 0,
+                         (int)(c0 + (int64_t)j * BN + (BN / CG) * (int)crank));
           }
         }
         __syncwarp();
         if (++stage == C::NST) { stage = 0; ph ^= 1; }
       }
-    } else if (warp == 1) {
+    } else if (warp == 1 && leader) {
       // MMA issuer: descriptors precomputed; per K step +32 B (= +2 in the
       // 16-byte address field), per stage +B_BYTES
       const uint64_t adesc = smem_desc(smem_u32(sA), C::SBO, C::LAYOUT);
@@ -377,9 +459,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           const uint64_t bs = bdesc + (uint64_t)((stage * C::B_BYTES) >> 4);
 #pragma unroll
           for (int kk = 0; kk < K / 16; ++kk)
-            if (!(debug & 2)) mma_f16(d, adesc + 2 * kk, bs + 2 * kk, kk > 0 ? 1u : 0u);
-          mma_commit(empty_bar(stage));
-          mma_commit(tfull_bar(acc));
+            if (!(debug & 2)) mma_f16<CG>(d, adesc + 2 * kk, bs + 2 * kk, kk > 0 ? 1u : 0u);
+          mma_commit<CG>(empty_bar(stage));
+          mma_commit<CG>(tfull_bar(acc));
         }
         __syncwarp();
         if (++stage == C::NST) { stage = 0; ph ^= 1; }
@@ -450,7 +532,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           m0 = fmaxf(fmaxf(m0, fabsf(v[28])), fabsf(v[29]));
           m1 = fmaxf(fmaxf(m1, fabsf(v[30])), fabsf(v[31]));
           const float mx = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3));
-          const bool hit = !(debug & 8) && overlap && mx >= s_r;
+          const bool hit = !(debug & 8) && overlap && (mx >= s_r || (debug & 64));
           if (dbgw && c == 0) a.dbg[j * 24 + 6] = (DBG ? clock64() : 0ll);
           if (__any_sync(0xffffffffu, hit)) {
             const long long ts0 = (DBG ? clock64() : 0ll);
@@ -484,7 +566,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             if (hit) {
               uint32_t m = 0;
 #pragma unroll
-              for (int q = 0; q < 32; ++q) m |= (fabsf(v[q]) >= s_r) ? (1u << q) : 0u;
+              for (int q = 0; q < 32; ++q) m |= (fabsf(v[q]) >= s_r || (debug & 64)) ? (1u << q) : 0u;
               m &= wmask;
               while (m) {
                 const int e = __ffs((int)m) - 1;
@@ -499,7 +581,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         if (dbgw) a.dbg[j * 24 + 7] = (DBG ? clock64() : 0ll);
         fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(tempty0 + 8 * acc);
+        if (lane == 0) {
+          if (leader)
+            mbar_arrive(tempty0 + 8 * acc);
+          else
+            mbar_arrive_cluster(map_to_rank(tempty0 + 8 * acc, 0));
+        }
         if (dbgw) a.dbg[j * 24 + 8] = (DBG ? clock64() : 0ll);
       }
       __threadfence_block();
@@ -513,14 +600,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       const int t = (int)threadIdx.x - 32 * RES0;
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const int r = t + 64 * h, k = r / n_iso;
+        const int r = t + 64 * h, k = (r + rbase) / n_iso;
         const int64_t g = (int64_t)tile * a.RT + k;
         RowState st;
         st.err = INFINITY;
         st.pre = INFINITY;
         st.dom = 0xffffffffu;
         st.sq = st.oq = 0;
-        st.iso = (uint8_t)(r - k * n_iso);
+        st.iso = (uint8_t)(r + rbase - k * n_iso);
         st.valid = (k < a.RT && g < a.n_tr) ? 1 : 0;
         st.sr = st.srr = 0.0;
         if (st.valid) {
@@ -599,7 +686,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           pre = fmin(pre, p2);
         }
         if (st.iso == 0 && st.valid) {
-          const int64_t g = (int64_t)tile * a.RT + r / n_iso;
+          const int64_t g = (int64_t)tile * a.RT + (r + rbase) / n_iso;
           Partial out;
           out.err = err;
           out.pre = pre;
@@ -613,7 +700,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       }
     }
     gt += (uint32_t)nt;
-    __syncthreads();
+    cta_sync<CG>();
   }
 
   if (is_res || is_scr) {
@@ -630,11 +717,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     atomicAdd(a.counters + 5, (unsigned long long)tw1);
     atomicAdd(a.counters + 6, (unsigned long long)tw2);
   }
-  __syncthreads();
+  cta_sync<CG>();
   if (warp == 0) {
     fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base)
-                 : "memory");
+    if constexpr (CG == 1)
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base)
+                   : "memory");
+    else
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem_base)
+                   : "memory");
   }
 }
 
@@ -662,13 +753,21 @@ static PFN_encodeTiled get_encode() {
 
 bool tc_supported(int K) { return K == 64 || K == 16; }
 
-template <int K>
+// rows per tensor tile (the planner sizes tiles with it)
+static int tc_cg(int K) {
+  if (K != 64) return 1;
+  const char* e = getenv("FIC_TC_CG");
+  return (e && atoi(e) == 2) ? 2 : 1;
+}
+int tc_tile_rows(int K) { return BM * tc_cg(K); }
+
+template <int K, int CG>
 static void launch_tc_k(const PoolView& P, const RangeView& Rv, const TcArgs& a, cudaStream_t s) {
-  using C = Cfg<K>;
+  using C = Cfg<K, CG>;
   CUtensorMap map;
   cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)P.D};
   cuuint64_t strides[1] = {(cuuint64_t)K * 2};
-  cuuint32_t box[2] = {(cuuint32_t)K, (cuuint32_t)BN};
+  cuuint32_t box[2] = {(cuuint32_t)K, (cuuint32_t)(BN / CG)};
   cuuint32_t estr[2] = {1, 1};
   CUresult cr = get_encode()(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, (void*)P.bh, dims, strides,
                              box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -678,32 +777,46 @@ static void launch_tc_k(const PoolView& P, const RangeView& Rv, const TcArgs& a,
   if (cr != CUDA_SUCCESS) throw Error{FIC_ECUDA, "cuTensorMapEncodeTiled failed"};
   static bool attr_set = false;
   if (!attr_set) {
-    FIC_CUDA(cudaFuncSetAttribute(k_match_tc<K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  C::SMEM));
-    FIC_CUDA(cudaFuncSetAttribute(k_match_tc<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  C::SMEM));
+    FIC_CUDA(cudaFuncSetAttribute(k_match_tc<K, CG, false>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    FIC_CUDA(cudaFuncSetAttribute(k_match_tc<K, CG, true>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     attr_set = true;
   }
   int dev = 0, sms = 148;
   FIC_CUDA(cudaGetDevice(&dev));
   FIC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  unsigned grid = (unsigned)std::min<int64_t>(a.n_items, sms);
+  const int64_t clusters = std::min<int64_t>(a.n_items, sms / CG);
   TcArgs aa = a;
   const char* dbg = getenv("FIC_TC_DEBUG");
   aa.debug = dbg ? atoi(dbg) : 0;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(clusters * CG));
+  cfg.blockDim = dim3(NTHREADS);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
   if (aa.debug)
-    k_match_tc<K, true><<<grid, NTHREADS, C::SMEM, s>>>(map, P, Rv, aa);
+    FIC_CUDA(cudaLaunchKernelEx(&cfg, k_match_tc<K, CG, true>, map, P, Rv, aa));
   else
-    k_match_tc<K, false><<<grid, NTHREADS, C::SMEM, s>>>(map, P, Rv, aa);
+    FIC_CUDA(cudaLaunchKernelEx(&cfg, k_match_tc<K, CG, false>, map, P, Rv, aa));
   FIC_CHECK_LAUNCH();
 }
 
 void launch_tc(const PoolView& P, const RangeView& Rv, const TcArgs& a, cudaStream_t s) {
   if (a.n_items == 0) return;
-  if (Rv.K == 64)
-    launch_tc_k<64>(P, Rv, a, s);
+  if (Rv.K == 64 && tc_cg(64) == 2)
+    launch_tc_k<64, 2>(P, Rv, a, s);
+  else if (Rv.K == 64)
+    launch_tc_k<64, 1>(P, Rv, a, s);
   else if (Rv.K == 16)
-    launch_tc_k<16>(P, Rv, a, s);
+    launch_tc_k<16, 1>(P, Rv, a, s);
   else
     invalid("tensor matcher supports range_size 4 and 8");
 }

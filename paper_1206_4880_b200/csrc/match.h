@@ -54,6 +54,7 @@ struct TcArgs {
   unsigned long long* dbg;     // timeline buffer (debug & 32)
 };
 bool tc_supported(int K);
+int tc_tile_rows(int K);
 void launch_tc(const PoolView& P, const RangeView& Rv, const TcArgs& a, cudaStream_t s);
 
 // Merge partial bests into records + RMS (codec.py:259-264, 399-405).

@@ -1,1 +1,1 @@
-FIC_TC_DEBUG=40 timeout 60 python tools/prof_encode.py 2>&1 | tail -22
+for cg in 1 2; do FIC_TC_CG=$cg timeout 60 python tools/prof_encode.py; FIC_TC_CG=$cg timeout 60 python tools/prof_encode.py; done
