@@ -491,8 +491,12 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
   // K1 pool builder
   PoolArgs pa{};
   pa.img = img;
+  pa.H = g.H;
   pa.W = g.W;
   pa.rs = g.rs;
+  pa.plane_rows = g.H - 1;
+  pa.pitch = (int)align_up((size_t)(g.W / 2 + 16), 16);
+  pa.planes = sc.get<uint8_t>((size_t)2 * pa.plane_rows * pa.pitch);
   pa.st = g.st;
   pa.ndx = g.ndx;
   pa.D = g.D;

@@ -287,6 +287,28 @@ void launch_slabs(const SlabArgs& a, cudaStream_t s) {
 // B_k = (K d_k - sum_d) / sqrt(K den) that the tensor-core screen consumes.
 // ============================================================================
 
+// Box-floor planes: plane[par][y][k] = (I[y][x] + I[y][x+1] + I[y+1][x] +
+// I[y+1][x+1]) >> 2 with x = 2k + par.  A decimated domain row (blocks.py:
+// 75-82) is then RS consecutive bytes of one plane row, so a domain is RS
+// short row reads from a 2 x (H-1) x W/2 byte array that stays in L2.
+__global__ void k_boxplanes(const uint8_t* img, int H, int W, int pitch, uint8_t* planes) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int64_t n = (int64_t)(H - 1) * (W - 1);
+  if (t >= n) return;
+  int y = (int)(t / (W - 1)), x = (int)(t - (int64_t)y * (W - 1));
+  const uint8_t* q = img + (int64_t)y * W + x;
+  uint8_t v = (uint8_t)((q[0] + q[1] + q[W] + q[W + 1]) >> 2);
+  planes[((int64_t)(x & 1) * (H - 1) + y) * pitch + (x >> 1)] = v;
+}
+
+// 8 bytes starting at byte offset k of an 8-byte aligned, padded row
+__device__ __forceinline__ unsigned long long bytes8(const uint8_t* row, int k) {
+  const unsigned long long* w = reinterpret_cast<const unsigned long long*>(row) + (k >> 3);
+  const int sh = (k & 7) * 8;
+  unsigned long long lo = __ldg(w), hi = __ldg(w + 1);
+  return sh ? ((lo >> sh) | (hi << (64 - sh))) : lo;
+}
+
 template <int RS>
 __global__ void __launch_bounds__(256) k_pool(PoolArgs a) {
   constexpr int K = RS * RS;
@@ -294,39 +316,49 @@ __global__ void __launch_bounds__(256) k_pool(PoolArgs a) {
   if (p >= a.D) return;
   uint32_t id = a.order ? a.order[p] : (uint32_t)p;
   int dy = (int)(id / (uint32_t)a.ndx), dx = (int)(id - (uint32_t)dy * a.ndx);
-  const uint8_t* base = a.img + (int64_t)dy * a.st * a.W + (int64_t)dx * a.st;
-  uint8_t v[K];
+  const int Y = dy * a.st, X = dx * a.st;
+  const uint8_t* plane = a.planes + (int64_t)(X & 1) * a.plane_rows * a.pitch;
+  uint32_t w[K / 4];
   uint32_t sd = 0, sdd = 0;
 #pragma unroll
   for (int i = 0; i < RS; ++i) {
-    const uint8_t* r0 = base + (int64_t)(2 * i) * a.W;
-    const uint8_t* r1 = r0 + a.W;
+    unsigned long long r8 = bytes8(plane + (int64_t)(Y + 2 * i) * a.pitch, X >> 1);
 #pragma unroll
     for (int j = 0; j < RS; ++j) {
-      uint32_t x = (r0[2 * j] + r0[2 * j + 1] + r1[2 * j] + r1[2 * j + 1]) >> 2;
-      v[i * RS + j] = (uint8_t)x;
+      uint32_t x = (uint32_t)(r8 >> (8 * j)) & 255u;
       sd += x;
       sdd += x * x;
+    }
+    if (RS == 8) {
+      w[2 * i] = (uint32_t)r8;
+      w[2 * i + 1] = (uint32_t)(r8 >> 32);
+    } else {
+      w[i] = (uint32_t)r8;
     }
   }
   int64_t den = (int64_t)K * sdd - (int64_t)sd * sd;
   a.inv_den[p] = den != 0 ? __ddiv_rn(1.0, (double)den) : 0.0;
   a.sums[p] = make_uint2(sd, sdd);
   a.ids[p] = id;
-  // raw bytes
-  uint32_t* rw = reinterpret_cast<uint32_t*>(a.raw + p * K);
+  uint4* rw = reinterpret_cast<uint4*>(a.raw + p * K);
 #pragma unroll
-  for (int q = 0; q < K / 4; ++q)
-    rw[q] = v[4 * q] | (v[4 * q + 1] << 8) | (v[4 * q + 2] << 16) | ((uint32_t)v[4 * q + 3] << 24);
+  for (int q = 0; q < K / 16; ++q) rw[q] = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
   if (a.bh) {
-    double scale = den > 0 ? __drcp_rn(__dsqrt_rn((double)K * (double)den)) : 0.0;
-    uint32_t* bw = reinterpret_cast<uint32_t*>(a.bh + p * K);
+    const double scale = den > 0 ? __drcp_rn(__dsqrt_rn((double)K * (double)den)) : 0.0;
+    uint4* bw = reinterpret_cast<uint4*>(a.bh + p * K);
 #pragma unroll
-    for (int q = 0; q < K / 2; ++q) {
-      float f0 = (float)(((double)((int)K * v[2 * q] - (int)sd)) * scale);
-      float f1 = (float)(((double)((int)K * v[2 * q + 1] - (int)sd)) * scale);
-      __half2 h = __floats2half2_rn(f0, f1);
-      bw[q] = *reinterpret_cast<uint32_t*>(&h);
+    for (int q = 0; q < K / 8; ++q) {
+      uint32_t h[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int k0 = 8 * q + 2 * e;
+        const int v0 = (w[k0 >> 2] >> (8 * (k0 & 3))) & 255, v1 = (w[(k0 + 1) >> 2] >> (8 * ((k0 + 1) & 3))) & 255;
+        const float f0 = (float)((double)(K * v0 - (int)sd) * scale);
+        const float f1 = (float)((double)(K * v1 - (int)sd) * scale);
+        __half2 hv = __floats2half2_rn(f0, f1);
+        h[e] = *reinterpret_cast<uint32_t*>(&hv);
+      }
+      bw[q] = make_uint4(h[0], h[1], h[2], h[3]);
     }
   }
 }
@@ -356,12 +388,17 @@ __global__ void k_pool_generic(PoolArgs a, int rs) {
 void launch_pool(const PoolArgs& a, cudaStream_t s) {
   if (a.D == 0) return;
   unsigned blocks = (unsigned)cdiv(a.D, 256);
-  if (a.rs == 8)
-    k_pool<8><<<blocks, 256, 0, s>>>(a);
-  else if (a.rs == 4)
-    k_pool<4><<<blocks, 256, 0, s>>>(a);
-  else
+  if ((a.rs == 8 || a.rs == 4) && a.planes) {
+    const int64_t n = (int64_t)(a.H - 1) * (a.W - 1);
+    k_boxplanes<<<(unsigned)cdiv(n, 256), 256, 0, s>>>(a.img, a.H, a.W, a.pitch, a.planes);
+    FIC_CHECK_LAUNCH();
+    if (a.rs == 8)
+      k_pool<8><<<blocks, 256, 0, s>>>(a);
+    else
+      k_pool<4><<<blocks, 256, 0, s>>>(a);
+  } else {
     k_pool_generic<<<blocks, 256, 0, s>>>(a, a.rs);
+  }
   FIC_CHECK_LAUNCH();
 }
 
@@ -398,9 +435,60 @@ __global__ void k_ranges(RangeArgs a) {
     }
 }
 
+// RS = 8 fast path: one thread per (range, isometry); rows are aligned 8-byte
+// loads, the permutation table lives in shared memory.
+__global__ void __launch_bounds__(256) k_ranges8(RangeArgs a) {
+  __shared__ uint8_t perm[8 * 64];
+  for (int i = threadIdx.x; i < a.n_iso * 64; i += blockDim.x) perm[i] = (uint8_t)a.inv_perm[i];
+  __syncthreads();
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)a.R * a.n_iso) return;
+  const int r = (int)(t / a.n_iso), iso = (int)(t - (int64_t)r * a.n_iso);
+  const int ry = r / a.nrx, rx = r - ry * a.nrx;
+  const uint8_t* base = a.img + (int64_t)ry * 8 * a.W + (int64_t)rx * 8;
+  uint8_t px[64];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    unsigned long long v = __ldg(reinterpret_cast<const unsigned long long*>(base + (int64_t)i * a.W));
+#pragma unroll
+    for (int j = 0; j < 8; ++j) px[8 * i + j] = (uint8_t)(v >> (8 * j));
+  }
+  if (iso == 0) {
+    int64_t sr = 0, srr = 0;
+#pragma unroll
+    for (int k = 0; k < 64; ++k) {
+      sr += px[k];
+      srr += px[k] * px[k];
+    }
+    RangeInfo inf;
+    inf.sr = (double)sr;
+    inf.srr = (double)srr;
+    inf.V = __dsub_rn((double)srr, __ddiv_rn((double)sr * (double)sr, 64.0));
+    inf.rho = (int32_t)((2 * sr + 64) / 128);
+    inf.pad = 0;
+    a.info[r] = inf;
+  }
+  uint4* out = reinterpret_cast<uint4*>(a.rows + ((int64_t)r * a.n_iso + iso) * 64);
+  const uint8_t* pm = perm + iso * 64;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    uint32_t w[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int k = 16 * q + 4 * e;
+      w[e] = px[pm[k]] | (px[pm[k + 1]] << 8) | (px[pm[k + 2]] << 16) | ((uint32_t)px[pm[k + 3]] << 24);
+    }
+    out[q] = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+}
+
 void launch_ranges(const RangeArgs& a, cudaStream_t s) {
   if (a.R == 0) return;
-  k_ranges<<<(unsigned)cdiv(a.R, 128), 128, 0, s>>>(a);
+  if (a.rs == 8 && a.W % 8 == 0) {
+    k_ranges8<<<(unsigned)cdiv((int64_t)a.R * a.n_iso, 256), 256, 0, s>>>(a);
+  } else {
+    k_ranges<<<(unsigned)cdiv(a.R, 128), 128, 0, s>>>(a);
+  }
   FIC_CHECK_LAUNCH();
 }
 

@@ -50,7 +50,9 @@ void launch_slabs(const SlabArgs& a, cudaStream_t s);
 // ---- K1: pool builder (blocks.py:75-82, codec.py:136-145) -------------------
 struct PoolArgs {
   const uint8_t* img;
-  int W, rs, st, ndx;
+  int H, W, rs, st, ndx;
+  uint8_t* planes;         // [2][plane_rows][pitch] box-floor planes (scratch)
+  int plane_rows, pitch;
   int64_t D;
   const uint32_t* order;   // raster id per pool position (nullptr = identity)
   uint8_t* raw;            // [D][K] decimated pixels, pool order
