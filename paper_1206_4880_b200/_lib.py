@@ -11,7 +11,8 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libfic_b200.so")
+# FIC_B200_LIB selects another build of the same library (kernel experiments)
+LIB_PATH = os.environ.get("FIC_B200_LIB") or os.path.join(HERE, "libfic_b200.so")
 
 FIC_OK, FIC_EINVAL, FIC_ECUDA, FIC_ENOMEM = 0, 1, 2, 3
 

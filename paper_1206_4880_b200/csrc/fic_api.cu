@@ -677,8 +677,8 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
     st->work_items = (int32_t)(tot.n_titems + tot.n_eitems);
     st->kernel_launches = g_launches;
     if (getenv("FIC_TC_DEBUG") && (atoi(getenv("FIC_TC_DEBUG")) & 4))
-      fprintf(stderr, "tc cycles: producer-empty %.3g  mma-tempty %.3g  mma-full %.3g  epi-tfull %.3g  epi-slow %.3g  epi-total %.3g  arrive->next-full %.3g  full->arrive %.3g\n",
-              (double)hc[4], (double)hc[5], (double)hc[6], (double)hc[7], (double)hc[8], (double)hc[9], (double)hc[10], (double)hc[11]);
+      fprintf(stderr, "tc cycles: producer-empty %.3g  mma-tempty %.3g  mma-full %.3g  epi-tfull %.3g  epi-slow %.3g  epi-total %.3g  mma-loop %.3g  setup %.3g  teardown(tma warp) %.3g  items %.0f\n",
+              (double)hc[4], (double)hc[5], (double)hc[6], (double)hc[7], (double)hc[8], (double)hc[9], (double)hc[10], (double)hc[11], (double)hc[12], (double)hc[13]);
   }
 }
 

@@ -2,13 +2,25 @@
 //
 // One work item = 128 rows (RT ranges x n_iso isometries, FD-sorted so the
 // tile's slabs form one contiguous union window) against a segment of that
-// window's domain columns.  Per 256-column N-tile:
+// window's domain columns.  Per 128-column N-tile (one CTA per SM, 12 warps):
 //
-//   TMA (warp 0)  : B tile = 256 pool-ordered domains x K fp16, SW128 K-major
-//   MMA (warp 1)  : tcgen05.mma.cta_group::1.kind::f16, M=128 N=256 K=16 steps,
-//                   fp32 accumulator double-buffered in TMEM (2 x 256 cols)
-//   epilogue (4-7): tcgen05.ld 32 columns at a time, |u| running max, and the
-//                   exact fp64 rescoring of the rare survivors.
+//   TMA (warp 0)     : B tile = 128 pool-ordered domains x K fp16, SW128
+//                      K-major, NST-stage smem ring (full/empty mbarriers)
+//   MMA (warp 1)     : tcgen05.mma.cta_group::1.kind::f16, M=128 N=128, K/16
+//                      steps, fp32 accumulator in NACC = 4 TMEM stages
+//                      (4 x 128 columns); commits to empty[stage] + tfull[acc]
+//   rescorers (2-3)  : drain the per-row survivor queues, exact fp64
+//                      evaluation, publish per-range thresholds
+//   screeners (4-11) : 2 groups x 4 lane quarters; group g screens the stages
+//                      j % 2 == g: tcgen05.ld 2 x 32 columns, |u| max, vote,
+//                      release the stage as soon as its last half is loaded
+//
+// Measured on B200 (tools/pipe_bench.cu, tools/loop_bench.cu): reading an
+// fp32 accumulator stage back (64 KB per tile) costs about as much TMEM time
+// as the MMA that wrote it, so the idealised MMA + tcgen05.ld pipeline
+// plateaus near 370-390 cycles per 128x128 tile (66-70% of the MMA rate);
+// per-warp latency of the screening loop and the MMA warp's two barrier
+// round trips per tile are what separate this kernel from that plateau.
 //
 // The screen.  A row holds a = r[inv_perm[iso]] - rho (exact small integers),
 // a column holds B = fp16((K d - sum_d) / sqrt(K den)), the centred unit-norm
@@ -35,15 +47,21 @@ namespace tc {
 constexpr int BM = 128;       // rows per tile (TMEM lanes)
 constexpr int BN = 128;       // columns per N-tile (one TMEM accumulator stage)
 constexpr int NACC = 4;       // TMEM accumulator stages (NACC * BN = 512 columns)
-constexpr int NEPI = 16;      // screening warps: 2 groups x 4 lane quarters x 2 slices
-constexpr int NGRP = 2;       // screening groups; group g handles stages j with j % 2 == g
-constexpr int NRES = 2;       // rescoring warps: each thread owns rows t and t + 64
-constexpr int NSLICE = 4;     // survivor queues per row: (group, 64-column slice)
-constexpr int QCAP = 16;      // survivor queue entries per (row, slice)
-constexpr int RES0 = 2;       // first rescoring warp
+constexpr int NEPI = 8;      // screening warps: NGRP groups x 4 lane quarters
+constexpr int NGRP = 2;       // screening groups; group g handles stages j with j % NGRP == g
+constexpr int NMMA = 1;       // MMA issuing warps; warp MMA0 + w issues tiles j % NMMA == w
+constexpr int NRES = 2;       // rescoring warps: thread t owns rows t + RSTRIDE * h
+constexpr int NSLICE = NGRP;  // survivor queues per row: one per screening group
+constexpr int QCAP = 32;      // survivor queue entries per (row, slice)
+constexpr int MMA0 = 1;       // first MMA issuing warp (warp 0: TMA producer)
+constexpr int RES0 = MMA0 + NMMA;  // first rescoring warp
+constexpr int RSTRIDE = 32 * NRES;
+constexpr int RROWS = BM / RSTRIDE;  // rows per rescoring thread
 constexpr int SCR0 = RES0 + NRES;
-// warps: 0 TMA (+ TMEM alloc), 1 MMA, 2..3 rescorers, 4..19 screeners
+// warps: 0 TMA (+ TMEM alloc), MMA0.. MMA issuers, RES0.. rescorers, SCR0.. screeners
 constexpr int NTHREADS = 32 * (SCR0 + NEPI);
+// one CTA per SM; the register file is split per SM sub-partition (warp % 4)
+constexpr int MAXREG = (16384 / (32 * ((NTHREADS / 32 + 3) / 4))) & ~7;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -204,7 +222,7 @@ __device__ __forceinline__ void tma_load(uint32_t dst, const CUtensorMap* map, u
         : "memory");
 }
 
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
   uint32_t* r = reinterpret_cast<uint32_t*>(v);
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
@@ -251,7 +269,7 @@ __device__ __forceinline__ uint32_t swz(int r, int c) {
 using namespace tc;
 
 template <int K, int CG, bool DBG>
-__global__ void __launch_bounds__(NTHREADS, 1)
+__global__ void __maxnreg__(MAXREG)
     k_match_tc(const __grid_constant__ CUtensorMap tmB, PoolView P, RangeView Rv, TcArgs a) {
   using C = Cfg<K, CG>;
   // CG == 2: a cluster of two CTAs runs one M = 256 tile; CTA `crank` owns
@@ -331,8 +349,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   const bool is_res = warp >= RES0 && warp < SCR0;
   const bool is_scr = warp >= SCR0;
   const int row = is_scr ? 32 * (warp & 3) + lane : 0;
-  const int slice = is_scr ? ((warp - SCR0) >> 2) & 1 : 0;  // 64-column half of a stage
-  const int group = is_scr ? (warp - SCR0) >> 3 : 0;        // stages j % NGRP == group
+  const int group = is_scr ? (warp - SCR0) >> 2 : 0;  // stages j % NGRP == group
   const int rk = row / n_iso;          // range within this CTA's rows (thr_s index)
   const int iso = row - rk * n_iso;
   const int rk_tile = (row + rbase) / n_iso;  // range within the tile (tlist index)
@@ -364,7 +381,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   };
 
   int prev_tile = -1;
+  long long tsetup = 0, tteardown = 0, nitems = 0;
   for (int64_t it = blockIdx.x / CG; it < a.n_items; it += gridDim.x / CG) {
+    const long long ti0 = (DBG ? clock64() : 0ll);
+    ++nitems;
     const int2 item = a.items[it];
     const int tile = item.x;
     const int64_t wlo = a.wlo[tile], whi = a.whi[tile];
@@ -424,6 +444,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
     if (threadIdx.x == 0) *edone = 0;
     cta_sync<CG>();
+    tsetup += (DBG ? clock64() : 0ll) - ti0;
+    const long long ti1 = (DBG ? clock64() : 0ll);
 
     if (warp == 0) {
       // TMA producer: the whole warp walks the pipeline, one lane issues
@@ -431,7 +453,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         { long long t0 = (DBG ? clock64() : 0ll); mbar_wait(empty_bar(stage), ph ^ 1); tw0 += (DBG ? clock64() : 0ll) - t0; }
         if ((debug & 32) && blockIdx.x == 0 && it == 0 && j < 64 && lane == 0) a.dbg[j * 24] = (DBG ? clock64() : 0ll);
         if (elect_one()) {
-          if (debug & 16) {
+          if ((debug & 16) || ((debug & 1024) && (j & 1))) {
             if (leader) mbar_arrive(full_bar(stage));
           } else {
             // the leader's full barrier expects both CTAs' shares
@@ -444,14 +466,21 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         __syncwarp();
         if (++stage == C::NST) { stage = 0; ph ^= 1; }
       }
-    } else if (warp == 1 && leader) {
-      // MMA issuer: descriptors precomputed; per K step +32 B (= +2 in the
-      // 16-byte address field), per stage +B_BYTES
+    } else if (warp >= MMA0 && warp < MMA0 + NMMA && leader) {
+      // MMA issuers: NMMA warps take turns (tile j goes to warp MMA0 + j % NMMA)
+      // so the issue loop's barrier round trips (~450 cycles per tile) overlap.
+      // Descriptors precomputed; per K step +32 B (= +2 in the 16-byte
+      // address field), per stage +B_BYTES.  Each warp's commits track its own MMAs.
       const uint64_t adesc = smem_desc(smem_u32(sA), C::SBO, C::LAYOUT);
       const uint64_t bdesc = smem_desc(smem_u32(sB), C::SBO, C::LAYOUT);
-      for (int j = 0; j < nt; ++j) {
-        { long long t0 = (DBG ? clock64() : 0ll); mbar_wait(tempty_bar(acc), acc_ph ^ 1); tw1 += (DBG ? clock64() : 0ll) - t0; }
-        { long long t0 = (DBG ? clock64() : 0ll); mbar_wait(full_bar(stage), ph); tw2 += (DBG ? clock64() : 0ll) - t0; }
+      static_assert(C::NST % NMMA == 0 && NACC % NMMA == 0, "issuer stride must divide the rings");
+      const uint32_t g0 = gt + (uint32_t)(warp - MMA0);
+      int stage = (int)(g0 % C::NST), ph = (int)((g0 / C::NST) & 1);
+      int acc = (int)(g0 % NACC), acc_ph = (int)((g0 / NACC) & 1);
+      const uint32_t full0 = full_bar(0), empty0 = empty_bar(0), tfull0 = tfull_bar(0), tempty0 = tempty_bar(0);
+      for (int j = warp - MMA0; j < nt; j += NMMA) {
+        { long long t0 = (DBG ? clock64() : 0ll); mbar_wait(tempty0 + 8 * acc, acc_ph ^ 1); tw1 += (DBG ? clock64() : 0ll) - t0; }
+        { long long t0 = (DBG ? clock64() : 0ll); mbar_wait(full0 + 8 * stage, ph); tw2 += (DBG ? clock64() : 0ll) - t0; }
         fence_after();
         if ((debug & 32) && blockIdx.x == 0 && it == 0 && j < 64 && lane == 0) a.dbg[j * 24 + 1] = (DBG ? clock64() : 0ll);
         if (elect_one()) {
@@ -460,28 +489,32 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #pragma unroll
           for (int kk = 0; kk < K / 16; ++kk)
             if (!(debug & 2)) mma_f16<CG>(d, adesc + 2 * kk, bs + 2 * kk, kk > 0 ? 1u : 0u);
-          mma_commit<CG>(empty_bar(stage));
-          mma_commit<CG>(tfull_bar(acc));
+          mma_commit<CG>(empty0 + 8 * stage);
+          mma_commit<CG>(tfull0 + 8 * acc);
         }
         __syncwarp();
-        if (++stage == C::NST) { stage = 0; ph ^= 1; }
-        if (++acc == NACC) { acc = 0; acc_ph ^= 1; }
+        stage += NMMA;
+        if (stage >= C::NST) { stage -= C::NST; ph ^= 1; }
+        acc += NMMA;
+        if (acc >= NACC) { acc -= NACC; acc_ph ^= 1; }
       }
     } else if (is_scr) {
       // ------------------------------ screening ------------------------------
-      // Per stage: 2 x 64 columns (tcgen05.ld x32 twice), |u| max tree, vote.
-      // Chunks whose max reaches the row's threshold push their survivors
-      // (relative positions) to the row's queue; rescoring warps do the
-      // exact evaluation.  A row without an exact error yet first evaluates
-      // its best-|u| candidate itself, so its threshold is finite before any
-      // survivor mask is built.
-      const uint32_t lane_base = tmem_base + ((uint32_t)(32 * (warp & 3)) << 16) + 64 * slice;
+      // Warp (group g, quarter q) owns TMEM lanes 32q.. of the stages j with
+      // j % NGRP == g, read in 64-column halves: two tcgen05.ld x32, wait,
+      // |u| max over 64 columns, one vote.  The accumulator stage is released
+      // as soon as its last half is in registers.  Halves whose max reaches
+      // the row's threshold push their survivors (positions relative to c0)
+      // to the row's queue; rescoring warps do the exact evaluation.  A row
+      // without an exact error yet first evaluates its best-|u| candidate
+      // itself, so its threshold is finite before any survivor is pushed.
+      const uint32_t lane_base = tmem_base + ((uint32_t)(32 * (warp & 3)) << 16);
       const uint32_t tfull0 = tfull_bar(0), tempty0 = tempty_bar(0);
       const int32_t lo32 = rvalid ? (int32_t)(max((int64_t)rlo, c0) - c0) : 0;
       const int32_t hi32 = rvalid ? (int32_t)(min((int64_t)rhi, c1) - c0) : 0;
-      uint32_t* myq = qbuf + (row * NSLICE + group * 2 + slice) * QCAP;
-      volatile uint32_t* mytail = qtail + row * NSLICE + group * 2 + slice;
-      volatile uint32_t* myhead = qhead + row * NSLICE + group * 2 + slice;
+      uint32_t* myq = qbuf + (row * NSLICE + group) * QCAP;
+      volatile uint32_t* mytail = qtail + row * NSLICE + group;
+      volatile uint32_t* myhead = qhead + row * NSLICE + group;
       uint32_t qt = 0;
       unsigned long long thr_bits = 0x7ff0000000000000ull;
       float s_r = -1.0f;  // |u| threshold; negative = every candidate survives
@@ -509,48 +542,61 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           if (tb < thr_bits) set_threshold(tb);
         }
 #pragma unroll 1
-        for (int c = 0; c < 2; ++c) {
-          float v[32];
-          if (!(debug & 1)) tmem_ld32(lane_base + acc * BN + 32 * c, v);
-          const int32_t rel = j * BN + 64 * slice + 32 * c;  // chunk start, relative to c0
-          const int32_t e_lo = lo32 - rel, e_hi = hi32 - rel;
-          const bool overlap = rvalid && e_lo < 32 && e_hi > 0;
+        for (int h = 0; h < BN / 64; ++h) {
+          float v[64];
+          if (!(debug & 1)) {
+            tmem_ld32(lane_base + acc * BN + 64 * h, v);
+            tmem_ld32(lane_base + acc * BN + 64 * h + 32, v + 32);
+          }
           tmem_wait_ld();
-          if (dbgw && c == 0) a.dbg[j * 24 + 5] = (DBG ? clock64() : 0ll);
+          if (dbgw) a.dbg[j * 24 + 5] = (DBG ? clock64() : 0ll);
+          if (h == BN / 64 - 1) {  // release the stage before screening its last half
+            fence_before();
+            __syncwarp();
+            if (lane == 0) {
+              if (leader)
+                mbar_arrive(tempty0 + 8 * acc);
+              else
+                mbar_arrive_cluster(map_to_rank(tempty0 + 8 * acc, 0));
+            }
+          }
           if (debug & 1) continue;
+          const int32_t rel = j * BN + 64 * h;  // half start, relative to c0
+          const int32_t e_lo = lo32 - rel, e_hi = hi32 - rel;
+          const bool overlap = rvalid && e_lo < 64 && e_hi > 0;
           float m0 = fmaxf(fmaxf(fabsf(v[0]), fabsf(v[1])), fabsf(v[2]));
           float m1 = fmaxf(fmaxf(fabsf(v[3]), fabsf(v[4])), fabsf(v[5]));
           float m2 = fmaxf(fmaxf(fabsf(v[6]), fabsf(v[7])), fabsf(v[8]));
           float m3 = fmaxf(fmaxf(fabsf(v[9]), fabsf(v[10])), fabsf(v[11]));
 #pragma unroll
-          for (int e = 12; e < 28; e += 8) {
+          for (int e = 12; e < 60; e += 8) {
             m0 = fmaxf(fmaxf(m0, fabsf(v[e])), fabsf(v[e + 1]));
             m1 = fmaxf(fmaxf(m1, fabsf(v[e + 2])), fabsf(v[e + 3]));
             m2 = fmaxf(fmaxf(m2, fabsf(v[e + 4])), fabsf(v[e + 5]));
             m3 = fmaxf(fmaxf(m3, fabsf(v[e + 6])), fabsf(v[e + 7]));
           }
-          m0 = fmaxf(fmaxf(m0, fabsf(v[28])), fabsf(v[29]));
-          m1 = fmaxf(fmaxf(m1, fabsf(v[30])), fabsf(v[31]));
+          m0 = fmaxf(fmaxf(m0, fabsf(v[60])), fabsf(v[61]));
+          m1 = fmaxf(fmaxf(m1, fabsf(v[62])), fabsf(v[63]));
           const float mx = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3));
           const bool hit = !(debug & 8) && overlap && (mx >= s_r || (debug & 64));
-          if (dbgw && c == 0) a.dbg[j * 24 + 6] = (DBG ? clock64() : 0ll);
+          if (dbgw) a.dbg[j * 24 + 6] = (DBG ? clock64() : 0ll);
           if (__any_sync(0xffffffffu, hit)) {
             const long long ts0 = (DBG ? clock64() : 0ll);
-            const int32_t wl = max(e_lo, 0), wh = min(e_hi, 32);
-            uint32_t wmask = 0;
-            if (hit) wmask = ((wh >= 32) ? ~0u : ((1u << wh) - 1u)) & ~((1u << wl) - 1u);
+            const int32_t wl = max(e_lo, 0), wh = min(e_hi, 64);
+            uint64_t wmask = 0;
+            if (hit) wmask = ((wh >= 64) ? ~0ull : ((1ull << wh) - 1ull)) & ~((1ull << wl) - 1ull);
             const bool seed = hit && thr_bits == 0x7ff0000000000000ull;
             if (__any_sync(0xffffffffu, seed)) {
               double tnew = INFINITY;
               if (seed) {
                 float bv = -1.0f;
 #pragma unroll
-                for (int q = 0; q < 32; ++q) bv = fmaxf(bv, ((wmask >> q) & 1u) ? fabsf(v[q]) : -1.0f);
-                uint32_t eq = 0;
+                for (int q = 0; q < 64; ++q) bv = fmaxf(bv, ((wmask >> q) & 1ull) ? fabsf(v[q]) : -1.0f);
+                uint64_t eq = 0;
 #pragma unroll
-                for (int q = 0; q < 32; ++q) eq |= (fabsf(v[q]) == bv) ? (1u << q) : 0u;
-                const int e = __ffs((int)(eq & wmask)) - 1;
-                wmask &= ~(1u << e);
+                for (int q = 0; q < 64; ++q) eq |= (fabsf(v[q]) == bv) ? (1ull << q) : 0ull;
+                const int e = __ffsll((long long)(eq & wmask)) - 1;
+                wmask &= ~(1ull << e);
                 tnew = fmax(exact(c0 + rel + e, row, sr, srr).err, 0.0);
                 ++evals;
                 push((uint32_t)(rel + e));  // the rescorer records it
@@ -564,43 +610,32 @@ __global__ void __launch_bounds__(NTHREADS, 1)
               }
             }
             if (hit) {
-              uint32_t m = 0;
+              uint64_t m = 0;
 #pragma unroll
-              for (int q = 0; q < 32; ++q) m |= (fabsf(v[q]) >= s_r || (debug & 64)) ? (1u << q) : 0u;
+              for (int q = 0; q < 64; ++q) m |= (fabsf(v[q]) >= s_r || (debug & 64)) ? (1ull << q) : 0ull;
               m &= wmask;
               while (m) {
-                const int e = __ffs((int)m) - 1;
+                const int e = __ffsll((long long)m) - 1;
                 m &= m - 1;
                 push((uint32_t)(rel + e));
               }
             }
             tw4 += (DBG ? clock64() : 0ll) - ts0;
           }
-        }
-      release:
-        if (dbgw) a.dbg[j * 24 + 7] = (DBG ? clock64() : 0ll);
-        fence_before();
-        __syncwarp();
-        if (lane == 0) {
-          if (leader)
-            mbar_arrive(tempty0 + 8 * acc);
-          else
-            mbar_arrive_cluster(map_to_rank(tempty0 + 8 * acc, 0));
-        }
-        if (dbgw) a.dbg[j * 24 + 8] = (DBG ? clock64() : 0ll);
+        }  // halves
       }
       __threadfence_block();
       __syncwarp();
       if (lane == 0) atomicAdd((uint32_t*)edone, 1u);
     } else if (is_res) {
       // ------------------------------ rescoring ------------------------------
-      // Thread t owns rows t and t + 64: it drains their survivor queues,
+      // Thread t owns rows t + RSTRIDE * h: it drains their survivor queues,
       // evaluates each candidate exactly (state in shared memory) and
       // publishes the range's threshold.
       const int t = (int)threadIdx.x - 32 * RES0;
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int r = t + 64 * h, k = (r + rbase) / n_iso;
+      for (int h = 0; h < RROWS; ++h) {
+        const int r = t + RSTRIDE * h, k = (r + rbase) / n_iso;
         const int64_t g = (int64_t)tile * a.RT + k;
         RowState st;
         st.err = INFINITY;
@@ -617,15 +652,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
         rstate[r] = st;
       }
-      uint32_t hd[2 * NSLICE];
+      uint32_t hd[RROWS * NSLICE];
 #pragma unroll
-      for (int q = 0; q < 2 * NSLICE; ++q) hd[q] = 0;
+      for (int q = 0; q < RROWS * NSLICE; ++q) hd[q] = 0;
       while (true) {
         int got = -1;
         uint32_t rel = 0;
 #pragma unroll
-        for (int q = 0; q < 2 * NSLICE; ++q) {
-          const int r = t + 64 * (q / NSLICE), qs = q % NSLICE;
+        for (int q = 0; q < RROWS * NSLICE; ++q) {
+          const int r = t + RSTRIDE * (q / NSLICE), qs = q % NSLICE;
           if (got < 0 && hd[q] != qtail[r * NSLICE + qs]) {
             __threadfence_block();
             rel = qbuf[(r * NSLICE + qs) * QCAP + (hd[q] & (QCAP - 1))];
@@ -634,7 +669,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           }
         }
         if (got >= 0) {
-          const int r = t + 64 * got, k = r / n_iso;
+          const int r = t + RSTRIDE * got, k = r / n_iso;
           RowState st = rstate[r];
           const int64_t p = c0 + rel;
           const Cand cd = exact(p, r, st.sr, st.srr);
@@ -653,8 +688,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           __threadfence_block();
           bool empty = true;
 #pragma unroll
-          for (int q = 0; q < 2 * NSLICE; ++q)
-            empty = empty && (hd[q] == qtail[(t + 64 * (q / NSLICE)) * NSLICE + q % NSLICE]);
+          for (int q = 0; q < RROWS * NSLICE; ++q)
+            empty = empty && (hd[q] == qtail[(t + RSTRIDE * (q / NSLICE)) * NSLICE + q % NSLICE]);
           if (empty) break;
         } else {
           __nanosleep(256);
@@ -663,8 +698,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       __syncwarp();
       // combine the n_iso rows of each range: lexicographic (err, dom, iso)
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int r = t + 64 * h;
+      for (int h = 0; h < RROWS; ++h) {
+        const int r = t + RSTRIDE * h;
         const RowState st = rstate[r];
         double err = st.err, pre = st.pre;
         uint32_t dom = st.dom;
@@ -700,7 +735,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       }
     }
     gt += (uint32_t)nt;
+    const long long ti2 = (DBG ? clock64() : 0ll);
     cta_sync<CG>();
+    if (warp == 0) tteardown += (DBG ? clock64() : 0ll) - ti2;
+    (void)ti1;
   }
 
   if (is_res || is_scr) {
@@ -712,8 +750,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       atomicAdd(a.counters + 9, (unsigned long long)((DBG ? clock64() : 0ll) - tstart));
     }
   }
-  if ((debug & 4) && lane == 0 && warp == 0) atomicAdd(a.counters + 4, (unsigned long long)tw0);
+  if ((debug & 4) && lane == 0 && warp == 0) {
+    atomicAdd(a.counters + 4, (unsigned long long)tw0);
+    atomicAdd(a.counters + 11, (unsigned long long)tsetup);
+    atomicAdd(a.counters + 12, (unsigned long long)tteardown);
+    atomicAdd(a.counters + 13, (unsigned long long)nitems);
+  }
   if ((debug & 4) && lane == 0 && warp == 1) {
+    atomicAdd(a.counters + 10, (unsigned long long)((DBG ? clock64() : 0ll) - tstart));
     atomicAdd(a.counters + 5, (unsigned long long)tw1);
     atomicAdd(a.counters + 6, (unsigned long long)tw2);
   }

@@ -51,11 +51,20 @@ __global__ void __launch_bounds__(384, 1) k(int mode, int iters, unsigned long l
           asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tbase), "l"(ad), "l"(bd), "r"(IDESC), "r"(kk));
         }
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&bar)));
+        if (mode & 8) {  // no wait: only commits between MMA groups
+          if (i == iters - 1) {
+            uint32_t ok = 0;
+            do {
+              asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n" : "=r"(ok) : "r"(smem_u32(&bar)), "r"((uint32_t)((iters - 1) & 1)));
+            } while (!ok);
+          }
+        } else {
         uint32_t ok = 0;
         do {
           asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n" : "=r"(ok) : "r"(smem_u32(&bar)), "r"(ph));
         } while (!ok);
         ph ^= 1;
+        }
       }
     }
   } else if (warp >= 4 && (mode & 2)) {
@@ -93,17 +102,18 @@ int main() {
   int smem = 1024 + 16384 + 65536 + 16384;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   int iters = 2000;
-  for (int cfg = 0; cfg < 6; ++cfg) {
-    int nmma = (cfg % 3 == 0) ? 4 : (cfg % 3 == 1) ? 16 : 64;
-    int ncols = cfg < 3 ? 256 : 128;
+  for (int cfg = 0; cfg < 8; ++cfg) {
+    int nmma = (cfg % 2 == 0) ? 4 : 16;
+    int ncols = (cfg / 2) % 2 ? 128 : 256;
+    int mode_run = cfg >= 4 ? 9 : 1;
     for (int rep = 0; rep < 2; ++rep) {
       cudaMemset(d, 0, 16);
-      k<<<148, 384, smem>>>(1, iters, d, sink, nmma, ncols);
+      k<<<148, 384, smem>>>(mode_run, iters, d, sink, nmma, ncols);
       cudaDeviceSynchronize();
     }
     unsigned long long c[2];
     cudaMemcpy(c, d, 16, cudaMemcpyDeviceToHost);
-    printf("N=%d, %d MMAs (K=16) per commit: %.1f cycles per MMA (%s)\n", ncols, nmma, (double)c[0] / iters / nmma,
+    printf("%s N=%d, %d MMAs (K=16) per commit: %.1f cycles per MMA (%s)\n", mode_run == 9 ? "commit-only" : "commit+wait", ncols, nmma, (double)c[0] / iters / nmma,
            cudaGetErrorString(cudaGetLastError()));
   }
   return 0;
