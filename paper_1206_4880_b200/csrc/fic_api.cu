@@ -324,6 +324,10 @@ __global__ void k_expand(const int32_t* nseg, const int32_t* base, int64_t n, in
   for (int s = 0; s < nseg[t]; ++s) items[b + s] = make_int2((int)t, s);
 }
 
+__global__ void k_fill_u64(unsigned long long* a, unsigned long long v, int64_t n) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) a[i] = v;
+}
 __global__ void k_i32_to_i64(const int32_t* a, int64_t* o, int n) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) o[i] = a[i];
@@ -617,8 +621,11 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
   RangeView Rv{ra.info, ra.rows, pb.lo, pb.hi, g.n_iso, K};
   tm.mark();  // 3
   if (tot.n_titems) {
+    unsigned long long* thr_g = sc.get<unsigned long long>(g.R);
+    k_fill_u64<<<(unsigned)cdiv(g.R, 256), 256, 0, s>>>(thr_g, 0x7ff0000000000000ull, g.R);
+    FIC_CHECK_LAUNCH();
     TcArgs ta{titems, tot.n_titems, rid_s + tb, n_tr, wlo, whi, seg_t, RT, sbase, partials,
-              counters, 0, nullptr};
+              counters, thr_g, 0, nullptr};
     const char* dbg_env = getenv("FIC_TC_DEBUG");
     if (dbg_env && (atoi(dbg_env) & 32)) {
       ta.dbg = sc.get<unsigned long long>(64 * 24);

@@ -40,6 +40,10 @@
 
 #include "match.h"
 
+#ifndef FIC_TC_XP
+#define FIC_TC_XP 0
+#endif
+
 namespace fic {
 
 namespace tc {
@@ -277,8 +281,10 @@ __global__ void __maxnreg__(MAXREG)
   const uint32_t crank = (CG == 2) ? cluster_rank() : 0u;
   const bool leader = crank == 0;
   const int rbase = BM * (int)crank;
-  // timing experiments (FIC_TC_DEBUG) compile into a separate instantiation
-  const int debug = DBG ? a.debug : 0;
+  // timing experiments (FIC_TC_DEBUG) compile into a separate instantiation;
+  // FIC_TC_XP (compile-time, default 0) applies the same bits to the
+  // production instantiation for uninstrumented experiment builds
+  const int debug = DBG ? a.debug : FIC_TC_XP;
   extern __shared__ uint8_t smem_raw[];
   // 1024-byte aligned base, derived from smem_raw so accesses stay in the shared window
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -437,7 +443,12 @@ __global__ void __maxnreg__(MAXREG)
       }
       prev_tile = tile;
     }
-    if (threadIdx.x < BM) thr_s[threadIdx.x] = 0x7ff0000000000000ull;  // +inf
+    if (threadIdx.x < BM) {  // per-range thresholds: start from what other segments found
+      unsigned long long tb = 0x7ff0000000000000ull;  // +inf
+      const int64_t g = (int64_t)tile * a.RT + threadIdx.x;
+      if ((int)threadIdx.x < a.RT && g < a.n_tr) tb = a.thr_g[a.tlist[g]];
+      thr_s[threadIdx.x] = tb;
+    }
     for (int i = threadIdx.x; i < NSLICE * BM; i += NTHREADS) {
       qtail[i] = 0;
       qhead[i] = 0;
@@ -537,7 +548,7 @@ __global__ void __maxnreg__(MAXREG)
         const bool dbgw = (debug & 32) && blockIdx.x == 0 && it == 0 && j < 64 && lane == 0 && warp == SCR0;
         if (dbgw) a.dbg[j * 24 + 4] = (DBG ? clock64() : 0ll);
         fence_after();
-        {  // thresholds published by the rescorers
+        if (!(debug & 4096)) {  // thresholds published by the rescorers
           const unsigned long long tb = thr_s[rk];
           if (tb < thr_bits) set_threshold(tb);
         }
@@ -563,7 +574,7 @@ __global__ void __maxnreg__(MAXREG)
           if (debug & 1) continue;
           const int32_t rel = j * BN + 64 * h;  // half start, relative to c0
           const int32_t e_lo = lo32 - rel, e_hi = hi32 - rel;
-          const bool overlap = rvalid && e_lo < 64 && e_hi > 0;
+          const bool overlap = (debug & 4096) ? true : (rvalid && e_lo < 64 && e_hi > 0);
           float m0 = fmaxf(fmaxf(fabsf(v[0]), fabsf(v[1])), fabsf(v[2]));
           float m1 = fmaxf(fmaxf(fabsf(v[3]), fabsf(v[4])), fabsf(v[5]));
           float m2 = fmaxf(fmaxf(fabsf(v[6]), fabsf(v[7])), fabsf(v[8]));
@@ -606,10 +617,13 @@ __global__ void __maxnreg__(MAXREG)
               const unsigned long long tb = (unsigned long long)__double_as_longlong(tnew);
               if (tb < thr_bits) {
                 set_threshold(tb);
-                if (iso == 0 && rvalid) atomicMin(thr_s + rk, tb);
+                if (iso == 0 && rvalid) {
+                  atomicMin(thr_s + rk, tb);
+                  atomicMin(a.thr_g + rid, tb);
+                }
               }
             }
-            if (hit) {
+            if (hit && !(debug & 8192)) {
               uint64_t m = 0;
 #pragma unroll
               for (int q = 0; q < 64; ++q) m |= (fabsf(v[q]) >= s_r || (debug & 64)) ? (1ull << q) : 0ull;
@@ -682,7 +696,11 @@ __global__ void __maxnreg__(MAXREG)
             st.oq = (uint8_t)cd.oq;
           }
           rstate[r] = st;
-          atomicMin(thr_s + k, (unsigned long long)__double_as_longlong(fmax(cd.err, 0.0)));
+          const unsigned long long eb = (unsigned long long)__double_as_longlong(fmax(cd.err, 0.0));
+          if (eb < thr_s[k]) {  // an improvement: publish to the screeners and the other segments
+            atomicMin(thr_s + k, eb);
+            atomicMin(a.thr_g + a.tlist[(int64_t)tile * a.RT + (r + rbase) / n_iso], eb);
+          }
           ++evals;
         } else if (*edone == (uint32_t)NEPI) {
           __threadfence_block();

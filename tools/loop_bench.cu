@@ -45,14 +45,16 @@ __global__ void __launch_bounds__(640, 1) k(int iters, int nacc, int nwarps, uns
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tbase = holder;
-  const uint32_t idesc = (1u << 4) | ((uint32_t)(256 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+  const uint32_t idesc = (1u << 4) | ((uint32_t)((mode >= 16 ? 128 : 256) >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+  // two issuing warps (nwarps == 2): warp 1 + w takes iterations j % 2 == w
   const uint64_t adesc = smem_desc(smem_u32(base)), bdesc = smem_desc(smem_u32(base + 16384));
   const uint32_t bar0 = smem_u32(&bars[0]);
   unsigned long long sink = 0;
   long long t0 = clock64();
   if (warp >= 1 && warp < 1 + nwarps) {
     int s = 0;
-    for (int j = 0; j < iters; ++j) {
+    const bool split = mode >= 16 && nwarps > 1;
+    for (int j = split ? warp - 1 : 0; j < iters; j += split ? nwarps : 1) {
       switch (mode) {
         case 0: asm volatile("" ::: "memory"); break;
         case 1: __syncwarp(); break;
@@ -101,6 +103,74 @@ __global__ void __launch_bounds__(640, 1) k(int iters, int nacc, int nwarps, uns
           break;
         }
         case 14: sink += clock64(); break;
+        case 20: {  // 2 waits + 8 MMA N128 (two tiles) + 3 commits
+          uint32_t ok = 0;
+          do {
+            asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+                         : "=r"(ok) : "r"(bar0 + 48), "r"(1u) : "memory");
+          } while (!ok);
+          do {
+            asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+                         : "=r"(ok) : "r"(bar0 + 40), "r"(1u) : "memory");
+          } while (!ok);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          if (elect_one()) {
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk)
+              asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n"
+                           ::"r"(tbase + 128 * ((2 * j + kk / 4) & 3)), "l"(adesc + 2 * (kk & 3)), "l"(bdesc + 2 * (kk & 3) + (uint64_t)(s * 1024)), "r"(idesc), "r"(kk & 3));
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar0 + 8 * (j & 3)));
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar0 + 32));
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar0 + 32));
+          }
+          __syncwarp();
+          break;
+        }
+        case 21:
+        case 22:
+        case 23: {  // clock spin of 100 / 200 / 300 cycles + 4 MMA N128 + 2 commits
+          const long long c0 = clock64();
+          while (clock64() - c0 < 100 * (mode - 20)) {}
+          if (elect_one()) {
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk)
+              asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n"
+                           ::"r"(tbase + 128 * (j & 3)), "l"(adesc + 2 * kk), "l"(bdesc + 2 * kk + (uint64_t)(s * 1024)), "r"(idesc), "r"(kk));
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar0 + 8 * (j & 3)));
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar0 + 32));
+          }
+          __syncwarp();
+          break;
+        }
+        case 16:
+        case 17:
+        case 18:
+        case 19:
+          // N=128: 16 no commit, 17 one commit, 18 two commits, 19 two commits + two completed waits
+          if (mode == 19) {
+            uint32_t ok = 0;
+            do {
+              asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+                           : "=r"(ok) : "r"(bar0 + 48), "r"(1u) : "memory");
+            } while (!ok);
+            do {
+              asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+                           : "=r"(ok) : "r"(bar0 + 40), "r"(1u) : "memory");
+            } while (!ok);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          }
+          if (elect_one()) {
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk)
+              asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n"
+                           ::"r"(tbase + 128 * (j & 3)), "l"(adesc + 2 * kk), "l"(bdesc + 2 * kk + (uint64_t)(s * 1024)), "r"(idesc), "r"(kk));
+            if (mode >= 17)
+              asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar0 + 8 * (j & 3)));
+            if (mode >= 18)
+              asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar0 + 32));
+          }
+          __syncwarp();
+          break;
         case 15: {  // shared-memory volatile load (threshold read)
           sink += *(volatile unsigned long long*)(base + 8 * lane);
           break;
@@ -108,7 +178,7 @@ __global__ void __launch_bounds__(640, 1) k(int iters, int nacc, int nwarps, uns
       }
       if (++s == 2) s = 0;
     }
-    if (mode >= 6 && mode <= 8) {
+    if (((mode >= 6 && mode <= 8) || mode >= 16) && warp == 1) {
       if (elect_one())
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar0 + 56));
       __syncwarp();
@@ -134,12 +204,17 @@ int main(int argc, char** argv) {
   const int iters = 4000;
   const char* names[] = {"empty", "syncwarp", "j % nacc", "smem addr", "elect", "tc fence after", "commit", "4 MMA N256",
                          "4 MMA N256 + commit", "lane0 branch + syncwarp", "wait::ld (none)", "tc fence before",
-                         "fence+syncwarp+arrive", "tcgen05.ld x32 + wait", "clock64", "lds volatile"};
+                         "fence+syncwarp+arrive", "tcgen05.ld x32 + wait", "clock64", "lds volatile",
+                         "4 MMA N128", "4 MMA N128 + commit", "4 MMA N128 + 2 commits", "2 waits + 4 MMA N128 + 2 commits",
+                         "2 waits + 8 MMA N128 + 3 commits", "spin100 + 4 MMA + 2 commits", "spin200 + 4 MMA + 2 commits",
+                         "spin300 + 4 MMA + 2 commits"};
   void (*fns[])(int, int, int, unsigned long long*) = {k<0>, k<1>, k<2>, k<3>, k<4>, k<5>, k<6>, k<7>,
-                                                      k<8>, k<9>, k<10>, k<11>, k<12>, k<13>, k<14>, k<15>};
-  for (int nw : {1, 16}) {
-    for (int mode = 0; mode < 16; ++mode) {
-      if (nw > 1 && mode >= 6 && mode <= 8) continue;  // MMA issue: one warp only
+                                                      k<8>, k<9>, k<10>, k<11>, k<12>, k<13>, k<14>, k<15>,
+                                                      k<16>, k<17>, k<18>, k<19>, k<20>, k<21>, k<22>, k<23>};
+  for (int nw : {1, 2}) {
+    for (int mode = 6; mode < 24; ++mode) {
+      if (mode > 8 && mode < 16) continue;
+      if (nw == 2 && mode < 19) continue;
       cudaFuncSetAttribute(fns[mode], cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       for (int rep = 0; rep < 2; ++rep) {
         cudaMemset(d, 0, 16);
