@@ -324,6 +324,14 @@ __global__ void k_expand(const int32_t* nseg, const int32_t* base, int64_t n, in
   for (int s = 0; s < nseg[t]; ++s) items[b + s] = make_int2((int)t, s);
 }
 
+__global__ void k_item_keys(const int2* items, int n, unsigned long long* keys) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) keys[i] = ((unsigned long long)(uint32_t)items[i].y << 32) | (uint32_t)items[i].x;
+}
+__global__ void k_item_unkey(const unsigned long long* keys, int n, int2* items) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) items[i] = make_int2((int)(uint32_t)keys[i], (int)(keys[i] >> 32));
+}
 __global__ void k_fill_u64(unsigned long long* a, unsigned long long v, int64_t n) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) a[i] = v;
@@ -611,6 +619,20 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
   if (n_tt) {
     k_expand<<<(unsigned)cdiv(n_tt, 128), 128, 0, s>>>(tnseg, tbase, n_tt, titems);
     FIC_CHECK_LAUNCH();
+    // segment-major order: every tile's first segment runs before any second
+    // segment, so later segments start from the thresholds the earlier ones found
+    {
+      unsigned long long* k0 = sc.get<unsigned long long>(tot.n_titems);
+      unsigned long long* k1 = sc.get<unsigned long long>(tot.n_titems);
+      const int n = (int)tot.n_titems;
+      k_item_keys<<<(unsigned)cdiv(n, 256), 256, 0, s>>>(titems, n, k0);
+      FIC_CHECK_LAUNCH();
+      cub_call(sc, [&](void* t, size_t& b) {
+        return cub::DeviceRadixSort::SortKeys(t, b, k0, k1, n, 0, 64, s);
+      });
+      k_item_unkey<<<(unsigned)cdiv(n, 256), 256, 0, s>>>(k1, n, titems);
+      FIC_CHECK_LAUNCH();
+    }
   }
   if (n_er) {
     k_expand<<<(unsigned)cdiv(n_er, 128), 128, 0, s>>>(enseg, ebase, n_er, eitems);
