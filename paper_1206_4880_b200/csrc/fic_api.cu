@@ -647,7 +647,7 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
     k_fill_u64<<<(unsigned)cdiv(g.R, 256), 256, 0, s>>>(thr_g, 0x7ff0000000000000ull, g.R);
     FIC_CHECK_LAUNCH();
     TcArgs ta{titems, tot.n_titems, rid_s + tb, n_tr, wlo, whi, seg_t, RT, sbase, partials,
-              counters, thr_g, 0, nullptr};
+              counters, counters + 15, thr_g, 0, nullptr};
     const char* dbg_env = getenv("FIC_TC_DEBUG");
     if (dbg_env && (atoi(dbg_env) & 32)) {
       ta.dbg = sc.get<unsigned long long>(64 * 24);

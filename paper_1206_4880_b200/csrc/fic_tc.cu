@@ -388,7 +388,16 @@ __global__ void __maxnreg__(MAXREG)
 
   int prev_tile = -1;
   long long tsetup = 0, tteardown = 0, nitems = 0;
-  for (int64_t it = blockIdx.x / CG; it < a.n_items; it += gridDim.x / CG) {
+  // work items are handed out dynamically (one CTA-wide fetch per item; the
+  // items are ordered segment-major, so the full-length segments go first);
+  // cluster pairs walk a static stride
+  __shared__ long long s_next_item;
+  if (CG == 1) {
+    if (threadIdx.x == 0) s_next_item = (long long)atomicAdd(a.item_ctr, 1ull);
+    __syncthreads();
+  }
+  for (int64_t it = (CG == 1) ? (int64_t)s_next_item : (int64_t)(blockIdx.x / CG); it < a.n_items;
+       it = (CG == 1) ? (int64_t)s_next_item : it + gridDim.x / CG) {
     const long long ti0 = (DBG ? clock64() : 0ll);
     ++nitems;
     const int2 item = a.items[it];
@@ -754,6 +763,7 @@ __global__ void __maxnreg__(MAXREG)
     }
     gt += (uint32_t)nt;
     const long long ti2 = (DBG ? clock64() : 0ll);
+    if (CG == 1 && threadIdx.x == 0) s_next_item = (long long)atomicAdd(a.item_ctr, 1ull);
     cta_sync<CG>();
     if (warp == 0) tteardown += (DBG ? clock64() : 0ll) - ti2;
     (void)ti1;

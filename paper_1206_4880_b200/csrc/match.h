@@ -50,6 +50,7 @@ struct TcArgs {
   const int64_t* slot_base;
   Partial* partials;
   unsigned long long* counters;  // [0] exact evaluations, [1] screened candidates
+  unsigned long long* item_ctr;  // dynamic work-item counter (zeroed before the launch)
   unsigned long long* thr_g;   // [R] best exact error so far per range (double bits), shared by
                                // the items (segments) of a range; any value is a valid bound
   int debug;                   // FIC_TC_DEBUG (timing experiments only; results invalid if != 0)

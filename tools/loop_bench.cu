@@ -126,6 +126,34 @@ __global__ void __launch_bounds__(640, 1) k(int iters, int nacc, int nwarps, uns
           __syncwarp();
           break;
         }
+        case 24: {  // 4 MMA N128 with the two (completed) waits interleaved after MMAs 2 and 3, 2 commits
+          const bool leader = elect_one();
+          auto mma = [&](int kk) {
+            if (leader)
+              asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n"
+                           ::"r"(tbase + 128 * (j & 3)), "l"(adesc + 2 * kk), "l"(bdesc + 2 * kk + (uint64_t)(s * 1024)), "r"(idesc), "r"(kk));
+          };
+          auto wt = [&](uint32_t b) {
+            uint32_t ok = 0;
+            do {
+              asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+                           : "=r"(ok) : "r"(b), "r"(1u) : "memory");
+            } while (!ok);
+          };
+          mma(0);
+          mma(1);
+          wt(bar0 + 48);
+          mma(2);
+          wt(bar0 + 40);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          mma(3);
+          if (leader) {
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar0 + 8 * (j & 3)));
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar0 + 32));
+          }
+          __syncwarp();
+          break;
+        }
         case 21:
         case 22:
         case 23: {  // clock spin of 100 / 200 / 300 cycles + 4 MMA N128 + 2 commits
@@ -207,12 +235,12 @@ int main(int argc, char** argv) {
                          "fence+syncwarp+arrive", "tcgen05.ld x32 + wait", "clock64", "lds volatile",
                          "4 MMA N128", "4 MMA N128 + commit", "4 MMA N128 + 2 commits", "2 waits + 4 MMA N128 + 2 commits",
                          "2 waits + 8 MMA N128 + 3 commits", "spin100 + 4 MMA + 2 commits", "spin200 + 4 MMA + 2 commits",
-                         "spin300 + 4 MMA + 2 commits"};
+                         "spin300 + 4 MMA + 2 commits", "4 MMA, waits interleaved, 2 commits"};
   void (*fns[])(int, int, int, unsigned long long*) = {k<0>, k<1>, k<2>, k<3>, k<4>, k<5>, k<6>, k<7>,
                                                       k<8>, k<9>, k<10>, k<11>, k<12>, k<13>, k<14>, k<15>,
-                                                      k<16>, k<17>, k<18>, k<19>, k<20>, k<21>, k<22>, k<23>};
+                                                      k<16>, k<17>, k<18>, k<19>, k<20>, k<21>, k<22>, k<23>, k<24>};
   for (int nw : {1, 2}) {
-    for (int mode = 6; mode < 24; ++mode) {
+    for (int mode = 6; mode < 25; ++mode) {
       if (mode > 8 && mode < 16) continue;
       if (nw == 2 && mode < 19) continue;
       cudaFuncSetAttribute(fns[mode], cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
