@@ -57,7 +57,7 @@ class Scratch {
 };
 
 struct Timer {
-  cudaEvent_t ev[8];
+  cudaEvent_t ev[24];
   int n = 0;
   cudaStream_t s;
   explicit Timer(cudaStream_t st) : s(st) {
@@ -324,13 +324,32 @@ __global__ void k_expand(const int32_t* nseg, const int32_t* base, int64_t n, in
   for (int s = 0; s < nseg[t]; ++s) items[b + s] = make_int2((int)t, s);
 }
 
-__global__ void k_item_keys(const int2* items, int n, unsigned long long* keys) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) keys[i] = ((unsigned long long)(uint32_t)items[i].y << 32) | (uint32_t)items[i].x;
-}
-__global__ void k_item_unkey(const unsigned long long* keys, int n, int2* items) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) items[i] = make_int2((int)(uint32_t)keys[i], (int)(keys[i] >> 32));
+// Work items in segment-major order: (tile t, segment s) sorted by (s, t).
+// One block: for each segment index, a block-wide scan of "tile t has a
+// segment s" gives the rank of t among those tiles.
+__global__ void __launch_bounds__(1024) k_items_segmajor(const int32_t* nseg, int64_t n, int2* items) {
+  using Scan = cub::BlockScan<int, 1024>;
+  using Reduce = cub::BlockReduce<int, 1024>;
+  __shared__ typename Scan::TempStorage scan_tmp;
+  __shared__ typename Reduce::TempStorage red_tmp;
+  __shared__ int s_max, s_total;
+  int mx = 0;
+  for (int64_t t = threadIdx.x; t < n; t += 1024) mx = max(mx, nseg[t]);
+  mx = Reduce(red_tmp).Reduce(mx, cuda::maximum<>{});
+  if (threadIdx.x == 0) s_max = mx;
+  __syncthreads();
+  int64_t base = 0;
+  for (int seg = 0; seg < s_max; ++seg) {
+    for (int64_t t0 = 0; t0 < n; t0 += 1024) {
+      const int64_t t = t0 + threadIdx.x;
+      const int flag = (t < n && nseg[t] > seg) ? 1 : 0;
+      int rank = 0, total = 0;
+      Scan(scan_tmp).ExclusiveSum(flag, rank, total);
+      if (flag) items[base + rank] = make_int2((int)t, seg);
+      base += total;
+      __syncthreads();
+    }
+  }
 }
 __global__ void k_fill_u64(unsigned long long* a, unsigned long long v, int64_t n) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -496,6 +515,12 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
   g_launches = 0;
   Scratch sc(s);
   Timer tm(s);
+  // FIC_PLAN_TIMING: extra events inside the planning phase (events 8..)
+  const bool ptime = getenv("FIC_PLAN_TIMING") != nullptr;
+  int pn = 8;
+  auto pmark = [&]() {
+    if (ptime && pn < 24) FIC_CUDA(cudaEventRecord(tm.ev[pn++], s));
+  };
   tm.mark();  // 0
   PlanBufs pb = make_plan(sc, s, img, g, p);
   tm.mark();  // 1
@@ -536,7 +561,9 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
   ra.inv_perm = d_inv;
   ra.info = sc.get<RangeInfo>(g.R);
   ra.rows = sc.get<uint8_t>((size_t)g.R * g.n_iso * K);
+  pmark();  // 8
   launch_ranges(ra, s);
+  pmark();  // 9
 
   // plan: classify, sort by (class, lo, hi), shard by cost
   unsigned long long* counters = sc.get<unsigned long long>(16);
@@ -549,8 +576,10 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
                   pool_sizes, counters + 2};
   k_classify<<<(unsigned)cdiv(g.R, 256), 256, 0, s>>>(ca);
   FIC_CHECK_LAUNCH();
+  // order by (class, lo) only (bits 32..63; stable, so ties keep raster order):
+  // tiles need contiguous windows, and the result does not depend on the order
   cub_call(sc, [&](void* t, size_t& b) {
-    return cub::DeviceRadixSort::SortPairs(t, b, key, key_s, rid, rid_s, g.R, 0, 64, s);
+    return cub::DeviceRadixSort::SortPairs(t, b, key, key_s, rid, rid_s, g.R, 32, 64, s);
   });
   unsigned long long* cost = sc.get<unsigned long long>(g.R);
   unsigned long long* cum = sc.get<unsigned long long>(g.R);
@@ -563,8 +592,10 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
   k_shard<<<1, 32, 0, s>>>(key_s, cum, g.R, shard, nshard, d_pc);
   FIC_CHECK_LAUNCH();
   PlanCounts pc;
+  pmark();  // 10
   FIC_CUDA(cudaMemcpyAsync(&pc, d_pc, sizeof(pc), cudaMemcpyDeviceToHost, s));
   FIC_CUDA(cudaStreamSynchronize(s));
+  pmark();  // 11
 
   const int64_t tb = pc.shard_begin, te = std::min(pc.shard_end, pc.n_tensor);
   const int64_t eb = std::max(pc.shard_begin, pc.n_tensor), ee = pc.shard_end;
@@ -610,35 +641,26 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
   k_totals<<<1, 32, 0, s>>>(tnseg, tbase, n_tt, enseg, ebase, n_er, nslots, sbase, g.R, d_tot);
   FIC_CHECK_LAUNCH();
   Totals tot;
+  pmark();  // 12
   FIC_CUDA(cudaMemcpyAsync(&tot, d_tot, sizeof(tot), cudaMemcpyDeviceToHost, s));
   FIC_CUDA(cudaStreamSynchronize(s));
+  pmark();  // 13
 
   int2* titems = sc.get<int2>(tot.n_titems);
   int2* eitems = sc.get<int2>(tot.n_eitems);
   Partial* partials = sc.get<Partial>(tot.n_slots);
   if (n_tt) {
-    k_expand<<<(unsigned)cdiv(n_tt, 128), 128, 0, s>>>(tnseg, tbase, n_tt, titems);
-    FIC_CHECK_LAUNCH();
     // segment-major order: every tile's first segment runs before any second
     // segment, so later segments start from the thresholds the earlier ones found
-    {
-      unsigned long long* k0 = sc.get<unsigned long long>(tot.n_titems);
-      unsigned long long* k1 = sc.get<unsigned long long>(tot.n_titems);
-      const int n = (int)tot.n_titems;
-      k_item_keys<<<(unsigned)cdiv(n, 256), 256, 0, s>>>(titems, n, k0);
-      FIC_CHECK_LAUNCH();
-      cub_call(sc, [&](void* t, size_t& b) {
-        return cub::DeviceRadixSort::SortKeys(t, b, k0, k1, n, 0, 64, s);
-      });
-      k_item_unkey<<<(unsigned)cdiv(n, 256), 256, 0, s>>>(k1, n, titems);
-      FIC_CHECK_LAUNCH();
-    }
+    k_items_segmajor<<<1, 1024, 0, s>>>(tnseg, n_tt, titems);
+    FIC_CHECK_LAUNCH();
   }
   if (n_er) {
     k_expand<<<(unsigned)cdiv(n_er, 128), 128, 0, s>>>(enseg, ebase, n_er, eitems);
     FIC_CHECK_LAUNCH();
   }
 
+  pmark();  // 14
   PoolView P{pa.raw, pa.bh, pa.inv_den, pa.sums, pa.ids, g.D};
   RangeView Rv{ra.info, ra.rows, pb.lo, pb.hi, g.n_iso, K};
   tm.mark();  // 3
@@ -683,6 +705,12 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
   FIC_CUDA(cudaMemcpyAsync(hs, pb.scal, sizeof(hs), cudaMemcpyDeviceToHost, s));
   tm.mark();  // 7
   FIC_CUDA(cudaStreamSynchronize(s));
+  if (ptime && pn == 15) {
+    fprintf(stderr, "plan timing (ms): fd %.3f pool %.3f | iso-upload %.3f ranges %.3f classify..shard %.3f sync1 %.3f "
+            "tiles..totals %.3f sync2 %.3f items %.3f | tensor %.3f exact %.3f merge %.3f readback %.3f\n",
+            tm.ms(0, 1), tm.ms(1, 2), tm.ms(2, 8), tm.ms(8, 9), tm.ms(9, 10), tm.ms(10, 11), tm.ms(11, 12),
+            tm.ms(12, 13), tm.ms(13, 14), tm.ms(3, 4), tm.ms(4, 5), tm.ms(5, 6), tm.ms(6, 7));
+  }
   if (st) {
     std::memset(st, 0, sizeof(*st));
     st->n_ranges = g.R;
