@@ -13,6 +13,7 @@ from __future__ import annotations
 import ctypes
 import math
 import struct
+import threading
 import time
 from dataclasses import dataclass, field
 
@@ -227,6 +228,48 @@ def encode_device(image_dev, strategy="dynamic_fd", *, range_size=8, domain_size
     return out
 
 
+class _Staging:
+    """Per-(device, shape) pinned host buffers and one packed device output
+    buffer for ``encode``: [pre f64 R | post f64 R | pools i64 R | records 7R]."""
+
+    def __init__(self, torch, dev, h, w, n_r):
+        self.n_r = n_r
+        self.lock = threading.Lock()
+        self.h_img = torch.empty((h, w), dtype=torch.uint8, pin_memory=True)
+        self.d_img = torch.empty((h, w), dtype=torch.uint8, device=dev)
+        nbytes = 24 * n_r + 7 * n_r
+        self.d_out = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+        self.h_out = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+
+    def _split(self, buf):
+        n = self.n_r
+        f64 = buf[:16 * n].view(self._torch.float64)
+        return (f64[:n], f64[n:], buf[16 * n:24 * n].view(self._torch.int64),
+                buf[24 * n:].view(n, 7))
+
+    def result(self):
+        pre, post, pools, records = self._split(self.d_out)
+        return DeviceResult(records, pre, post, pools, {})
+
+    def host_views(self):
+        return tuple(t.numpy() for t in self._split(self.h_out))
+
+
+_STAGING: dict = {}
+
+
+def _staging(torch, dev, h, w, n_r):
+    key = (str(dev), h, w, n_r)
+    st = _STAGING.get(key)
+    if st is None:
+        if len(_STAGING) > 8:
+            _STAGING.clear()
+        st = _Staging(torch, dev, h, w, n_r)
+        st._torch = torch
+        _STAGING[key] = st
+    return st
+
+
 def encode(image, strategy: str = "dynamic_fd", *, range_size: int = 8,
            domain_size: int = 16, stride: int = 1, isometries: bool = False,
            workers: int = 1, fd_source: str = "original", delta: float | None = None,
@@ -240,18 +283,28 @@ def encode(image, strategy: str = "dynamic_fd", *, range_size: int = 8,
     t0 = time.perf_counter()
     torch = _torch()
     image, h, w = validate(image, strategy, range_size, domain_size, stride, fd_source)
-    if hasattr(image, "is_cuda") and image.is_cuda:
-        img_dev = image
-    else:
-        dev = torch.device("cuda", torch.cuda.current_device()) if device is None else device
-        img_dev = torch.from_numpy(np.ascontiguousarray(image)).to(dev, non_blocking=False)
-    res = encode_device(img_dev, strategy, range_size=range_size, domain_size=domain_size,
-                        stride=stride, isometries=isometries, fd_source=fd_source,
-                        delta=delta, matcher=matcher)
-    records = res.records.cpu().numpy().view(RECORD_DTYPE).ravel().copy()
-    pre = res.pre_rms.cpu().numpy()
-    post = res.post_rms.cpu().numpy()
-    pools = res.pool_sizes.cpu().numpy()
+    dev = (image.device if getattr(image, "is_cuda", False) else
+           torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device))
+    n_r = (h // range_size) * (w // range_size)
+    stage = _staging(torch, dev, h, w, n_r)
+    with stage.lock, torch.cuda.device(dev):
+        if getattr(image, "is_cuda", False):
+            img_dev = image
+        else:
+            # host image -> pinned staging -> device (one async copy)
+            stage.h_img.numpy()[...] = image
+            stage.d_img.copy_(stage.h_img, non_blocking=True)
+            img_dev = stage.d_img
+        stage.d_out.zero_()
+        res = encode_device(img_dev, strategy, range_size=range_size, domain_size=domain_size,
+                            stride=stride, isometries=isometries, fd_source=fd_source,
+                            delta=delta, matcher=matcher, out=stage.result())
+        # all outputs live in one device buffer -> one copy back
+        stage.h_out.copy_(stage.d_out, non_blocking=True)
+        torch.cuda.current_stream(dev).synchronize()
+        pre, post, pools, records = stage.host_views()
+        records = records.view(RECORD_DTYPE).ravel().copy()
+        pre, post, pools = pre.copy(), post.copy(), pools.copy()
     st = res.stats
     code = FractalCode(w, h, range_size, domain_size, stride, STRATEGY_IDS[strategy],
                        bool(isometries), records)

@@ -459,7 +459,9 @@ static PlanBufs make_plan(Scratch& sc, cudaStream_t s, const uint8_t* img, const
     // K3: stable sort of domains by FD (== AvlTree flatten, avltree.py:150-189)
     k_iota<<<(unsigned)cdiv(g.D, 256), 256, 0, s>>>(iin, g.D);
     FIC_CHECK_LAUNCH();
-    int nbits = 64;
+    // FDs are clamped to [2, 3] (fa.clamp), so the sign and exponent bits of
+    // every key are equal (0x400): sorting the 52 mantissa bits is exact
+    const int nbits = fa.clamp ? 52 : 64;
     cub_call(sc, [&](void* t, size_t& b) {
       return cub::DeviceRadixSort::SortPairs(t, b, kin, kout, iin, pb.order, (int64_t)g.D, 0,
                                              nbits, s);
