@@ -709,9 +709,9 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
   FIC_CUDA(cudaStreamSynchronize(s));
   if (ptime && pn == 15) {
     fprintf(stderr, "plan timing (ms): fd %.3f pool %.3f | iso-upload %.3f ranges %.3f classify..shard %.3f sync1 %.3f "
-            "tiles..totals %.3f sync2 %.3f items %.3f | tensor %.3f exact %.3f merge %.3f readback %.3f\n",
+            "tiles..totals %.3f sync2 %.3f items %.3f | tensor %.3f exact %.3f merge %.3f readback %.3f | seed rounds %llu hit rounds %llu hit lanes %llu\n",
             tm.ms(0, 1), tm.ms(1, 2), tm.ms(2, 8), tm.ms(8, 9), tm.ms(9, 10), tm.ms(10, 11), tm.ms(11, 12),
-            tm.ms(12, 13), tm.ms(13, 14), tm.ms(3, 4), tm.ms(4, 5), tm.ms(5, 6), tm.ms(6, 7));
+            tm.ms(12, 13), tm.ms(13, 14), tm.ms(3, 4), tm.ms(4, 5), tm.ms(5, 6), tm.ms(6, 7), hc[14], hc[12], hc[13]);
   }
   if (st) {
     std::memset(st, 0, sizeof(*st));
@@ -735,7 +735,7 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
     st->exact_tiles = (int32_t)n_er;
     st->work_items = (int32_t)(tot.n_titems + tot.n_eitems);
     st->kernel_launches = g_launches;
-    if (getenv("FIC_TC_DEBUG") && (atoi(getenv("FIC_TC_DEBUG")) & 4))
+    if ((getenv("FIC_TC_DEBUG") && (atoi(getenv("FIC_TC_DEBUG")) & 4)) || getenv("FIC_TC_PROF"))
       fprintf(stderr, "tc cycles: producer-empty %.3g  mma-tempty %.3g  mma-full %.3g  epi-tfull %.3g  epi-slow %.3g  epi-total %.3g  mma-loop %.3g  setup %.3g  teardown(tma warp) %.3g  items %.0f\n",
               (double)hc[4], (double)hc[5], (double)hc[6], (double)hc[7], (double)hc[8], (double)hc[9], (double)hc[10], (double)hc[11], (double)hc[12], (double)hc[13]);
   }

@@ -43,6 +43,10 @@
 #ifndef FIC_TC_XP
 #define FIC_TC_XP 0
 #endif
+#ifndef FIC_TC_PROF
+#define FIC_TC_PROF 0  // 1: cycle accounting (debug & 4 counters) in the production instantiation
+#endif
+#define TCLK() ((DBG || FIC_TC_PROF) ? clock64() : 0ll)
 
 namespace fic {
 
@@ -56,6 +60,10 @@ constexpr int NGRP = 2;       // screening groups; group g handles stages j with
 constexpr int NMMA = 1;       // MMA issuing warps; warp MMA0 + w issues tiles j % NMMA == w
 constexpr int NRES = 2;       // rescoring warps: thread t owns rows t + RSTRIDE * h
 constexpr int NSLICE = NGRP;  // survivor queues per row: one per screening group
+constexpr int CH = 64;        // TMEM columns per screening chunk (tcgen05.ld x32 per 32)
+// Parity waits are only sound if a waiter can never be two phases ahead of a
+// barrier: a group must own fixed accumulator stages (NGRP divides NACC).
+static_assert(NACC % NGRP == 0, "screening groups must own whole accumulator stages");
 constexpr int QCAP = 32;      // survivor queue entries per (row, slice)
 constexpr int MMA0 = 1;       // first MMA issuing warp (warp 0: TMA producer)
 constexpr int RES0 = MMA0 + NMMA;  // first rescoring warp
@@ -363,9 +371,9 @@ __global__ void __maxnreg__(MAXREG)
   int32_t rlo = 0, rhi = 0;
   uint32_t rid = 0;
   bool rvalid = false;
-  unsigned long long evals = 0;
+  unsigned long long evals = 0, seed_rounds = 0, hit_rounds = 0, hit_lanes = 0;
   long long tw0 = 0, tw1 = 0, tw2 = 0, tw3 = 0, tw4 = 0;  // stall cycles (debug & 4)
-  const long long tstart = (DBG ? clock64() : 0ll);
+  const long long tstart = TCLK();
 
   // exact rescoring of pool position p (codec.py:218-258 via eval_candidate)
   auto exact = [&](int64_t p, int erow, double esr, double esrr) -> Cand {
@@ -398,7 +406,7 @@ __global__ void __maxnreg__(MAXREG)
   }
   for (int64_t it = (CG == 1) ? (int64_t)s_next_item : (int64_t)(blockIdx.x / CG); it < a.n_items;
        it = (CG == 1) ? (int64_t)s_next_item : it + gridDim.x / CG) {
-    const long long ti0 = (DBG ? clock64() : 0ll);
+    const long long ti0 = TCLK();
     ++nitems;
     const int2 item = a.items[it];
     const int tile = item.x;
@@ -464,14 +472,14 @@ __global__ void __maxnreg__(MAXREG)
     }
     if (threadIdx.x == 0) *edone = 0;
     cta_sync<CG>();
-    tsetup += (DBG ? clock64() : 0ll) - ti0;
-    const long long ti1 = (DBG ? clock64() : 0ll);
+    tsetup += TCLK() - ti0;
+    const long long ti1 = TCLK();
 
     if (warp == 0) {
       // TMA producer: the whole warp walks the pipeline, one lane issues
       for (int j = 0; j < nt; ++j) {
-        { long long t0 = (DBG ? clock64() : 0ll); mbar_wait(empty_bar(stage), ph ^ 1); tw0 += (DBG ? clock64() : 0ll) - t0; }
-        if ((debug & 32) && blockIdx.x == 0 && it == 0 && j < 64 && lane == 0) a.dbg[j * 24] = (DBG ? clock64() : 0ll);
+        { long long t0 = TCLK(); mbar_wait(empty_bar(stage), ph ^ 1); tw0 += TCLK() - t0; }
+        if ((debug & 32) && blockIdx.x == 0 && it == 0 && j < 64 && lane == 0) a.dbg[j * 24] = TCLK();
         if (elect_one()) {
           if ((debug & 16) || ((debug & 1024) && (j & 1))) {
             if (leader) mbar_arrive(full_bar(stage));
@@ -499,10 +507,10 @@ __global__ void __maxnreg__(MAXREG)
       int acc = (int)(g0 % NACC), acc_ph = (int)((g0 / NACC) & 1);
       const uint32_t full0 = full_bar(0), empty0 = empty_bar(0), tfull0 = tfull_bar(0), tempty0 = tempty_bar(0);
       for (int j = warp - MMA0; j < nt; j += NMMA) {
-        { long long t0 = (DBG ? clock64() : 0ll); mbar_wait(tempty0 + 8 * acc, acc_ph ^ 1); tw1 += (DBG ? clock64() : 0ll) - t0; }
-        { long long t0 = (DBG ? clock64() : 0ll); mbar_wait(full0 + 8 * stage, ph); tw2 += (DBG ? clock64() : 0ll) - t0; }
+        { long long t0 = TCLK(); mbar_wait(tempty0 + 8 * acc, acc_ph ^ 1); tw1 += TCLK() - t0; }
+        { long long t0 = TCLK(); mbar_wait(full0 + 8 * stage, ph); tw2 += TCLK() - t0; }
         fence_after();
-        if ((debug & 32) && blockIdx.x == 0 && it == 0 && j < 64 && lane == 0) a.dbg[j * 24 + 1] = (DBG ? clock64() : 0ll);
+        if ((debug & 32) && blockIdx.x == 0 && it == 0 && j < 64 && lane == 0) a.dbg[j * 24 + 1] = TCLK();
         if (elect_one()) {
           const uint32_t d = tmem_base + acc * BN;
           const uint64_t bs = bdesc + (uint64_t)((stage * C::B_BYTES) >> 4);
@@ -553,24 +561,24 @@ __global__ void __maxnreg__(MAXREG)
       for (int j = (int)((group - (int)(gt % NGRP) + NGRP) % NGRP); j < nt; j += NGRP) {
         const uint32_t gj = gt + (uint32_t)j;
         const int acc = (int)(gj % NACC), acc_ph = (int)((gj / NACC) & 1);
-        { long long t0 = (DBG ? clock64() : 0ll); mbar_wait_sleep(tfull0 + 8 * acc, acc_ph); tw3 += (DBG ? clock64() : 0ll) - t0; }
+        { long long t0 = TCLK(); mbar_wait_sleep(tfull0 + 8 * acc, acc_ph); tw3 += TCLK() - t0; }
         const bool dbgw = (debug & 32) && blockIdx.x == 0 && it == 0 && j < 64 && lane == 0 && warp == SCR0;
-        if (dbgw) a.dbg[j * 24 + 4] = (DBG ? clock64() : 0ll);
+        if (dbgw) a.dbg[j * 24 + 4] = TCLK();
         fence_after();
         if (!(debug & 4096)) {  // thresholds published by the rescorers
           const unsigned long long tb = thr_s[rk];
           if (tb < thr_bits) set_threshold(tb);
         }
 #pragma unroll 1
-        for (int h = 0; h < BN / 64; ++h) {
-          float v[64];
+        for (int h = 0; h < BN / CH; ++h) {
+          float v[CH];
           if (!(debug & 1)) {
-            tmem_ld32(lane_base + acc * BN + 64 * h, v);
-            tmem_ld32(lane_base + acc * BN + 64 * h + 32, v + 32);
+#pragma unroll
+            for (int c = 0; c < CH / 32; ++c) tmem_ld32(lane_base + acc * BN + CH * h + 32 * c, v + 32 * c);
           }
           tmem_wait_ld();
-          if (dbgw) a.dbg[j * 24 + 5] = (DBG ? clock64() : 0ll);
-          if (h == BN / 64 - 1) {  // release the stage before screening its last half
+          if (dbgw) a.dbg[j * 24 + 5] = TCLK();
+          if (h == BN / CH - 1) {  // release the stage before screening its last chunk
             fence_before();
             __syncwarp();
             if (lane == 0) {
@@ -581,40 +589,45 @@ __global__ void __maxnreg__(MAXREG)
             }
           }
           if (debug & 1) continue;
-          const int32_t rel = j * BN + 64 * h;  // half start, relative to c0
+          const int32_t rel = j * BN + CH * h;  // chunk start, relative to c0
           const int32_t e_lo = lo32 - rel, e_hi = hi32 - rel;
-          const bool overlap = (debug & 4096) ? true : (rvalid && e_lo < 64 && e_hi > 0);
+          const bool overlap = (debug & 4096) ? true : (rvalid && e_lo < CH && e_hi > 0);
           float m0 = fmaxf(fmaxf(fabsf(v[0]), fabsf(v[1])), fabsf(v[2]));
           float m1 = fmaxf(fmaxf(fabsf(v[3]), fabsf(v[4])), fabsf(v[5]));
           float m2 = fmaxf(fmaxf(fabsf(v[6]), fabsf(v[7])), fabsf(v[8]));
           float m3 = fmaxf(fmaxf(fabsf(v[9]), fabsf(v[10])), fabsf(v[11]));
 #pragma unroll
-          for (int e = 12; e < 60; e += 8) {
+          for (int e = 12; e < CH - 4; e += 8) {
             m0 = fmaxf(fmaxf(m0, fabsf(v[e])), fabsf(v[e + 1]));
             m1 = fmaxf(fmaxf(m1, fabsf(v[e + 2])), fabsf(v[e + 3]));
             m2 = fmaxf(fmaxf(m2, fabsf(v[e + 4])), fabsf(v[e + 5]));
             m3 = fmaxf(fmaxf(m3, fabsf(v[e + 6])), fabsf(v[e + 7]));
           }
-          m0 = fmaxf(fmaxf(m0, fabsf(v[60])), fabsf(v[61]));
-          m1 = fmaxf(fmaxf(m1, fabsf(v[62])), fabsf(v[63]));
+          m0 = fmaxf(fmaxf(m0, fabsf(v[CH - 4])), fabsf(v[CH - 3]));
+          m1 = fmaxf(fmaxf(m1, fabsf(v[CH - 2])), fabsf(v[CH - 1]));
           const float mx = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3));
           const bool hit = !(debug & 8) && overlap && (mx >= s_r || (debug & 64));
-          if (dbgw) a.dbg[j * 24 + 6] = (DBG ? clock64() : 0ll);
-          if (__any_sync(0xffffffffu, hit)) {
-            const long long ts0 = (DBG ? clock64() : 0ll);
-            const int32_t wl = max(e_lo, 0), wh = min(e_hi, 64);
+          if (dbgw) a.dbg[j * 24 + 6] = TCLK();
+          if ((debug & 32768) && __any_sync(0xffffffffu, hit)) {  // experiment: hits detected, no slow path
+            ++hit_rounds;
+          } else if (__any_sync(0xffffffffu, hit)) {
+            ++hit_rounds;
+            hit_lanes += hit ? 1 : 0;
+            const long long ts0 = TCLK();
+            const int32_t wl = max(e_lo, 0), wh = min(e_hi, CH);
             uint64_t wmask = 0;
             if (hit) wmask = ((wh >= 64) ? ~0ull : ((1ull << wh) - 1ull)) & ~((1ull << wl) - 1ull);
             const bool seed = hit && thr_bits == 0x7ff0000000000000ull;
             if (__any_sync(0xffffffffu, seed)) {
+              ++seed_rounds;
               double tnew = INFINITY;
               if (seed) {
                 float bv = -1.0f;
 #pragma unroll
-                for (int q = 0; q < 64; ++q) bv = fmaxf(bv, ((wmask >> q) & 1ull) ? fabsf(v[q]) : -1.0f);
+                for (int q = 0; q < CH; ++q) bv = fmaxf(bv, ((wmask >> q) & 1ull) ? fabsf(v[q]) : -1.0f);
                 uint64_t eq = 0;
 #pragma unroll
-                for (int q = 0; q < 64; ++q) eq |= (fabsf(v[q]) == bv) ? (1ull << q) : 0ull;
+                for (int q = 0; q < CH; ++q) eq |= (fabsf(v[q]) == bv) ? (1ull << q) : 0ull;
                 const int e = __ffsll((long long)(eq & wmask)) - 1;
                 wmask &= ~(1ull << e);
                 tnew = fmax(exact(c0 + rel + e, row, sr, srr).err, 0.0);
@@ -635,15 +648,19 @@ __global__ void __maxnreg__(MAXREG)
             if (hit && !(debug & 8192)) {
               uint64_t m = 0;
 #pragma unroll
-              for (int q = 0; q < 64; ++q) m |= (fabsf(v[q]) >= s_r || (debug & 64)) ? (1ull << q) : 0ull;
+              for (int q = 0; q < CH; ++q) m |= (fabsf(v[q]) >= s_r || (debug & 64)) ? (1ull << q) : 0ull;
               m &= wmask;
+              if (debug & 16384) {  // experiment: mask only, no pushes
+                evals += __popcll(m);
+                m = 0;
+              }
               while (m) {
                 const int e = __ffsll((long long)m) - 1;
                 m &= m - 1;
                 push((uint32_t)(rel + e));
               }
             }
-            tw4 += (DBG ? clock64() : 0ll) - ts0;
+            tw4 += TCLK() - ts0;
           }
         }  // halves
       }
@@ -762,30 +779,38 @@ __global__ void __maxnreg__(MAXREG)
       }
     }
     gt += (uint32_t)nt;
-    const long long ti2 = (DBG ? clock64() : 0ll);
+    const long long ti2 = TCLK();
     if (CG == 1 && threadIdx.x == 0) s_next_item = (long long)atomicAdd(a.item_ctr, 1ull);
     cta_sync<CG>();
-    if (warp == 0) tteardown += (DBG ? clock64() : 0ll) - ti2;
+    if (warp == 0) tteardown += TCLK() - ti2;
     (void)ti1;
   }
 
   if (is_res || is_scr) {
     for (int m = 16; m >= 1; m >>= 1) evals += __shfl_xor_sync(0xffffffffu, evals, m);
     if (lane == 0) atomicAdd(a.counters, evals);
-    if ((debug & 4) && lane == 0 && is_scr) {
+    if (lane == 0 && seed_rounds) atomicAdd(a.counters + 14, seed_rounds);  // warp-level seeding rounds
+    if (!DBG) {  // hit statistics (warp-level rounds, lanes)
+      for (int m = 16; m >= 1; m >>= 1) hit_lanes += __shfl_xor_sync(0xffffffffu, hit_lanes, m);
+      if (lane == 0 && hit_rounds) {
+        atomicAdd(a.counters + 12, hit_rounds);
+        atomicAdd(a.counters + 13, hit_lanes);
+      }
+    }
+    if (((debug & 4) || FIC_TC_PROF) && lane == 0 && is_scr) {
       atomicAdd(a.counters + 7, (unsigned long long)tw3);
       atomicAdd(a.counters + 8, (unsigned long long)tw4);
-      atomicAdd(a.counters + 9, (unsigned long long)((DBG ? clock64() : 0ll) - tstart));
+      atomicAdd(a.counters + 9, (unsigned long long)(TCLK() - tstart));
     }
   }
-  if ((debug & 4) && lane == 0 && warp == 0) {
+  if (((debug & 4) || FIC_TC_PROF) && lane == 0 && warp == 0) {
     atomicAdd(a.counters + 4, (unsigned long long)tw0);
     atomicAdd(a.counters + 11, (unsigned long long)tsetup);
     atomicAdd(a.counters + 12, (unsigned long long)tteardown);
     atomicAdd(a.counters + 13, (unsigned long long)nitems);
   }
-  if ((debug & 4) && lane == 0 && warp == 1) {
-    atomicAdd(a.counters + 10, (unsigned long long)((DBG ? clock64() : 0ll) - tstart));
+  if (((debug & 4) || FIC_TC_PROF) && lane == 0 && warp == 1) {
+    atomicAdd(a.counters + 10, (unsigned long long)(TCLK() - tstart));
     atomicAdd(a.counters + 5, (unsigned long long)tw1);
     atomicAdd(a.counters + 6, (unsigned long long)tw2);
   }

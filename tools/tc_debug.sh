@@ -4,10 +4,11 @@ import torch
 from paper_1206_4880_b200 import codec, synth
 c = synth.CONFIGS["cfg3"]
 img = torch.from_numpy(c.make()).cuda()
+t = []
 for i in range(4):
     res = codec.encode_device(img, c.strategy, range_size=c.range_size, domain_size=c.domain_size, stride=c.stride, isometries=True, delta=c.delta)
     torch.cuda.synchronize()
+    t.append(res.stats["ms_tensor"])
+print("ms_tensor", ["%.3f" % x for x in t], "evals", res.stats["exact_evals"])
 PY
-python tools/gpu_check.py 2>&1 | tail -2
-FIC_PLAN_TIMING=1 python /tmp/pt.py 2>&1 | tail -3
-timeout 120 python bench.py --steps 5 --warmup 3 2>&1 | tail -1 | cut -c1-250
+for v in g2m2 base g2m2 base; do echo -n "$v "; FIC_B200_LIB=build/var/$v.so timeout 60 python /tmp/pt.py 2>&1 | tail -1; done
