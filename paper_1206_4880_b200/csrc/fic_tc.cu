@@ -61,6 +61,10 @@ constexpr int NMMA = 1;       // MMA issuing warps; warp MMA0 + w issues tiles j
 constexpr int NRES = 2;       // rescoring warps: thread t owns rows t + RSTRIDE * h
 constexpr int NSLICE = NGRP;  // survivor queues per row: one per screening group
 constexpr int CH = 64;        // TMEM columns per screening chunk (tcgen05.ld x32 per 32)
+#ifndef FIC_TC_WIDE
+#define FIC_TC_WIDE 0
+#endif
+constexpr bool WIDE = FIC_TC_WIDE;  // load a whole stage before screening (needs ~170 registers)
 // Parity waits are only sound if a waiter can never be two phases ahead of a
 // barrier: a group must own fixed accumulator stages (NGRP divides NACC).
 static_assert(NACC % NGRP == 0, "screening groups must own whole accumulator stages");
@@ -569,29 +573,58 @@ __global__ void __maxnreg__(MAXREG)
           const unsigned long long tb = thr_s[rk];
           if (tb < thr_bits) set_threshold(tb);
         }
-#pragma unroll 1
-        for (int h = 0; h < BN / CH; ++h) {
-          float v[CH];
-          if (!(debug & 1)) {
+        // slow path of one chunk (rare): seed the row's threshold if it has
+        // none, then push the chunk's survivors to the row's queue
+        auto slow_path = [&](const float* v, int32_t rel, int32_t e_lo, int32_t e_hi, bool hit) {
+          ++hit_rounds;
+          hit_lanes += hit ? 1 : 0;
+          const long long ts0 = TCLK();
+          const int32_t wl = max(e_lo, 0), wh = min(e_hi, CH);
+          uint64_t wmask = 0;
+          if (hit) wmask = ((wh >= 64) ? ~0ull : ((1ull << wh) - 1ull)) & ~((1ull << wl) - 1ull);
+          const bool seed = hit && thr_bits == 0x7ff0000000000000ull;
+          if (__any_sync(0xffffffffu, seed)) {
+            ++seed_rounds;
+            double tnew = INFINITY;
+            if (seed) {
+              float bv = -1.0f;
 #pragma unroll
-            for (int c = 0; c < CH / 32; ++c) tmem_ld32(lane_base + acc * BN + CH * h + 32 * c, v + 32 * c);
-          }
-          tmem_wait_ld();
-          if (dbgw) a.dbg[j * 24 + 5] = TCLK();
-          if (h == BN / CH - 1) {  // release the stage before screening its last chunk
-            fence_before();
-            __syncwarp();
-            if (lane == 0) {
-              if (leader)
-                mbar_arrive(tempty0 + 8 * acc);
-              else
-                mbar_arrive_cluster(map_to_rank(tempty0 + 8 * acc, 0));
+              for (int q = 0; q < CH; ++q) bv = fmaxf(bv, ((wmask >> q) & 1ull) ? fabsf(v[q]) : -1.0f);
+              uint64_t eq = 0;
+#pragma unroll
+              for (int q = 0; q < CH; ++q) eq |= (fabsf(v[q]) == bv) ? (1ull << q) : 0ull;
+              const int e = __ffsll((long long)(eq & wmask)) - 1;
+              wmask &= ~(1ull << e);
+              tnew = fmax(exact(c0 + rel + e, row, sr, srr).err, 0.0);
+              ++evals;
+              push((uint32_t)(rel + e));  // the rescorer records it
+            }
+            for (int m = 1; m < n_iso; m <<= 1)
+              tnew = fmin(tnew, __shfl_xor_sync(0xffffffffu, tnew, m));
+            const unsigned long long tb = (unsigned long long)__double_as_longlong(tnew);
+            if (tb < thr_bits) {
+              set_threshold(tb);
+              if (iso == 0 && rvalid) {
+                atomicMin(thr_s + rk, tb);
+                atomicMin(a.thr_g + rid, tb);
+              }
             }
           }
-          if (debug & 1) continue;
-          const int32_t rel = j * BN + CH * h;  // chunk start, relative to c0
-          const int32_t e_lo = lo32 - rel, e_hi = hi32 - rel;
-          const bool overlap = (debug & 4096) ? true : (rvalid && e_lo < CH && e_hi > 0);
+          if (hit) {
+            uint64_t m = 0;
+#pragma unroll
+            for (int q = 0; q < CH; ++q) m |= (fabsf(v[q]) >= s_r || (debug & 64)) ? (1ull << q) : 0ull;
+            m &= wmask;
+            while (m) {
+              const int e = __ffsll((long long)m) - 1;
+              m &= m - 1;
+              push((uint32_t)(rel + e));
+            }
+          }
+          tw4 += TCLK() - ts0;
+        };
+        // |u| max of CH values: four FMNMX3 chains
+        auto chunk_max = [&](const float* v) {
           float m0 = fmaxf(fmaxf(fabsf(v[0]), fabsf(v[1])), fabsf(v[2]));
           float m1 = fmaxf(fmaxf(fabsf(v[3]), fabsf(v[4])), fabsf(v[5]));
           float m2 = fmaxf(fmaxf(fabsf(v[6]), fabsf(v[7])), fabsf(v[8]));
@@ -605,64 +638,56 @@ __global__ void __maxnreg__(MAXREG)
           }
           m0 = fmaxf(fmaxf(m0, fabsf(v[CH - 4])), fabsf(v[CH - 3]));
           m1 = fmaxf(fmaxf(m1, fabsf(v[CH - 2])), fabsf(v[CH - 1]));
-          const float mx = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3));
-          const bool hit = !(debug & 8) && overlap && (mx >= s_r || (debug & 64));
-          if (dbgw) a.dbg[j * 24 + 6] = TCLK();
-          if ((debug & 32768) && __any_sync(0xffffffffu, hit)) {  // experiment: hits detected, no slow path
-            ++hit_rounds;
-          } else if (__any_sync(0xffffffffu, hit)) {
-            ++hit_rounds;
-            hit_lanes += hit ? 1 : 0;
-            const long long ts0 = TCLK();
-            const int32_t wl = max(e_lo, 0), wh = min(e_hi, CH);
-            uint64_t wmask = 0;
-            if (hit) wmask = ((wh >= 64) ? ~0ull : ((1ull << wh) - 1ull)) & ~((1ull << wl) - 1ull);
-            const bool seed = hit && thr_bits == 0x7ff0000000000000ull;
-            if (__any_sync(0xffffffffu, seed)) {
-              ++seed_rounds;
-              double tnew = INFINITY;
-              if (seed) {
-                float bv = -1.0f;
-#pragma unroll
-                for (int q = 0; q < CH; ++q) bv = fmaxf(bv, ((wmask >> q) & 1ull) ? fabsf(v[q]) : -1.0f);
-                uint64_t eq = 0;
-#pragma unroll
-                for (int q = 0; q < CH; ++q) eq |= (fabsf(v[q]) == bv) ? (1ull << q) : 0ull;
-                const int e = __ffsll((long long)(eq & wmask)) - 1;
-                wmask &= ~(1ull << e);
-                tnew = fmax(exact(c0 + rel + e, row, sr, srr).err, 0.0);
-                ++evals;
-                push((uint32_t)(rel + e));  // the rescorer records it
-              }
-              for (int m = 1; m < n_iso; m <<= 1)
-                tnew = fmin(tnew, __shfl_xor_sync(0xffffffffu, tnew, m));
-              const unsigned long long tb = (unsigned long long)__double_as_longlong(tnew);
-              if (tb < thr_bits) {
-                set_threshold(tb);
-                if (iso == 0 && rvalid) {
-                  atomicMin(thr_s + rk, tb);
-                  atomicMin(a.thr_g + rid, tb);
-                }
-              }
-            }
-            if (hit && !(debug & 8192)) {
-              uint64_t m = 0;
-#pragma unroll
-              for (int q = 0; q < CH; ++q) m |= (fabsf(v[q]) >= s_r || (debug & 64)) ? (1ull << q) : 0ull;
-              m &= wmask;
-              if (debug & 16384) {  // experiment: mask only, no pushes
-                evals += __popcll(m);
-                m = 0;
-              }
-              while (m) {
-                const int e = __ffsll((long long)m) - 1;
-                m &= m - 1;
-                push((uint32_t)(rel + e));
-              }
-            }
-            tw4 += TCLK() - ts0;
+          return fmaxf(fmaxf(m0, m1), fmaxf(m2, m3));
+        };
+        auto release = [&]() {
+          fence_before();
+          __syncwarp();
+          if (lane == 0) {
+            if (leader)
+              mbar_arrive(tempty0 + 8 * acc);
+            else
+              mbar_arrive_cluster(map_to_rank(tempty0 + 8 * acc, 0));
           }
-        }  // halves
+        };
+        if constexpr (WIDE) {
+          // the whole stage in registers: loads, release, independent chunk maxima
+          float v[BN];
+          if (!(debug & 1)) {
+#pragma unroll
+            for (int c = 0; c < BN / 32; ++c) tmem_ld32(lane_base + acc * BN + 32 * c, v + 32 * c);
+          }
+          tmem_wait_ld();
+          release();
+          if (debug & 1) continue;
+          float mx[BN / CH];
+#pragma unroll
+          for (int h = 0; h < BN / CH; ++h) mx[h] = chunk_max(v + CH * h);
+#pragma unroll
+          for (int h = 0; h < BN / CH; ++h) {
+            const int32_t rel = j * BN + CH * h;
+            const int32_t e_lo = lo32 - rel, e_hi = hi32 - rel;
+            const bool hit = !(debug & 8) && rvalid && e_lo < CH && e_hi > 0 && mx[h] >= s_r;
+            if (__any_sync(0xffffffffu, hit)) slow_path(v + CH * h, rel, e_lo, e_hi, hit);
+          }
+        } else {
+#pragma unroll 1
+          for (int h = 0; h < BN / CH; ++h) {
+            float v[CH];
+            if (!(debug & 1)) {
+#pragma unroll
+              for (int c = 0; c < CH / 32; ++c) tmem_ld32(lane_base + acc * BN + CH * h + 32 * c, v + 32 * c);
+            }
+            tmem_wait_ld();
+            if (h == BN / CH - 1) release();  // release the stage before screening its last chunk
+            if (debug & 1) continue;
+            const int32_t rel = j * BN + CH * h;  // chunk start, relative to c0
+            const int32_t e_lo = lo32 - rel, e_hi = hi32 - rel;
+            const float mx = chunk_max(v);
+            const bool hit = !(debug & 8) && rvalid && e_lo < CH && e_hi > 0 && mx >= s_r;
+            if (__any_sync(0xffffffffu, hit)) slow_path(v, rel, e_lo, e_hi, hit);
+          }
+        }
       }
       __threadfence_block();
       __syncwarp();
