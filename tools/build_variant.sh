@@ -2,7 +2,8 @@
 # Build an experiment variant of the library: tools/build_variant.sh NAME "-DFIC_TC_XP=..."
 set -e
 cd /root/repo
-make -s >/dev/null
+# the other objects come from the last in-tree build (run `make` first);
+# the variant's fic_tc.cu is compiled on its own so the in-tree library is untouched
 mkdir -p build/var
 nvcc -O3 -std=c++17 -lineinfo -gencode arch=compute_100a,code=sm_100a -Xcompiler -fPIC --expt-relaxed-constexpr $2 \
   -c paper_1206_4880_b200/csrc/fic_tc.cu -o build/var/fic_tc_$1.o
