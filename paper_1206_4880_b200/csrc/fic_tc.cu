@@ -55,11 +55,12 @@ namespace tc {
 constexpr int BM = 128;       // rows per tile (TMEM lanes)
 constexpr int BN = 128;       // columns per N-tile (one TMEM accumulator stage)
 constexpr int NACC = 4;       // TMEM accumulator stages (NACC * BN = 512 columns)
-constexpr int NEPI = 8;      // screening warps: NGRP groups x 4 lane quarters
 constexpr int NGRP = 2;       // screening groups; group g handles stages j with j % NGRP == g
+constexpr int NSPLIT = 1;     // column slices per lane quarter within a group
+constexpr int NEPI = 4 * NGRP * NSPLIT;  // screening warps: groups x slices x 4 lane quarters
 constexpr int NMMA = 1;       // MMA issuing warps; warp MMA0 + w issues tiles j % NMMA == w
 constexpr int NRES = 2;       // rescoring warps: thread t owns rows t + RSTRIDE * h
-constexpr int NSLICE = NGRP;  // survivor queues per row: one per screening group
+constexpr int NSLICE = NGRP * NSPLIT;  // survivor queues per row: one per (group, slice)
 constexpr int CH = 64;        // TMEM columns per screening chunk (tcgen05.ld x32 per 32)
 #ifndef FIC_TC_WIDE
 #define FIC_TC_WIDE 0
@@ -68,6 +69,7 @@ constexpr bool WIDE = FIC_TC_WIDE;  // load a whole stage before screening (need
 // Parity waits are only sound if a waiter can never be two phases ahead of a
 // barrier: a group must own fixed accumulator stages (NGRP divides NACC).
 static_assert(NACC % NGRP == 0, "screening groups must own whole accumulator stages");
+static_assert((BN / NSPLIT) % CH == 0 && CH % 32 == 0, "slices hold whole chunks of x32 loads");
 constexpr int QCAP = 32;      // survivor queue entries per (row, slice)
 constexpr int MMA0 = 1;       // first MMA issuing warp (warp 0: TMA producer)
 constexpr int RES0 = MMA0 + NMMA;  // first rescoring warp
@@ -332,7 +334,7 @@ __global__ void __maxnreg__(MAXREG)
     }
     for (int b = 0; b < NACC; ++b) {
       mbar_init(tfull_bar(b), 1);
-      mbar_init(tempty_bar(b), (NEPI / NGRP) * CG);
+      mbar_init(tempty_bar(b), (NEPI / NGRP) * CG);  // the 4 * NSPLIT warps of the stage's group
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -367,7 +369,9 @@ __global__ void __maxnreg__(MAXREG)
   const bool is_res = warp >= RES0 && warp < SCR0;
   const bool is_scr = warp >= SCR0;
   const int row = is_scr ? 32 * (warp & 3) + lane : 0;
-  const int group = is_scr ? (warp - SCR0) >> 2 : 0;  // stages j % NGRP == group
+  const int group = is_scr ? ((warp - SCR0) >> 2) % NGRP : 0;  // stages j % NGRP == group
+  const int slice = is_scr ? ((warp - SCR0) >> 2) / NGRP : 0;  // columns slice * BN / NSPLIT ..
+  constexpr int SW = BN / NSPLIT;                               // columns per slice
   const int rk = row / n_iso;          // range within this CTA's rows (thr_s index)
   const int iso = row - rk * n_iso;
   const int rk_tile = (row + rbase) / n_iso;  // range within the tile (tlist index)
@@ -544,9 +548,10 @@ __global__ void __maxnreg__(MAXREG)
       const uint32_t tfull0 = tfull_bar(0), tempty0 = tempty_bar(0);
       const int32_t lo32 = rvalid ? (int32_t)(max((int64_t)rlo, c0) - c0) : 0;
       const int32_t hi32 = rvalid ? (int32_t)(min((int64_t)rhi, c1) - c0) : 0;
-      uint32_t* myq = qbuf + (row * NSLICE + group) * QCAP;
-      volatile uint32_t* mytail = qtail + row * NSLICE + group;
-      volatile uint32_t* myhead = qhead + row * NSLICE + group;
+      const int qsl = group * NSPLIT + slice;
+      uint32_t* myq = qbuf + (row * NSLICE + qsl) * QCAP;
+      volatile uint32_t* mytail = qtail + row * NSLICE + qsl;
+      volatile uint32_t* myhead = qhead + row * NSLICE + qsl;
       uint32_t qt = 0;
       unsigned long long thr_bits = 0x7ff0000000000000ull;
       float s_r = -1.0f;  // |u| threshold; negative = every candidate survives
@@ -582,6 +587,10 @@ __global__ void __maxnreg__(MAXREG)
           const int32_t wl = max(e_lo, 0), wh = min(e_hi, CH);
           uint64_t wmask = 0;
           if (hit) wmask = ((wh >= 64) ? ~0ull : ((1ull << wh) - 1ull)) & ~((1ull << wl) - 1ull);
+          if (hit && thr_bits == 0x7ff0000000000000ull) {  // another group may have seeded the range meanwhile
+            const unsigned long long tb = thr_s[rk];
+            if (tb < thr_bits) set_threshold(tb);
+          }
           const bool seed = hit && thr_bits == 0x7ff0000000000000ull;
           if (__any_sync(0xffffffffu, seed)) {
             ++seed_rounds;
@@ -652,36 +661,37 @@ __global__ void __maxnreg__(MAXREG)
         };
         if constexpr (WIDE) {
           // the whole stage in registers: loads, release, independent chunk maxima
-          float v[BN];
+          float v[SW];
           if (!(debug & 1)) {
 #pragma unroll
-            for (int c = 0; c < BN / 32; ++c) tmem_ld32(lane_base + acc * BN + 32 * c, v + 32 * c);
+            for (int c = 0; c < SW / 32; ++c) tmem_ld32(lane_base + acc * BN + slice * SW + 32 * c, v + 32 * c);
           }
           tmem_wait_ld();
           release();
           if (debug & 1) continue;
-          float mx[BN / CH];
+          float mx[SW / CH];
 #pragma unroll
-          for (int h = 0; h < BN / CH; ++h) mx[h] = chunk_max(v + CH * h);
+          for (int h = 0; h < SW / CH; ++h) mx[h] = chunk_max(v + CH * h);
 #pragma unroll
-          for (int h = 0; h < BN / CH; ++h) {
-            const int32_t rel = j * BN + CH * h;
+          for (int h = 0; h < SW / CH; ++h) {
+            const int32_t rel = j * BN + slice * SW + CH * h;
             const int32_t e_lo = lo32 - rel, e_hi = hi32 - rel;
             const bool hit = !(debug & 8) && rvalid && e_lo < CH && e_hi > 0 && mx[h] >= s_r;
             if (__any_sync(0xffffffffu, hit)) slow_path(v + CH * h, rel, e_lo, e_hi, hit);
           }
         } else {
 #pragma unroll 1
-          for (int h = 0; h < BN / CH; ++h) {
+          for (int h = 0; h < SW / CH; ++h) {
             float v[CH];
             if (!(debug & 1)) {
 #pragma unroll
-              for (int c = 0; c < CH / 32; ++c) tmem_ld32(lane_base + acc * BN + CH * h + 32 * c, v + 32 * c);
+              for (int c = 0; c < CH / 32; ++c)
+                tmem_ld32(lane_base + acc * BN + slice * SW + CH * h + 32 * c, v + 32 * c);
             }
             tmem_wait_ld();
-            if (h == BN / CH - 1) release();  // release the stage before screening its last chunk
+            if (h == SW / CH - 1) release();  // release the stage before screening its last chunk
             if (debug & 1) continue;
-            const int32_t rel = j * BN + CH * h;  // chunk start, relative to c0
+            const int32_t rel = j * BN + slice * SW + CH * h;  // chunk start, relative to c0
             const int32_t e_lo = lo32 - rel, e_hi = hi32 - rel;
             const float mx = chunk_max(v);
             const bool hit = !(debug & 8) && rvalid && e_lo < CH && e_hi > 0 && mx >= s_r;

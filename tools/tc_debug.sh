@@ -11,4 +11,5 @@ for i in range(4):
     t.append(res.stats["ms_tensor"])
 print("ms_tensor", ["%.3f" % x for x in t], "evals", res.stats["exact_evals"])
 PY
-for v in base w2 base w2; do echo -n "$v "; FIC_B200_LIB=build/var/$v.so timeout 60 python /tmp/pt.py 2>&1 | tail -1; done
+echo start
+for v in base s2m1 s2m1c32 s2m2 s2m2c32; do echo -n "$v "; FIC_B200_LIB=build/var/$v.so timeout 60 python /tmp/pt.py 2>&1 | tail -1; done

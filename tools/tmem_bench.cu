@@ -31,8 +31,34 @@ __global__ void k_ld(int iters, unsigned long long* out, float* sink) {
                    : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
                    : "r"(base + col));
       asm volatile("tcgen05.wait::ld.sync.aligned;");
+      float m0 = 0, m1 = 0, m2 = 0, m3 = 0;
 #pragma unroll
-      for (int e = 0; e < 32; ++e) acc += __uint_as_float(r[e]);
+      for (int e = 0; e < 32; e += 4) {
+        m0 = fmaxf(m0, fabsf(__uint_as_float(r[e]))); m1 = fmaxf(m1, fabsf(__uint_as_float(r[e + 1])));
+        m2 = fmaxf(m2, fabsf(__uint_as_float(r[e + 2]))); m3 = fmaxf(m3, fabsf(__uint_as_float(r[e + 3])));
+      }
+      acc += fmaxf(fmaxf(m0, m1), fmaxf(m2, m3));
+    } else if (SHAPE == 2) {  // two 32x32b.x32 in flight, one wait
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                   : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+                   : "r"(base + col));
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                   : "=r"(r[32]), "=r"(r[33]), "=r"(r[34]), "=r"(r[35]), "=r"(r[36]), "=r"(r[37]), "=r"(r[38]), "=r"(r[39]), "=r"(r[40]), "=r"(r[41]), "=r"(r[42]), "=r"(r[43]), "=r"(r[44]), "=r"(r[45]), "=r"(r[46]), "=r"(r[47]), "=r"(r[48]), "=r"(r[49]), "=r"(r[50]), "=r"(r[51]), "=r"(r[52]), "=r"(r[53]), "=r"(r[54]), "=r"(r[55]), "=r"(r[56]), "=r"(r[57]), "=r"(r[58]), "=r"(r[59]), "=r"(r[60]), "=r"(r[61]), "=r"(r[62]), "=r"(r[63])
+                   : "r"(base + col + 32));
+      asm volatile("tcgen05.wait::ld.sync.aligned;");
+      float m0 = 0, m1 = 0, m2 = 0, m3 = 0;
+#pragma unroll
+      for (int e = 0; e < 64; e += 4) {
+        m0 = fmaxf(m0, fabsf(__uint_as_float(r[e]))); m1 = fmaxf(m1, fabsf(__uint_as_float(r[e + 1])));
+        m2 = fmaxf(m2, fabsf(__uint_as_float(r[e + 2]))); m3 = fmaxf(m3, fabsf(__uint_as_float(r[e + 3])));
+      }
+      acc += fmaxf(fmaxf(m0, m1), fmaxf(m2, m3));
+    } else if (SHAPE == 3) {  // one 32x32b.x32, no compute (pure load + wait)
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                   : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+                   : "r"(base + col));
+      asm volatile("tcgen05.wait::ld.sync.aligned;");
+      acc += __uint_as_float(r[0]);
     } else {  // 16x256b.x8: 32 regs (rows 2x16, 64 columns... same bytes)
       asm volatile("tcgen05.ld.sync.aligned.16x256b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
                    : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
@@ -63,7 +89,7 @@ void run(const char* name) {
   }
   unsigned long long cyc;
   cudaMemcpy(&cyc, d, 8, cudaMemcpyDeviceToHost);
-  double bytes = (double)iters * NW * 32 * 32 * 4;  // per SM
+  double bytes = (double)iters * NW * 32 * 32 * 4 * (SHAPE == 2 ? 2 : 1);  // per SM
   printf("%-28s warps=%2d  %.1f B/cycle/SM  (%llu cycles, err=%s)\n", name, NW, bytes / cyc, cyc,
          cudaGetErrorString(cudaGetLastError()));
   cudaFree(d);
@@ -71,11 +97,14 @@ void run(const char* name) {
 }
 
 int main() {
-  run<4, 0>("ld 32x32b.x32");
-  run<8, 0>("ld 32x32b.x32");
-  run<16, 0>("ld 32x32b.x32");
-  run<4, 1>("ld 16x256b.x8");
-  run<8, 1>("ld 16x256b.x8");
-  run<16, 1>("ld 16x256b.x8");
+  run<4, 0>("ld x32 + max");
+  run<8, 0>("ld x32 + max");
+  run<16, 0>("ld x32 + max");
+  run<4, 2>("ld 2 x32 + max");
+  run<8, 2>("ld 2 x32 + max");
+  run<16, 2>("ld 2 x32 + max");
+  run<4, 3>("ld x32 only");
+  run<8, 3>("ld x32 only");
+  run<16, 3>("ld x32 only");
   return 0;
 }
