@@ -263,6 +263,7 @@ struct TileArgs {
   int64_t tb, te;                 // tensor positions of this shard
   int RT;
   int seg;
+  int seg0;
   int32_t* wlo;
   int32_t* whi;
   int32_t* nseg;
@@ -279,7 +280,8 @@ __global__ void k_tiles(TileArgs a) {
   int32_t lo = (int32_t)((a.key[b] >> 32) & 0x7fffffffu);
   int32_t hi = 0;
   for (int64_t i = b; i < e; ++i) hi = max(hi, (int32_t)(uint32_t)a.key[i]);
-  int32_t ns = (int32_t)cdiv(hi - lo, a.seg);
+  // a short first segment (seg0 columns), then seg-column segments
+  int32_t ns = (hi - lo <= a.seg0) ? 1 : 1 + (int32_t)cdiv(hi - lo - a.seg0, a.seg);
   a.wlo[t] = lo;
   a.whi[t] = hi;
   a.nseg[t] = ns;
@@ -511,6 +513,9 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
   const bool tensor_ok = (p.matcher != FIC_MATCH_EXACT) && tc_supported(K);
   const int small_pool = p.small_pool > 0 ? p.small_pool : 256;
   const int seg_t = p.max_segment > 0 ? (int)align_up(p.max_segment, 256) : 65536;
+  // first segment of each tensor tile (a multiple of the 128-column N-tile);
+  // a short one seeds thresholds early but measured no faster at cfg3
+  const int seg0 = getenv("FIC_SEG0") ? std::max(128, atoi(getenv("FIC_SEG0")) / 128 * 128) : seg_t;
   const int seg_e = 4096;
   const int RT = (tensor_ok ? tc_tile_rows(K) : 128) / g.n_iso;
 
@@ -615,7 +620,7 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
   int32_t* ebase = sc.get<int32_t>(n_er);
   int64_t* sbase = sc.get<int64_t>(g.R);
   if (n_tt) {
-    TileArgs ta{key_s, rid_s, tb, te, RT, seg_t, wlo, whi, tnseg, nslots, g.n_iso, counters + 3};
+    TileArgs ta{key_s, rid_s, tb, te, RT, seg_t, seg0, wlo, whi, tnseg, nslots, g.n_iso, counters + 3};
     k_tiles<<<(unsigned)cdiv(n_tt, 128), 128, 0, s>>>(ta);
     FIC_CHECK_LAUNCH();
     cub_call(sc, [&](void* t, size_t& b) {
@@ -670,7 +675,7 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
     unsigned long long* thr_g = sc.get<unsigned long long>(g.R);
     k_fill_u64<<<(unsigned)cdiv(g.R, 256), 256, 0, s>>>(thr_g, 0x7ff0000000000000ull, g.R);
     FIC_CHECK_LAUNCH();
-    TcArgs ta{titems, tot.n_titems, rid_s + tb, n_tr, wlo, whi, seg_t, RT, sbase, partials,
+    TcArgs ta{titems, tot.n_titems, rid_s + tb, n_tr, wlo, whi, seg_t, seg0, RT, sbase, partials,
               counters, counters + 15, thr_g, 0, nullptr};
     const char* dbg_env = getenv("FIC_TC_DEBUG");
     if (dbg_env && (atoi(dbg_env) & 32)) {

@@ -419,8 +419,10 @@ __global__ void __maxnreg__(MAXREG)
     const int2 item = a.items[it];
     const int tile = item.x;
     const int64_t wlo = a.wlo[tile], whi = a.whi[tile];
-    const int64_t c0 = wlo + (int64_t)item.y * a.seg_len;
-    const int64_t c1 = min(whi, c0 + a.seg_len);
+    // segment 0 is short (a.seg0 columns): run first for every tile
+    // (segment-major order), it seeds the per-range thresholds cheaply
+    const int64_t c0 = item.y == 0 ? wlo : wlo + a.seg0 + (int64_t)(item.y - 1) * a.seg_len;
+    const int64_t c1 = min(whi, item.y == 0 ? c0 + a.seg0 : c0 + a.seg_len);
     const int nt = (int)cdiv(c1 - c0, BN);
 
     if (tile != prev_tile) {

@@ -45,7 +45,8 @@ struct TcArgs {
   int64_t n_tr;
   const int32_t* wlo;          // [tiles] union window
   const int32_t* whi;
-  int seg_len;
+  int seg_len;                 // columns per work item (segments >= 1)
+  int seg0;                    // columns of a tile's first segment (short: it seeds the thresholds)
   int RT;                      // ranges per tile = 128 / n_iso
   const int64_t* slot_base;
   Partial* partials;

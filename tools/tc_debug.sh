@@ -9,7 +9,7 @@ for i in range(4):
     res = codec.encode_device(img, c.strategy, range_size=c.range_size, domain_size=c.domain_size, stride=c.stride, isometries=True, delta=c.delta)
     torch.cuda.synchronize()
     t.append(res.stats["ms_tensor"])
-print("ms_tensor", ["%.3f" % x for x in t], "evals", res.stats["exact_evals"])
+print("ms_tensor", ["%.3f" % x for x in t], "evals", res.stats["exact_evals"], "items", res.stats["work_items"])
 PY
-echo start
-for v in base s2m1 s2m1c32 s2m2 s2m2c32; do echo -n "$v "; FIC_B200_LIB=build/var/$v.so timeout 60 python /tmp/pt.py 2>&1 | tail -1; done
+python tools/gpu_check.py 2>&1 | tail -2
+for s0 in 65536 4096 1024 512 256 128; do echo -n "seg0=$s0 "; FIC_SEG0=$s0 timeout 60 python /tmp/pt.py 2>&1 | tail -1; done
