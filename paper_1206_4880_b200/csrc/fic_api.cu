@@ -281,7 +281,7 @@ __global__ void k_tiles(TileArgs a) {
   int32_t hi = 0;
   for (int64_t i = b; i < e; ++i) hi = max(hi, (int32_t)(uint32_t)a.key[i]);
   // a short first segment (seg0 columns), then seg-column segments
-  int32_t ns = (hi - lo <= a.seg0) ? 1 : 1 + (int32_t)cdiv(hi - lo - a.seg0, a.seg);
+  int32_t ns = (hi <= lo) ? 0 : (hi - lo <= a.seg0) ? 1 : 1 + (int32_t)cdiv(hi - lo - a.seg0, a.seg);
   a.wlo[t] = lo;
   a.whi[t] = hi;
   a.nseg[t] = ns;
