@@ -240,6 +240,8 @@ class _Staging:
         nbytes = 24 * n_r + 7 * n_r
         self.d_out = torch.empty(nbytes, dtype=torch.uint8, device=dev)
         self.h_out = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+        self._h_np = None
+        self._d_res = None
 
     def _split(self, buf):
         n = self.n_r
@@ -248,11 +250,18 @@ class _Staging:
                 buf[24 * n:].view(n, 7))
 
     def result(self):
-        pre, post, pools, records = self._split(self.d_out)
-        return DeviceResult(records, pre, post, pools, {})
+        if self._d_res is None:  # device views of the packed buffer (made once)
+            pre, post, pools, records = self._split(self.d_out)
+            self._d_res = (records, pre, post, pools)
+        return DeviceResult(*self._d_res, {})
 
     def host_views(self):
-        return tuple(t.numpy() for t in self._split(self.h_out))
+        if self._h_np is None:  # numpy views of the pinned buffer (made once)
+            n, buf = self.n_r, self.h_out.numpy()
+            f64 = buf[:16 * n].view(np.float64)
+            self._h_np = (f64[:n], f64[n:], buf[16 * n:24 * n].view(np.int64),
+                          buf[24 * n:].reshape(n, 7))
+        return self._h_np
 
 
 _STAGING: dict = {}
@@ -303,7 +312,7 @@ def encode(image, strategy: str = "dynamic_fd", *, range_size: int = 8,
         stage.h_out.copy_(stage.d_out, non_blocking=True)
         torch.cuda.current_stream(dev).synchronize()
         pre, post, pools, records = stage.host_views()
-        records = records.view(RECORD_DTYPE).ravel().copy()
+        records = records.copy().view(RECORD_DTYPE).ravel()  # byte copy, then a view
         pre, post, pools = pre.copy(), post.copy(), pools.copy()
     st = res.stats
     code = FractalCode(w, h, range_size, domain_size, stride, STRATEGY_IDS[strategy],

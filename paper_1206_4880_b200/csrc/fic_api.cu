@@ -8,6 +8,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
+#include <tuple>
 #include <vector>
 
 #include "kernels.h"
@@ -57,14 +60,20 @@ class Scratch {
 };
 
 struct Timer {
-  cudaEvent_t ev[24];
+  cudaEvent_t* ev;
   int n = 0;
   cudaStream_t s;
+  // events are created once per thread and device and reused
   explicit Timer(cudaStream_t st) : s(st) {
-    for (auto& e : ev) FIC_CUDA(cudaEventCreate(&e));
-  }
-  ~Timer() {
-    for (auto& e : ev) cudaEventDestroy(e);
+    static thread_local std::map<int, std::vector<cudaEvent_t>> pool;
+    int dev = 0;
+    FIC_CUDA(cudaGetDevice(&dev));
+    auto& v = pool[dev];
+    if (v.empty()) {
+      v.resize(24);
+      for (auto& e : v) FIC_CUDA(cudaEventCreate(&e));
+    }
+    ev = v.data();
   }
   void mark() { FIC_CUDA(cudaEventRecord(ev[n++], s)); }
   double ms(int a, int b) {
@@ -166,14 +175,27 @@ static DbcTables make_dbc(Scratch& sc, cudaStream_t s, int side, const double* h
     for (int j = 0; j < t.J; ++j) w[j] = (xs[j] - mean) / dd;
   }
   t.ln_len = need;
-  t.quot = sc.get<uint16_t>(t.J * 256);
-  t.ln = sc.get<double>(need);
-  t.w = sc.get<double>(t.J);
-  FIC_CUDA(cudaMemcpyAsync(t.quot, q.data(), t.J * 256 * sizeof(uint16_t),
-                           cudaMemcpyHostToDevice, s));
-  FIC_CUDA(cudaMemcpyAsync(t.ln, ln.data(), need * sizeof(double), cudaMemcpyHostToDevice, s));
-  // pageable-source copies: the host buffers are staged before the call returns
-  FIC_CUDA(cudaMemcpyAsync(t.w, w.data(), t.J * sizeof(double), cudaMemcpyHostToDevice, s));
+  // the tables depend only on (device, side, ln values, weights): upload once
+  // and keep them (a few KB per block side) instead of copying every call
+  static std::mutex mu;
+  static std::map<std::vector<double>, DbcTables> cache;
+  int dev = 0;
+  FIC_CUDA(cudaGetDevice(&dev));
+  std::vector<double> key{(double)dev, (double)side, (double)need};
+  key.insert(key.end(), w.begin(), w.end());
+  key.insert(key.end(), ln.begin(), ln.end());
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  FIC_CUDA(cudaMalloc(&t.quot, t.J * 256 * sizeof(uint16_t)));
+  FIC_CUDA(cudaMalloc(&t.ln, need * sizeof(double)));
+  FIC_CUDA(cudaMalloc(&t.w, t.J * sizeof(double)));
+  FIC_CUDA(cudaMemcpy(t.quot, q.data(), t.J * 256 * sizeof(uint16_t), cudaMemcpyHostToDevice));
+  FIC_CUDA(cudaMemcpy(t.ln, ln.data(), need * sizeof(double), cudaMemcpyHostToDevice));
+  FIC_CUDA(cudaMemcpy(t.w, w.data(), t.J * sizeof(double), cudaMemcpyHostToDevice));
+  cache.emplace(std::move(key), t);
+  (void)sc;
+  (void)s;
   return t;
 }
 
