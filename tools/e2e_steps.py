@@ -30,3 +30,25 @@ for _ in range(10):
 for k, v in T.items():
     print(f"{k:24s} {v / 10:.3f} ms")
 print("ms_total (GPU events)", res.stats["ms_total"])
+
+# inside encode_device: Python parts vs the library call
+import ctypes
+from paper_1206_4880_b200 import _lib
+lib = _lib.load()
+T2 = {}
+def t2(name, t0):
+    T2[name] = T2.get(name, 0.0) + (time.perf_counter() - t0) * 1e3
+out = st.result()
+for _ in range(10):
+    t0 = time.perf_counter(); prm = codec.make_params(c.strategy, 8, 16, 1, True, "original", c.delta, "auto", (0, 1)); t2("make_params", t0)
+    t0 = time.perf_counter(); s_ = _lib.FicStats(); strm = torch.cuda.current_stream(dev).cuda_stream; t2("stats+stream", t0)
+    t0 = time.perf_counter()
+    rc = lib.fic_encode_v1(ctypes.c_void_p(st.d_img.data_ptr()), h, w, ctypes.byref(prm),
+                           ctypes.c_void_p(out.records.data_ptr()), ctypes.c_void_p(out.pre_rms.data_ptr()),
+                           ctypes.c_void_p(out.post_rms.data_ptr()), ctypes.c_void_p(out.pool_sizes.data_ptr()),
+                           ctypes.byref(s_), ctypes.c_void_p(strm))
+    t2("library call", t0)
+    t0 = time.perf_counter(); d = s_.as_dict(); t2("as_dict", t0)
+for k, v in T2.items():
+    print(f"{k:24s} {v / 10:.3f} ms")
+print("ms_total", d["ms_total"])
