@@ -472,8 +472,11 @@ __global__ void __maxnreg__(MAXREG)
     }
     if (threadIdx.x < BM) {  // per-range thresholds: start from what other segments found
       unsigned long long tb = 0x7ff0000000000000ull;  // +inf
-      const int64_t g = (int64_t)tile * a.RT + threadIdx.x;
-      if ((int)threadIdx.x < a.RT && g < a.n_tr) tb = a.thr_g[a.tlist[g]];
+      // thr_s is indexed by the CTA-local range (row / n_iso); the peer CTA
+      // of a pair holds the tile's ranges from rbase / n_iso on
+      const int kl = (int)threadIdx.x, kt = kl + rbase / n_iso;
+      const int64_t g = (int64_t)tile * a.RT + kt;
+      if (kl < BM / n_iso && kt < a.RT && g < a.n_tr) tb = a.thr_g[a.tlist[g]];
       thr_s[threadIdx.x] = tb;
     }
     for (int i = threadIdx.x; i < NSLICE * BM; i += NTHREADS) {

@@ -205,3 +205,18 @@ def test_deterministic_across_runs_and_segments():
     for x in (b, c2):
         assert torch.equal(a.records, x.records)
         assert torch.equal(a.post_rms, x.post_rms) and torch.equal(a.pre_rms, x.pre_rms)
+
+
+def test_cta_pair_matcher_equals_default(monkeypatch):
+    """The cta_group::2 variant of the matcher (FIC_TC_CG=2: M = 256 rows per
+    CTA pair) returns the same records as the default one-CTA matcher."""
+    import torch
+    c = synth.CONFIGS["cfg2"]
+    img = torch.from_numpy(c.make()).cuda()
+    kw = dict(range_size=8, domain_size=16, stride=4, isometries=True, delta=0.1)
+    a = codec.encode_device(img, "dynamic_fd", **kw)
+    monkeypatch.setenv("FIC_TC_CG", "2")
+    b = codec.encode_device(img, "dynamic_fd", max_segment=1024, **kw)
+    assert b.stats["tensor_tiles"] > 0
+    assert torch.equal(a.records, b.records)
+    assert torch.equal(a.post_rms, b.post_rms) and torch.equal(a.pre_rms, b.pre_rms)

@@ -11,5 +11,5 @@ for i in range(4):
     t.append(res.stats["ms_tensor"])
 print("ms_tensor", ["%.3f" % x for x in t], "evals", res.stats["exact_evals"], "items", res.stats["work_items"])
 PY
-python tools/gpu_check.py 2>&1 | tail -2
-for s0 in 65536 4096 1024 512 256 128; do echo -n "seg0=$s0 "; FIC_SEG0=$s0 timeout 60 python /tmp/pt.py 2>&1 | tail -1; done
+FIC_TC_CG=2 timeout 120 python tools/gpu_check.py 2>&1 | tail -3
+for v in 1 2; do echo -n "CG=$v "; FIC_TC_CG=$v timeout 60 python /tmp/pt.py 2>&1 | tail -1; done
