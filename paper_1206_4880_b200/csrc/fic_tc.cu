@@ -58,8 +58,8 @@ constexpr int NACC = 4;       // TMEM accumulator stages (NACC * BN = 512 column
 constexpr int NGRP = 2;       // screening groups; group g handles stages j with j % NGRP == g
 constexpr int NSPLIT = 1;     // column slices per lane quarter within a group
 constexpr int NEPI = 4 * NGRP * NSPLIT;  // screening warps: groups x slices x 4 lane quarters
-constexpr int NMMA = 1;       // MMA issuing warps; warp MMA0 + w issues tiles j % NMMA == w
-constexpr int NRES = 2;       // rescoring warps: thread t owns rows t + RSTRIDE * h
+constexpr int NMMA = 2;       // MMA issuing warps; warp MMA0 + w issues tiles j % NMMA == w
+constexpr int NRES = 1;       // rescoring warps: thread t owns rows t + RSTRIDE * h
 constexpr int NSLICE = NGRP * NSPLIT;  // survivor queues per row: one per (group, slice)
 constexpr int CH = 64;        // TMEM columns per screening chunk (tcgen05.ld x32 per 32)
 #ifndef FIC_TC_WIDE
@@ -208,8 +208,9 @@ __device__ __forceinline__ uint32_t map_to_rank(uint32_t addr, uint32_t rank) {
 }
 
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
-               : "memory");
+  // default semantics, as CUTLASS's ClusterBarrier::arrive(cta_id) (the
+  // .release.cluster form measured several times slower here)
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 
 template <int CG>
@@ -685,7 +686,7 @@ __global__ void __maxnreg__(MAXREG)
             if (__any_sync(0xffffffffu, hit)) slow_path(v + CH * h, rel, e_lo, e_hi, hit);
           }
         } else {
-#pragma unroll 1
+#pragma unroll
           for (int h = 0; h < SW / CH; ++h) {
             float v[CH];
             if (!(debug & 1)) {
@@ -699,7 +700,9 @@ __global__ void __maxnreg__(MAXREG)
             const int32_t rel = j * BN + slice * SW + CH * h;  // chunk start, relative to c0
             const int32_t e_lo = lo32 - rel, e_hi = hi32 - rel;
             const float mx = chunk_max(v);
-            const bool hit = !(debug & 8) && rvalid && e_lo < CH && e_hi > 0 && mx >= s_r;
+            // bitwise, so the max is computed unconditionally (no branch around it)
+            const bool in_window = rvalid & (e_lo < CH) & (e_hi > 0);
+            const bool hit = !(debug & 8) & in_window & (mx >= s_r);
             if (__any_sync(0xffffffffu, hit)) slow_path(v, rel, e_lo, e_hi, hit);
           }
         }
