@@ -587,8 +587,10 @@ __global__ void __maxnreg__(MAXREG)
         // slow path of one chunk (rare): seed the row's threshold if it has
         // none, then push the chunk's survivors to the row's queue
         auto slow_path = [&](const float* v, int32_t rel, int32_t e_lo, int32_t e_hi, bool hit) {
-          ++hit_rounds;
-          hit_lanes += hit ? 1 : 0;
+          if (FIC_TC_PROF) {  // statistics (profiling builds only: registers are tight)
+            ++hit_rounds;
+            hit_lanes += hit ? 1 : 0;
+          }
           const long long ts0 = TCLK();
           const int32_t wl = max(e_lo, 0), wh = min(e_hi, CH);
           uint64_t wmask = 0;
@@ -599,7 +601,7 @@ __global__ void __maxnreg__(MAXREG)
           }
           const bool seed = hit && thr_bits == 0x7ff0000000000000ull;
           if (__any_sync(0xffffffffu, seed)) {
-            ++seed_rounds;
+            if (FIC_TC_PROF) ++seed_rounds;
             double tnew = INFINITY;
             if (seed) {
               float bv = -1.0f;
@@ -682,7 +684,7 @@ __global__ void __maxnreg__(MAXREG)
           for (int h = 0; h < SW / CH; ++h) {
             const int32_t rel = j * BN + slice * SW + CH * h;
             const int32_t e_lo = lo32 - rel, e_hi = hi32 - rel;
-            const bool hit = !(debug & 8) && rvalid && e_lo < CH && e_hi > 0 && mx[h] >= s_r;
+            const bool hit = !(debug & 8) & rvalid & (e_lo < CH) & (e_hi > 0) & (mx[h] >= s_r);
             if (__any_sync(0xffffffffu, hit)) slow_path(v + CH * h, rel, e_lo, e_hi, hit);
           }
         } else {
@@ -833,7 +835,7 @@ __global__ void __maxnreg__(MAXREG)
     for (int m = 16; m >= 1; m >>= 1) evals += __shfl_xor_sync(0xffffffffu, evals, m);
     if (lane == 0) atomicAdd(a.counters, evals);
     if (lane == 0 && seed_rounds) atomicAdd(a.counters + 14, seed_rounds);  // warp-level seeding rounds
-    if (!DBG) {  // hit statistics (warp-level rounds, lanes)
+    if (!DBG && FIC_TC_PROF) {  // hit statistics (warp-level rounds, lanes)
       for (int m = 16; m >= 1; m >>= 1) hit_lanes += __shfl_xor_sync(0xffffffffu, hit_lanes, m);
       if (lane == 0 && hit_rounds) {
         atomicAdd(a.counters + 12, hit_rounds);
