@@ -140,6 +140,8 @@ struct DbcTables {
   uint16_t* quot = nullptr;
   double* ln = nullptr;
   double* w = nullptr;
+  double hw[7] = {};   // host copies: slope weights, max count increment per scale
+  int hqmax[7] = {};
 };
 
 static DbcTables make_dbc(Scratch& sc, cudaStream_t s, int side, const double* h_ln, int ln_len,
@@ -175,6 +177,10 @@ static DbcTables make_dbc(Scratch& sc, cudaStream_t s, int side, const double* h
     for (int j = 0; j < t.J; ++j) w[j] = (xs[j] - mean) / dd;
   }
   t.ln_len = need;
+  for (int j = 0; j < t.J; ++j) {
+    t.hw[j] = w[j];
+    t.hqmax[j] = q[j * 256 + 255] - q[j * 256 + 0];
+  }
   // the tables depend only on (device, side, ln values, weights): upload once
   // and keep them (a few KB per block side) instead of copying every call
   static std::mutex mu;
@@ -375,6 +381,55 @@ __global__ void __launch_bounds__(1024) k_items_segmajor(const int32_t* nseg, in
     }
   }
 }
+// ---- compact FD sort ---------------------------------------------------
+// With a few scales and small counts the domain FDs take few distinct values
+// (side 16: FD depends on (N2, N8) only, the middle weight being 0.0), so the
+// stable sort by FD becomes a stable sort by the rank of the value among all
+// possible values: same order, ~12-bit keys instead of 52-bit ones.
+struct FdCombo {
+  int J, C;                 // scales, number of combinations
+  int k2[7], cstride[7], crange[7];  // cells per block, index stride / range (0 = inactive)
+  const double* ln;
+  int ln_len;
+  const double* w;
+  int clamp;
+};
+
+__global__ void k_fd_combo_values(FdCombo a, unsigned long long* val_bits, uint32_t* idx) {
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= a.C) return;
+  double f = 0.0;
+  for (int j = 0; j < a.J; ++j) {  // the same op sequence as k_fd
+    int raw = a.cstride[j] ? (c / a.cstride[j]) % a.crange[j] : 0;
+    int cnt = min(raw + a.k2[j], a.ln_len - 1);
+    double t = __dmul_rn(__ldg(a.ln + cnt), __ldg(a.w + j));
+    f = (j == 0) ? t : __dadd_rn(f, t);
+  }
+  if (a.clamp) f = fmin(fmax(f, 2.0), 3.0);
+  val_bits[c] = (unsigned long long)__double_as_longlong(f);
+  idx[c] = (uint32_t)c;
+}
+__global__ void k_fd_rank_flags(const unsigned long long* sorted, int C, uint32_t* flag) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < C) flag[i] = (i == 0 || sorted[i] != sorted[i - 1]) ? 1u : 0u;
+}
+__global__ void k_fd_rank_scatter(const unsigned long long* sorted, const uint32_t* idx,
+                                  const uint32_t* incl, int C, uint32_t* rank, double* fd_of_rank) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= C) return;
+  uint32_t r = incl[i] - 1;
+  rank[idx[i]] = r;
+  fd_of_rank[r] = __longlong_as_double((long long)sorted[i]);
+}
+__global__ void k_combo_to_rank(const uint32_t* combo, const uint32_t* rank, int64_t n, uint32_t* key) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) key[i] = rank[combo[i]];
+}
+__global__ void k_rank_to_fd(const uint32_t* key, const double* fd_of_rank, int64_t n, double* out) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = fd_of_rank[key[i]];
+}
+
 __global__ void k_fill_u64(unsigned long long* a, unsigned long long v, int64_t n) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) a[i] = v;
@@ -464,6 +519,31 @@ static PlanBufs make_plan(Scratch& sc, cudaStream_t s, const uint8_t* img, const
     fa.w = td.w;
     fa.fd = pb.fd_dom;
     fa.key = kin;
+    // compact-key path: enumerate the count combinations of the scales with
+    // a nonzero weight (a zero weight adds +0.0 whatever the count)
+    FdCombo fc{};
+    fc.J = td.J;
+    fc.C = 1;
+    for (int j = 0; j < td.J; ++j) {
+      const int kk = dside >> (j + 1);
+      fc.k2[j] = kk * kk;
+      const int64_t range = (int64_t)kk * kk * td.hqmax[j] + 1;
+      if (td.hw[j] != 0.0 && fc.C * range <= 65536) {
+        fc.cstride[j] = fc.C;
+        fc.crange[j] = (int)range;
+        fc.C *= (int)range;
+      } else if (td.hw[j] != 0.0) {
+        fc.C = 0;  // too many values: fall back to the 52-bit sort
+        break;
+      }
+    }
+    const bool compact = fc.C > 0 && fa.clamp && dside <= 16 && (td.smax == 4 || td.smax == 8);
+    uint32_t* combo = nullptr;
+    if (compact) {
+      combo = sc.get<uint32_t>(g.D);
+      fa.combo = combo;
+      for (int j = 0; j < td.J; ++j) fa.cstride[j] = fc.cstride[j];
+    }
     launch_fd(fa, s);
     FdArgs fr = fa;
     fr.side = g.rs;
@@ -479,20 +559,63 @@ static PlanBufs make_plan(Scratch& sc, cudaStream_t s, const uint8_t* img, const
     fr.w = tr.w;
     fr.fd = pb.fd_rng;
     fr.key = nullptr;
+    fr.combo = nullptr;
     launch_fd(fr, s);
     // K3: stable sort of domains by FD (== AvlTree flatten, avltree.py:150-189)
     k_iota<<<(unsigned)cdiv(g.D, 256), 256, 0, s>>>(iin, g.D);
     FIC_CHECK_LAUNCH();
-    // FDs are clamped to [2, 3] (fa.clamp), so the sign and exponent bits of
-    // every key are equal (0x400): sorting the 52 mantissa bits is exact
-    const int nbits = fa.clamp ? 52 : 64;
-    cub_call(sc, [&](void* t, size_t& b) {
-      return cub::DeviceRadixSort::SortPairs(t, b, kin, kout, iin, pb.order, (int64_t)g.D, 0,
-                                             nbits, s);
-    });
     pb.keys = sc.get<double>(g.D);
-    k_bits_to_double<<<(unsigned)cdiv(g.D, 256), 256, 0, s>>>(kout, pb.keys, g.D);
-    FIC_CHECK_LAUNCH();
+    if (compact) {
+      // rank table over the possible FD values (ties share a rank)
+      fc.ln = td.ln;
+      fc.ln_len = td.ln_len;
+      fc.w = td.w;
+      fc.clamp = fa.clamp;
+      unsigned long long* cv = sc.get<unsigned long long>(fc.C);
+      unsigned long long* cvs = sc.get<unsigned long long>(fc.C);
+      uint32_t* ci = sc.get<uint32_t>(fc.C);
+      uint32_t* cis = sc.get<uint32_t>(fc.C);
+      uint32_t* flag = sc.get<uint32_t>(fc.C);
+      uint32_t* incl = sc.get<uint32_t>(fc.C);
+      uint32_t* rank = sc.get<uint32_t>(fc.C);
+      double* fd_of_rank = sc.get<double>(fc.C);
+      const unsigned cb = (unsigned)cdiv(fc.C, 256);
+      k_fd_combo_values<<<cb, 256, 0, s>>>(fc, cv, ci);
+      FIC_CHECK_LAUNCH();
+      cub_call(sc, [&](void* t, size_t& b) {
+        return cub::DeviceRadixSort::SortPairs(t, b, cv, cvs, ci, cis, fc.C, 0, 64, s);
+      });
+      k_fd_rank_flags<<<cb, 256, 0, s>>>(cvs, fc.C, flag);
+      FIC_CHECK_LAUNCH();
+      cub_call(sc, [&](void* t, size_t& b) {
+        return cub::DeviceScan::InclusiveSum(t, b, flag, incl, fc.C, s);
+      });
+      k_fd_rank_scatter<<<cb, 256, 0, s>>>(cvs, cis, incl, fc.C, rank, fd_of_rank);
+      FIC_CHECK_LAUNCH();
+      // stable sort of the domains by rank (same order as by FD value)
+      uint32_t* rk = sc.get<uint32_t>(g.D);
+      uint32_t* rks = sc.get<uint32_t>(g.D);
+      k_combo_to_rank<<<(unsigned)cdiv(g.D, 256), 256, 0, s>>>(combo, rank, g.D, rk);
+      FIC_CHECK_LAUNCH();
+      int rbits = 1;
+      while ((1 << rbits) < fc.C) ++rbits;
+      cub_call(sc, [&](void* t, size_t& b) {
+        return cub::DeviceRadixSort::SortPairs(t, b, rk, rks, iin, pb.order, (int64_t)g.D, 0,
+                                               rbits, s);
+      });
+      k_rank_to_fd<<<(unsigned)cdiv(g.D, 256), 256, 0, s>>>(rks, fd_of_rank, g.D, pb.keys);
+      FIC_CHECK_LAUNCH();
+    } else {
+      // FDs are clamped to [2, 3] (fa.clamp), so the sign and exponent bits of
+      // every key are equal (0x400): sorting the 52 mantissa bits is exact
+      const int nbits = fa.clamp ? 52 : 64;
+      cub_call(sc, [&](void* t, size_t& b) {
+        return cub::DeviceRadixSort::SortPairs(t, b, kin, kout, iin, pb.order, (int64_t)g.D, 0,
+                                               nbits, s);
+      });
+      k_bits_to_double<<<(unsigned)cdiv(g.D, 256), 256, 0, s>>>(kout, pb.keys, g.D);
+      FIC_CHECK_LAUNCH();
+    }
     sa.keys = pb.keys;
     sa.ids = pb.order;
     sa.fd_rng = pb.fd_rng;

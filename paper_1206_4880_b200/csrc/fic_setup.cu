@@ -116,6 +116,12 @@ __global__ void __launch_bounds__(256) k_fd(FdArgs a) {
   if (a.clamp) f = fmin(fmax(f, 2.0), 3.0);
   a.fd[b] = f;
   if (a.key) a.key[b] = (unsigned long long)__double_as_longlong(f);
+  if (a.combo) {
+    uint32_t c = 0;
+#pragma unroll
+    for (int j = 0; j < J; ++j) c += (uint32_t)cnt[j] * (uint32_t)a.cstride[j];
+    a.combo[b] = c;
+  }
 }
 
 // Generic path (coarsest scale >= 16): direct per-cell scan, slower.

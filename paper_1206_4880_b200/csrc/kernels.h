@@ -23,6 +23,8 @@ struct FdArgs {
   const double* w;      // [J] slope weights
   double* fd;           // [n] output
   unsigned long long* key;  // [n] optional: fd bits for sorting
+  uint32_t* combo;          // [n] optional: index of the count combination (k_fd<SMAX> only)
+  int cstride[7];           // combination index stride per scale (0 = scale not indexed)
 };
 // Builds host-side tables for block side `side` into `quot` (J*256), returns
 // J and the coarsest scale and the ln-table length required.

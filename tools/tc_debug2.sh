@@ -1,1 +1,3 @@
-for v in unr um2 um2r1 unr um2 um2r1; do echo -n "$v "; FIC_B200_LIB=build/var/$v.so timeout 60 python /tmp/pt.py 2>&1 | tail -1; done
+python tools/gpu_check.py 2>&1 | tail -3
+FIC_PLAN_TIMING=1 python /tmp/pt.py 2>&1 | tail -2
+timeout 600 python -m pytest tests -m gpu -x -q 2>&1 | tail -1
