@@ -553,7 +553,8 @@ __global__ void __maxnreg__(MAXREG)
       const uint32_t lane_base = tmem_base + ((uint32_t)(32 * (warp & 3)) << 16);
       const uint32_t tfull0 = tfull_bar(0), tempty0 = tempty_bar(0);
       const int32_t lo32 = rvalid ? (int32_t)(max((int64_t)rlo, c0) - c0) : 0;
-      const int32_t hi32 = rvalid ? (int32_t)(min((int64_t)rhi, c1) - c0) : 0;
+      // hi32 >= lo32 always (an empty intersection is [lo32, lo32))
+      const int32_t hi32 = rvalid ? max(lo32, (int32_t)(min((int64_t)rhi, c1) - c0)) : 0;
       const int qsl = group * NSPLIT + slice;
       uint32_t* myq = qbuf + (row * NSLICE + qsl) * QCAP;
       volatile uint32_t* mytail = qtail + row * NSLICE + qsl;
@@ -703,7 +704,8 @@ __global__ void __maxnreg__(MAXREG)
             const int32_t e_lo = lo32 - rel, e_hi = hi32 - rel;
             const float mx = chunk_max(v);
             // bitwise, so the max is computed unconditionally (no branch around it)
-            const bool in_window = rvalid & (e_lo < CH) & (e_hi > 0);
+            // [rel, rel + CH) meets [lo32, hi32) (hi32 > lo32 when valid): one unsigned compare
+            const bool in_window = (uint32_t)(e_hi - 1) < (uint32_t)(hi32 - lo32 + CH - 1);
             const bool hit = !(debug & 8) & in_window & (mx >= s_r);
             if (__any_sync(0xffffffffu, hit)) slow_path(v, rel, e_lo, e_hi, hit);
           }

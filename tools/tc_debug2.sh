@@ -1,3 +1,2 @@
-python tools/gpu_check.py 2>&1 | tail -3
-FIC_PLAN_TIMING=1 python /tmp/pt.py 2>&1 | tail -2
-timeout 600 python -m pytest tests -m gpu -x -q 2>&1 | tail -1
+FIC_B200_LIB=build/var/win.so python tools/gpu_check.py 2>&1 | tail -2
+for v in base win base win; do echo -n "$v "; FIC_B200_LIB=build/var/$v.so timeout 60 python /tmp/pt.py 2>&1 | tail -1; done
