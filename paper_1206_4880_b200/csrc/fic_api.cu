@@ -657,7 +657,7 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
   const int shard = std::min(std::max(0, p.shard_index), nshard - 1);
   const bool tensor_ok = (p.matcher != FIC_MATCH_EXACT) && tc_supported(K);
   const int small_pool = p.small_pool > 0 ? p.small_pool : 256;
-  const int seg_t = p.max_segment > 0 ? (int)align_up(p.max_segment, 256) : 65536;
+  const int seg_t = p.max_segment > 0 ? (int)align_up(p.max_segment, 256) : 131072;
   // first segment of each tensor tile (a multiple of the 128-column N-tile);
   // a short one seeds thresholds early but measured no faster at cfg3
   const int seg0 = getenv("FIC_SEG0") ? std::max(128, atoi(getenv("FIC_SEG0")) / 128 * 128) : seg_t;
