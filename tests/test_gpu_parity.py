@@ -220,3 +220,16 @@ def test_cta_pair_matcher_equals_default(monkeypatch):
     assert b.stats["tensor_tiles"] > 0
     assert torch.equal(a.records, b.records)
     assert torch.equal(a.post_rms, b.post_rms) and torch.equal(a.pre_rms, b.pre_rms)
+
+
+def test_decode_full_size_matches_oracle():
+    """Decoder at the headline size: the GPU decode of the cfg3 code (10
+    iterations) is byte-identical to the oracle's (codec.py:516-598)."""
+    c = synth.CONFIGS["cfg3"]
+    img = c.make()
+    code, _ = codec.encode(img, c.strategy, range_size=c.range_size, domain_size=c.domain_size,
+                           stride=c.stride, isometries=True, delta=c.delta)
+    out = codec.decode(code, iterations=10)
+    ref = orc.decode(code.records, code.width, code.height, code.range_size, code.domain_size,
+                     code.stride, iterations=10)
+    assert np.array_equal(out, ref)
