@@ -316,7 +316,7 @@ __device__ __forceinline__ unsigned long long bytes8(const uint8_t* row, int k) 
 }
 
 template <int RS>
-__global__ void __launch_bounds__(256) k_pool(PoolArgs a) {
+__global__ void __launch_bounds__(256, 4) k_pool(PoolArgs a) {
   constexpr int K = RS * RS;
   int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= a.D) return;
