@@ -408,15 +408,20 @@ __global__ void __maxnreg__(MAXREG)
   // work items are handed out dynamically (one CTA-wide fetch per item; the
   // items are ordered segment-major, so the full-length segments go first);
   // cluster pairs walk a static stride
-  __shared__ long long s_next_item;
+  // s_item[k & 1] holds the k-th item of this CTA; the (k+1)-th is fetched
+  // when the k-th starts, so the TMA producer can prefetch its first B tiles
+  __shared__ long long s_item[2];
   if (CG == 1) {
-    if (threadIdx.x == 0) s_next_item = (long long)atomicAdd(a.item_ctr, 1ull);
+    if (threadIdx.x == 0) s_item[0] = (long long)atomicAdd(a.item_ctr, 1ull);
     __syncthreads();
   }
-  for (int64_t it = (CG == 1) ? (int64_t)s_next_item : (int64_t)(blockIdx.x / CG); it < a.n_items;
-       it = (CG == 1) ? (int64_t)s_next_item : it + gridDim.x / CG) {
+  int npre = 0;        // producer: B tiles of the current item issued during the previous one
+  uint32_t kitem = 0;  // items this CTA started
+  for (int64_t it = (CG == 1) ? (int64_t)s_item[0] : (int64_t)(blockIdx.x / CG); it < a.n_items;
+       it = (CG == 1) ? (int64_t)s_item[kitem & 1] : it + gridDim.x / CG) {
     const long long ti0 = TCLK();
     ++nitems;
+    if (CG == 1 && threadIdx.x == 0) s_item[(kitem + 1) & 1] = (long long)atomicAdd(a.item_ctr, 1ull);
     const int2 item = a.items[it];
     const int tile = item.x;
     const int64_t wlo = a.wlo[tile], whi = a.whi[tile];
@@ -491,7 +496,7 @@ __global__ void __maxnreg__(MAXREG)
 
     if (warp == 0) {
       // TMA producer: the whole warp walks the pipeline, one lane issues
-      for (int j = 0; j < nt; ++j) {
+      for (int j = npre; j < nt; ++j) {
         { long long t0 = TCLK(); mbar_wait(empty_bar(stage), ph ^ 1); tw0 += TCLK() - t0; }
         if ((debug & 32) && blockIdx.x == 0 && it == 0 && j < 64 && lane == 0) a.dbg[j * 24] = TCLK();
         if (elect_one()) {
@@ -507,6 +512,30 @@ __global__ void __maxnreg__(MAXREG)
         }
         __syncwarp();
         if (++stage == C::NST) { stage = 0; ph ^= 1; }
+      }
+      // prefetch the first B tiles of the next item into the ring (stages
+      // free up as this item's MMAs complete); the next item skips them
+      npre = 0;
+      if (CG == 1 && !(debug & 16)) {
+        const int64_t nit = s_item[(kitem + 1) & 1];
+        if (nit < a.n_items) {
+          const int2 nx = a.items[nit];
+          const int64_t nlo = a.wlo[nx.x], nhi = a.whi[nx.x];
+          const int64_t n0 = nx.y == 0 ? nlo : nlo + a.seg0 + (int64_t)(nx.y - 1) * a.seg_len;
+          const int64_t n1 = min(nhi, nx.y == 0 ? n0 + a.seg0 : n0 + a.seg_len);
+          const int nnt = (int)cdiv(n1 - n0, BN);
+          const int pre = min(nnt, C::NST / 2);
+          for (int j = 0; j < pre; ++j) {
+            mbar_wait(empty_bar(stage), ph ^ 1);
+            if (elect_one()) {
+              mbar_expect_tx(full_bar(stage), C::TX_BYTES);
+              tma_load<CG>(smem_u32(sB + stage * C::B_BYTES), &tmB, full_bar(stage), 0, (int)(n0 + (int64_t)j * BN));
+            }
+            __syncwarp();
+            if (++stage == C::NST) { stage = 0; ph ^= 1; }
+          }
+          npre = pre;
+        }
       }
     } else if (warp >= MMA0 && warp < MMA0 + NMMA && leader) {
       // MMA issuers: NMMA warps take turns (tile j goes to warp MMA0 + j % NMMA)
@@ -826,8 +855,8 @@ __global__ void __maxnreg__(MAXREG)
       }
     }
     gt += (uint32_t)nt;
+    ++kitem;
     const long long ti2 = TCLK();
-    if (CG == 1 && threadIdx.x == 0) s_next_item = (long long)atomicAdd(a.item_ctr, 1ull);
     cta_sync<CG>();
     if (warp == 0) tteardown += TCLK() - ti2;
     (void)ti1;
