@@ -273,7 +273,34 @@ def fd_cases():
     save("fd_cases.npz", **out)
 
 
+def bench_cases():
+    """The reference's benchmark run path (bench.py:216-269): RunRecord rows of
+    run_single for every strategy on its own synthetic corpus (timing columns
+    blanked), plus the CSV header."""
+    import json
+    corpus = rbench.synthetic_corpus(size=64, seed=7)
+    rows = []
+    for name, img in corpus.items():
+        for strat in rcodec.STRATEGIES:
+            rec, _code, _recon = rbench.run_single(name, img, strat, stride=4, isometries=True)
+            row = rec.to_row()
+            for col in rbench.TIMING_COLUMNS:
+                row[rbench.CSV_COLUMNS.index(col)] = ""
+            rows.append({"name": name, "strategy": strat, "row": row})
+    out = {"columns": rbench.CSV_COLUMNS, "timing_columns": list(rbench.TIMING_COLUMNS),
+           "images": {k: v.tolist() for k, v in corpus.items()}, "runs": rows}
+    path = os.path.join(HERE, "bench_cases.json")
+    with open(path, "w") as f:
+        json.dump(out, f)
+    print(f"wrote {path} ({os.path.getsize(path)} bytes)")
+
+
 if __name__ == "__main__":
-    fd_cases()
-    encode_cases()
-    delta_cases()
+    if len(sys.argv) > 1:
+        for fn in sys.argv[1:]:
+            globals()[fn]()
+    else:
+        fd_cases()
+        encode_cases()
+        delta_cases()
+        bench_cases()

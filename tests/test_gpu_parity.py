@@ -233,3 +233,23 @@ def test_decode_full_size_matches_oracle():
     ref = orc.decode(code.records, code.width, code.height, code.range_size, code.domain_size,
                      code.stride, iterations=10)
     assert np.array_equal(out, ref)
+
+
+@pytest.mark.gpu
+def test_run_single_rows_match_reference_bench_rows():
+    """runs.run_single on the GPU encoder reproduces every non-timing CSV
+    column of the reference's bench.run_single (golden: bench_cases.json)."""
+    import json
+    import os
+    from conftest import ROOT
+    from paper_1206_4880_b200 import runs
+    g = json.loads(open(os.path.join(ROOT, "tests", "golden", "bench_cases.json")).read())
+    timing = [g["columns"].index(c) for c in g["timing_columns"]]
+    for run in g["runs"]:
+        img = np.array(g["images"][run["name"]], dtype=np.uint8)
+        rec, code, recon = runs.run_single(run["name"], img, run["strategy"], stride=4,
+                                           isometries=True)
+        row = rec.to_row()
+        for i in timing:
+            row[i] = ""
+        assert row == run["row"], run["name"] + "/" + run["strategy"]

@@ -136,3 +136,49 @@ def test_make_params_fields():
     assert (p.shard_index, p.shard_count, p.n_fd_weights_dom, p.n_fd_weights_rng) == (1, 4, 3, 2)
     with pytest.raises(ValueError, match="unknown matcher"):
         codec.make_params("dynamic_fd", 8, 16, 2, True, "original", None, "bogus", (0, 1))
+
+
+def _bench_cases():
+    import json
+    return json.loads(open(os.path.join(ROOT, "tests", "golden", "bench_cases.json")).read())
+
+
+def test_run_record_columns_and_formatting_match_reference():
+    from paper_1206_4880_b200 import runs
+    g = _bench_cases()
+    assert runs.CSV_COLUMNS == g["columns"]
+    assert list(runs.TIMING_COLUMNS) == g["timing_columns"]
+    # a record rebuilt from a reference row formats back to the same strings
+    row = g["runs"][0]["row"]
+    typed = dict(zip(g["columns"], row))
+    rec = runs.RunRecord(
+        image_name=typed["image_name"], image_size=int(typed["image_size"]),
+        range_size=int(typed["range_size"]), domain_size=int(typed["domain_size"]),
+        stride=int(typed["stride"]), isometries=bool(int(typed["isometries"])),
+        strategy=typed["strategy"], strategy_id=int(typed["strategy_id"]),
+        encode_seconds=1.25, fd_overhead_seconds=0.0,
+        comparisons=int(typed["comparisons"]), mean_pool_size=float(typed["mean_pool_size"]),
+        domain_count=int(typed["domain_count"]), compressed_bytes=int(typed["compressed_bytes"]),
+        pre_rms_mean=float(typed["pre_rms_mean"]), post_rms_mean=float(typed["post_rms_mean"]),
+        psnr_db=float(typed["psnr_db"]), decode_iterations=int(typed["decode_iterations"]))
+    out = rec.to_row()
+    assert out[8:10] == ["1.250000", "0.000000"]
+    assert out[:8] + out[10:] == row[:8] + row[10:]
+    rec.psnr_db = rec.decode_iterations = None
+    assert rec.to_row()[-2:] == ["", ""]
+
+
+def test_write_csv_and_pgm(tmp_path):
+    import csv
+    from paper_1206_4880_b200 import runs
+    rec = runs.RunRecord("img", 64, 8, 16, 4, False, "nosearch", 1, 0.1, 0.0, 10, 1.0, 169,
+                         100, 1.0, 2.0, float("inf"), 10)
+    runs.write_csv([rec, rec], tmp_path / "r.csv")
+    rows = list(csv.reader(open(tmp_path / "r.csv")))
+    assert rows[0] == runs.CSV_COLUMNS and len(rows) == 3 and rows[1][16] == "inf"
+    img = (np.arange(12, dtype=np.uint8) * 20).reshape(3, 4)
+    runs.write_pgm(img, tmp_path / "i.pgm")
+    assert (tmp_path / "i.pgm").read_bytes() == b"P5\n4 3\n255\n" + img.tobytes()
+    assert runs.fidelity_psnr(img, img) == float("inf")
+    with pytest.raises(ValueError, match="dimension mismatch"):
+        runs.fidelity_psnr(img, img[:2])
