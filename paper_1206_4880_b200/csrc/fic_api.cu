@@ -83,6 +83,25 @@ struct Timer {
   }
 };
 
+// Side stream (one per thread and device): the pool builder and the range
+// preparation run on it, overlapping the FD sort and the work planning on
+// the caller's stream; event-ordered both ways.
+struct SideStream {
+  cudaStream_t s2 = nullptr;
+  cudaEvent_t ev[6] = {};  // 0 fork (after ranges alloc), 1 fork (order ready), 2 join, 3..4 pool timing
+  static SideStream& get() {
+    static thread_local std::map<int, SideStream> m;
+    int dev = 0;
+    FIC_CUDA(cudaGetDevice(&dev));
+    SideStream& ss = m[dev];
+    if (!ss.s2) {
+      FIC_CUDA(cudaStreamCreateWithFlags(&ss.s2, cudaStreamNonBlocking));
+      for (auto& e : ss.ev) FIC_CUDA(cudaEventCreate(&e));
+    }
+    return ss;
+  }
+};
+
 static const char* kStrategyTuple = "('exhaustive', 'nosearch', 'static2', 'dynamic_fd')";
 
 // Validation in the reference's order (codec.py:313-331, blocks.py:63-68,
@@ -142,6 +161,7 @@ struct DbcTables {
   double* w = nullptr;
   double hw[7] = {};   // host copies: slope weights, max count increment per scale
   int hqmax[7] = {};
+  const std::vector<double>* hln = nullptr;  // host copy of the ln table (cached, never freed)
 };
 
 static DbcTables make_dbc(Scratch& sc, cudaStream_t s, int side, const double* h_ln, int ln_len,
@@ -199,6 +219,7 @@ static DbcTables make_dbc(Scratch& sc, cudaStream_t s, int side, const double* h
   FIC_CUDA(cudaMemcpy(t.quot, q.data(), t.J * 256 * sizeof(uint16_t), cudaMemcpyHostToDevice));
   FIC_CUDA(cudaMemcpy(t.ln, ln.data(), need * sizeof(double), cudaMemcpyHostToDevice));
   FIC_CUDA(cudaMemcpy(t.w, w.data(), t.J * sizeof(double), cudaMemcpyHostToDevice));
+  t.hln = new std::vector<double>(ln);
   cache.emplace(std::move(key), t);
   (void)sc;
   (void)s;
@@ -385,49 +406,64 @@ __global__ void __launch_bounds__(1024) k_items_segmajor(const int32_t* nseg, in
 // With a few scales and small counts the domain FDs take few distinct values
 // (side 16: FD depends on (N2, N8) only, the middle weight being 0.0), so the
 // stable sort by FD becomes a stable sort by the rank of the value among all
-// possible values: same order, ~12-bit keys instead of 52-bit ones.
+// possible values: same order, ~12-bit keys instead of 52-bit ones.  The
+// rank table depends only on the DBC tables, so the host builds it once (the
+// same fp64 op sequence as the kernels: product, then left-to-right sum,
+// clamp) and keeps it on the device.
 struct FdCombo {
   int J, C;                 // scales, number of combinations
   int k2[7], cstride[7], crange[7];  // cells per block, index stride / range (0 = inactive)
-  const double* ln;
-  int ln_len;
-  const double* w;
-  int clamp;
+};
+struct RankTable {
+  uint32_t* rank_of_combo = nullptr;  // [C]
+  double* fd_of_rank = nullptr;       // [n_rank] strictly increasing
+  int n_rank = 0;
 };
 
-__global__ void k_fd_combo_values(FdCombo a, unsigned long long* val_bits, uint32_t* idx) {
-  int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= a.C) return;
-  double f = 0.0;
-  for (int j = 0; j < a.J; ++j) {  // the same op sequence as k_fd
-    int raw = a.cstride[j] ? (c / a.cstride[j]) % a.crange[j] : 0;
-    int cnt = min(raw + a.k2[j], a.ln_len - 1);
-    double t = __dmul_rn(__ldg(a.ln + cnt), __ldg(a.w + j));
-    f = (j == 0) ? t : __dadd_rn(f, t);
+static RankTable make_rank_table(const DbcTables& td, const FdCombo& fc, int clamp) {
+  static std::mutex mu;
+  static std::map<std::vector<int64_t>, RankTable> cache;
+  int dev = 0;
+  FIC_CUDA(cudaGetDevice(&dev));
+  std::vector<int64_t> key{dev, (int64_t)(uintptr_t)td.quot, fc.J, fc.C, clamp};
+  for (int j = 0; j < fc.J; ++j) {
+    key.push_back(fc.k2[j]);
+    key.push_back(fc.cstride[j]);
+    key.push_back(fc.crange[j]);
   }
-  if (a.clamp) f = fmin(fmax(f, 2.0), 3.0);
-  val_bits[c] = (unsigned long long)__double_as_longlong(f);
-  idx[c] = (uint32_t)c;
-}
-__global__ void k_fd_rank_flags(const unsigned long long* sorted, int C, uint32_t* flag) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < C) flag[i] = (i == 0 || sorted[i] != sorted[i - 1]) ? 1u : 0u;
-}
-__global__ void k_fd_rank_scatter(const unsigned long long* sorted, const uint32_t* idx,
-                                  const uint32_t* incl, int C, uint32_t* rank, double* fd_of_rank) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= C) return;
-  uint32_t r = incl[i] - 1;
-  rank[idx[i]] = r;
-  fd_of_rank[r] = __longlong_as_double((long long)sorted[i]);
-}
-__global__ void k_combo_to_rank(const uint32_t* combo, const uint32_t* rank, int64_t n, uint32_t* key) {
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) key[i] = rank[combo[i]];
-}
-__global__ void k_rank_to_fd(const uint32_t* key, const double* fd_of_rank, int64_t n, double* out) {
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) out[i] = fd_of_rank[key[i]];
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  const std::vector<double>& ln = *td.hln;
+  std::vector<double> val(fc.C);
+  for (int c = 0; c < fc.C; ++c) {
+    double f = 0.0;
+    for (int j = 0; j < fc.J; ++j) {  // k_fd: __dmul_rn then __dadd_rn, no contraction
+      const int raw = fc.cstride[j] ? (c / fc.cstride[j]) % fc.crange[j] : 0;
+      const int cnt = std::min(raw + fc.k2[j], td.ln_len - 1);
+      volatile double t = ln[cnt] * td.hw[j];
+      f = (j == 0) ? (double)t : f + (double)t;
+    }
+    if (clamp) f = std::fmin(std::fmax(f, 2.0), 3.0);
+    val[c] = f;
+  }
+  std::vector<int> idx(fc.C);
+  for (int c = 0; c < fc.C; ++c) idx[c] = c;
+  std::stable_sort(idx.begin(), idx.end(), [&](int x, int y) { return val[x] < val[y]; });
+  std::vector<uint32_t> rank(fc.C);
+  std::vector<double> fdr;
+  for (int i = 0; i < fc.C; ++i) {
+    if (i == 0 || val[idx[i]] != val[idx[i - 1]]) fdr.push_back(val[idx[i]]);
+    rank[idx[i]] = (uint32_t)(fdr.size() - 1);
+  }
+  RankTable rt;
+  rt.n_rank = (int)fdr.size();
+  FIC_CUDA(cudaMalloc(&rt.rank_of_combo, fc.C * sizeof(uint32_t)));
+  FIC_CUDA(cudaMalloc(&rt.fd_of_rank, fdr.size() * sizeof(double)));
+  FIC_CUDA(cudaMemcpy(rt.rank_of_combo, rank.data(), fc.C * sizeof(uint32_t), cudaMemcpyHostToDevice));
+  FIC_CUDA(cudaMemcpy(rt.fd_of_rank, fdr.data(), fdr.size() * sizeof(double), cudaMemcpyHostToDevice));
+  cache.emplace(std::move(key), rt);
+  return rt;
 }
 
 __global__ void k_fill_u64(unsigned long long* a, unsigned long long v, int64_t n) {
@@ -466,7 +502,7 @@ struct PlanBufs {
 };
 
 static PlanBufs make_plan(Scratch& sc, cudaStream_t s, const uint8_t* img, const Geo& g,
-                          const fic_params_t& p) {
+                          const fic_params_t& p, bool want_fd_dom) {
   PlanBufs pb;
   pb.lo = sc.get<int32_t>(g.R);
   pb.hi = sc.get<int32_t>(g.R);
@@ -496,10 +532,8 @@ static PlanBufs make_plan(Scratch& sc, cudaStream_t s, const uint8_t* img, const
                             p.n_fd_weights_dom);
     DbcTables tr = make_dbc(sc, s, g.rs, p.h_ln_table, p.ln_len, p.h_fd_weights_rng,
                             p.n_fd_weights_rng);
-    pb.fd_dom = sc.get<double>(g.D);
+    pb.fd_dom = want_fd_dom ? sc.get<double>(g.D) : nullptr;
     pb.fd_rng = sc.get<double>(g.R);
-    unsigned long long* kin = sc.get<unsigned long long>(g.D);
-    unsigned long long* kout = sc.get<unsigned long long>(g.D);
     uint32_t* iin = sc.get<uint32_t>(g.D);
     pb.order = sc.get<uint32_t>(g.D);
     FdArgs fa{};
@@ -518,7 +552,6 @@ static PlanBufs make_plan(Scratch& sc, cudaStream_t s, const uint8_t* img, const
     fa.ln_len = td.ln_len;
     fa.w = td.w;
     fa.fd = pb.fd_dom;
-    fa.key = kin;
     // compact-key path: enumerate the count combinations of the scales with
     // a nonzero weight (a zero weight adds +0.0 whatever the count)
     FdCombo fc{};
@@ -537,20 +570,32 @@ static PlanBufs make_plan(Scratch& sc, cudaStream_t s, const uint8_t* img, const
         break;
       }
     }
-    const bool compact = fc.C > 0 && fa.clamp && dside <= 16 && (td.smax == 4 || td.smax == 8);
-    uint32_t* combo = nullptr;
+    const bool compact = fc.C > 0 && fa.clamp && dside <= 16 && (td.smax == 4 || td.smax == 8) &&
+                         !getenv("FIC_FD_WIDE_SORT");
+    RankTable rt;
+    uint32_t* rk = nullptr;
+    unsigned long long* kin = nullptr;
     if (compact) {
-      combo = sc.get<uint32_t>(g.D);
-      fa.combo = combo;
+      rt = make_rank_table(td, fc, fa.clamp);
+      rk = sc.get<uint32_t>(g.D);
+      fa.rank_of_combo = rt.rank_of_combo;
+      fa.rank = rk;
       for (int j = 0; j < td.J; ++j) fa.cstride[j] = fc.cstride[j];
+    } else {
+      kin = sc.get<unsigned long long>(g.D);
+      fa.key = kin;
     }
+    fa.iota = iin;
     launch_fd(fa, s);
-    FdArgs fr = fa;
+    FdArgs fr{};
+    fr.src = img;
+    fr.W = g.W;
     fr.side = g.rs;
     fr.bst = g.rs;
     fr.nbx = g.nrx;
     fr.n = g.R;
     fr.mode = FD_IMAGE;
+    fr.clamp = 1;
     fr.J = tr.J;
     fr.smax = tr.smax;
     fr.quot = tr.quot;
@@ -558,65 +603,38 @@ static PlanBufs make_plan(Scratch& sc, cudaStream_t s, const uint8_t* img, const
     fr.ln_len = tr.ln_len;
     fr.w = tr.w;
     fr.fd = pb.fd_rng;
-    fr.key = nullptr;
-    fr.combo = nullptr;
     launch_fd(fr, s);
     // K3: stable sort of domains by FD (== AvlTree flatten, avltree.py:150-189)
-    k_iota<<<(unsigned)cdiv(g.D, 256), 256, 0, s>>>(iin, g.D);
-    FIC_CHECK_LAUNCH();
-    pb.keys = sc.get<double>(g.D);
     if (compact) {
-      // rank table over the possible FD values (ties share a rank)
-      fc.ln = td.ln;
-      fc.ln_len = td.ln_len;
-      fc.w = td.w;
-      fc.clamp = fa.clamp;
-      unsigned long long* cv = sc.get<unsigned long long>(fc.C);
-      unsigned long long* cvs = sc.get<unsigned long long>(fc.C);
-      uint32_t* ci = sc.get<uint32_t>(fc.C);
-      uint32_t* cis = sc.get<uint32_t>(fc.C);
-      uint32_t* flag = sc.get<uint32_t>(fc.C);
-      uint32_t* incl = sc.get<uint32_t>(fc.C);
-      uint32_t* rank = sc.get<uint32_t>(fc.C);
-      double* fd_of_rank = sc.get<double>(fc.C);
-      const unsigned cb = (unsigned)cdiv(fc.C, 256);
-      k_fd_combo_values<<<cb, 256, 0, s>>>(fc, cv, ci);
-      FIC_CHECK_LAUNCH();
-      cub_call(sc, [&](void* t, size_t& b) {
-        return cub::DeviceRadixSort::SortPairs(t, b, cv, cvs, ci, cis, fc.C, 0, 64, s);
-      });
-      k_fd_rank_flags<<<cb, 256, 0, s>>>(cvs, fc.C, flag);
-      FIC_CHECK_LAUNCH();
-      cub_call(sc, [&](void* t, size_t& b) {
-        return cub::DeviceScan::InclusiveSum(t, b, flag, incl, fc.C, s);
-      });
-      k_fd_rank_scatter<<<cb, 256, 0, s>>>(cvs, cis, incl, fc.C, rank, fd_of_rank);
-      FIC_CHECK_LAUNCH();
       // stable sort of the domains by rank (same order as by FD value)
-      uint32_t* rk = sc.get<uint32_t>(g.D);
       uint32_t* rks = sc.get<uint32_t>(g.D);
-      k_combo_to_rank<<<(unsigned)cdiv(g.D, 256), 256, 0, s>>>(combo, rank, g.D, rk);
-      FIC_CHECK_LAUNCH();
       int rbits = 1;
-      while ((1 << rbits) < fc.C) ++rbits;
+      while ((1 << rbits) < rt.n_rank) ++rbits;
       cub_call(sc, [&](void* t, size_t& b) {
         return cub::DeviceRadixSort::SortPairs(t, b, rk, rks, iin, pb.order, (int64_t)g.D, 0,
                                                rbits, s);
       });
-      k_rank_to_fd<<<(unsigned)cdiv(g.D, 256), 256, 0, s>>>(rks, fd_of_rank, g.D, pb.keys);
-      FIC_CHECK_LAUNCH();
+      uint32_t* rstart = sc.get<uint32_t>(rt.n_rank + 1);
+      launch_rank_start(rks, g.D, rt.n_rank, rstart, s);
+      sa.keys = nullptr;
+      sa.rk = rks;
+      sa.fd_of_rank = rt.fd_of_rank;
+      sa.rank_start = rstart;
+      sa.n_rank = rt.n_rank;
     } else {
       // FDs are clamped to [2, 3] (fa.clamp), so the sign and exponent bits of
       // every key are equal (0x400): sorting the 52 mantissa bits is exact
+      unsigned long long* kout = sc.get<unsigned long long>(g.D);
       const int nbits = fa.clamp ? 52 : 64;
       cub_call(sc, [&](void* t, size_t& b) {
         return cub::DeviceRadixSort::SortPairs(t, b, kin, kout, iin, pb.order, (int64_t)g.D, 0,
                                                nbits, s);
       });
+      pb.keys = sc.get<double>(g.D);
       k_bits_to_double<<<(unsigned)cdiv(g.D, 256), 256, 0, s>>>(kout, pb.keys, g.D);
       FIC_CHECK_LAUNCH();
+      sa.keys = pb.keys;
     }
-    sa.keys = pb.keys;
     sa.ids = pb.order;
     sa.fd_rng = pb.fd_rng;
   }
@@ -674,10 +692,31 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
     if (ptime && pn < 24) FIC_CUDA(cudaEventRecord(tm.ev[pn++], s));
   };
   tm.mark();  // 0
-  PlanBufs pb = make_plan(sc, s, img, g, p);
+  SideStream& side = SideStream::get();
+
+  // ranges (side stream: needs only the image)
+  std::vector<int> perm(8 * K), inv(8 * K);
+  iso_tables(g.rs, perm.data(), inv.data());
+  int* d_inv = sc.get<int>(8 * K);
+  FIC_CUDA(cudaMemcpyAsync(d_inv, inv.data(), 8 * K * sizeof(int), cudaMemcpyHostToDevice, s));
+  RangeArgs ra{};
+  ra.img = img;
+  ra.W = g.W;
+  ra.rs = g.rs;
+  ra.nrx = g.nrx;
+  ra.R = g.R;
+  ra.n_iso = g.n_iso;
+  ra.inv_perm = d_inv;
+  ra.info = sc.get<RangeInfo>(g.R);
+  ra.rows = sc.get<uint8_t>((size_t)g.R * g.n_iso * K);
+  FIC_CUDA(cudaEventRecord(side.ev[0], s));
+  FIC_CUDA(cudaStreamWaitEvent(side.s2, side.ev[0], 0));
+  launch_ranges(ra, side.s2);
+
+  PlanBufs pb = make_plan(sc, s, img, g, p, false);
   tm.mark();  // 1
 
-  // K1 pool builder
+  // K1 pool builder (side stream: needs the FD order, overlaps the planning)
   PoolArgs pa{};
   pa.img = img;
   pa.H = g.H;
@@ -695,26 +734,14 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
   pa.inv_den = sc.get<double>(g.D);
   pa.sums = sc.get<uint2>(g.D);
   pa.ids = sc.get<uint32_t>(g.D);
-  launch_pool(pa, s);
+  FIC_CUDA(cudaEventRecord(side.ev[1], s));
+  FIC_CUDA(cudaStreamWaitEvent(side.s2, side.ev[1], 0));
+  FIC_CUDA(cudaEventRecord(side.ev[3], side.s2));
+  launch_pool(pa, side.s2);
+  FIC_CUDA(cudaEventRecord(side.ev[4], side.s2));
+  FIC_CUDA(cudaEventRecord(side.ev[2], side.s2));
   tm.mark();  // 2
-
-  // ranges
-  std::vector<int> perm(8 * K), inv(8 * K);
-  iso_tables(g.rs, perm.data(), inv.data());
-  int* d_inv = sc.get<int>(8 * K);
-  FIC_CUDA(cudaMemcpyAsync(d_inv, inv.data(), 8 * K * sizeof(int), cudaMemcpyHostToDevice, s));
-  RangeArgs ra{};
-  ra.img = img;
-  ra.W = g.W;
-  ra.rs = g.rs;
-  ra.nrx = g.nrx;
-  ra.R = g.R;
-  ra.n_iso = g.n_iso;
-  ra.inv_perm = d_inv;
-  ra.info = sc.get<RangeInfo>(g.R);
-  ra.rows = sc.get<uint8_t>((size_t)g.R * g.n_iso * K);
   pmark();  // 8
-  launch_ranges(ra, s);
   pmark();  // 9
 
   // plan: classify, sort by (class, lo, hi), shard by cost
@@ -813,6 +840,7 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
   }
 
   pmark();  // 14
+  FIC_CUDA(cudaStreamWaitEvent(s, side.ev[2], 0));  // join: pool + ranges
   PoolView P{pa.raw, pa.bh, pa.inv_den, pa.sums, pa.ids, g.D};
   RangeView Rv{ra.info, ra.rows, pb.lo, pb.hi, g.n_iso, K};
   tm.mark();  // 3
@@ -858,9 +886,9 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
   tm.mark();  // 7
   FIC_CUDA(cudaStreamSynchronize(s));
   if (ptime && pn == 15) {
-    fprintf(stderr, "plan timing (ms): fd %.3f pool %.3f | iso-upload %.3f ranges %.3f classify..shard %.3f sync1 %.3f "
+    fprintf(stderr, "plan timing (ms): fd %.3f pool(side) %.3f | fork %.3f - %.3f classify..shard %.3f sync1 %.3f "
             "tiles..totals %.3f sync2 %.3f items %.3f | tensor %.3f exact %.3f merge %.3f readback %.3f | seed rounds %llu hit rounds %llu hit lanes %llu\n",
-            tm.ms(0, 1), tm.ms(1, 2), tm.ms(2, 8), tm.ms(8, 9), tm.ms(9, 10), tm.ms(10, 11), tm.ms(11, 12),
+            tm.ms(0, 1), [&] { float t = 0; cudaEventElapsedTime(&t, side.ev[3], side.ev[4]); return (double)t; }(), tm.ms(2, 8), tm.ms(8, 9), tm.ms(9, 10), tm.ms(10, 11), tm.ms(11, 12),
             tm.ms(12, 13), tm.ms(13, 14), tm.ms(3, 4), tm.ms(4, 5), tm.ms(5, 6), tm.ms(6, 7), hc[14], hc[12], hc[13]);
   }
   if (st) {
@@ -873,7 +901,11 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
     st->fd_max = hs[1];
     st->half_width = p.strategy == FIC_DYNAMIC_FD ? hs[2] : 0.0;
     st->ms_fd = tm.ms(0, 1);
-    st->ms_pool = tm.ms(1, 2);
+    {
+      float t = 0;
+      cudaEventElapsedTime(&t, side.ev[3], side.ev[4]);
+      st->ms_pool = t;
+    }
     st->ms_match = tm.ms(3, 6);
     st->ms_tensor = tm.ms(3, 4);
     st->ms_exact = tm.ms(4, 5);
@@ -900,7 +932,7 @@ static void plan_impl(const uint8_t* img, int H, int W, const fic_params_t& p, d
     check_dbc_side(g.rs);
   }
   Scratch sc(s);
-  PlanBufs pb = make_plan(sc, s, img, g, p);
+  PlanBufs pb = make_plan(sc, s, img, g, p, fd_dom != nullptr);
   if (fd_dom && pb.fd_dom)
     FIC_CUDA(cudaMemcpyAsync(fd_dom, pb.fd_dom, g.D * sizeof(double), cudaMemcpyDeviceToDevice, s));
   if (fd_rng && pb.fd_rng)

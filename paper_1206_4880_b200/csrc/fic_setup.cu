@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "kernels.h"
@@ -114,14 +115,153 @@ __global__ void __launch_bounds__(256) k_fd(FdArgs a) {
     f = (j == 0) ? t : __dadd_rn(f, t);
   }
   if (a.clamp) f = fmin(fmax(f, 2.0), 3.0);
-  a.fd[b] = f;
+  if (a.fd) a.fd[b] = f;
   if (a.key) a.key[b] = (unsigned long long)__double_as_longlong(f);
-  if (a.combo) {
+  if (a.combo || a.rank) {
     uint32_t c = 0;
 #pragma unroll
     for (int j = 0; j < J; ++j) c += (uint32_t)cnt[j] * (uint32_t)a.cstride[j];
-    a.combo[b] = c;
+    if (a.rank_of_combo)
+      a.rank[b] = __ldg(a.rank_of_combo + c);
+    else
+      a.combo[b] = c;
   }
+  if (a.iota) a.iota[b] = (uint32_t)b;
+}
+
+// K2 for 16x16 domain blocks on the image (scales 2, 4, 8) at a small
+// stride: one CTA per T x T tile of domain positions.  The stride-1 domains
+// overlap almost entirely, so the per-cell maxima / minima are computed once
+// per pixel position of the tile's image patch (cell (y, x) of scale s covers
+// pixels [y, y+s) x [x, x+s), built from scale s/2 like fdim.py:63-72), the
+// per-cell count increments floor(max/h) - floor(min/h) are stored, and each
+// block's count is a strided sum of them, done separably (rows, then
+// columns).  Same integer counts as k_fd, hence the same FD bits.
+template <int T>
+__global__ void __launch_bounds__(256) k_fd16_tile(FdArgs a) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  __shared__ uint16_t quot[3][256];
+  for (int i = threadIdx.x; i < 3 * 256; i += blockDim.x) quot[i >> 8][i & 255] = a.quot[i];
+  const int st = a.bst;
+  const int PW = (T - 1) * st + 16;  // patch side (pixels)
+  const int PP = PW * PW;
+  uint8_t* P = sm;
+  uint8_t* X2 = P + PP;
+  uint8_t* N2 = X2 + PP;
+  uint8_t* C2 = N2 + PP;
+  uint8_t* X4 = C2 + PP;
+  uint8_t* N4 = X4 + PP;
+  uint8_t* C4 = N4 + PP;
+  uint8_t* C8 = C4 + PP;
+  uint16_t* H2 = reinterpret_cast<uint16_t*>(sm + ((8 * PP + 15) & ~15));
+  uint16_t* H4 = H2 + PW * T;
+  uint16_t* H8 = H4 + PW * T;
+  const int64_t nby = a.n / a.nbx;
+  const int kx0 = blockIdx.x * T, ky0 = blockIdx.y * T;
+  const int x0 = kx0 * st, y0 = ky0 * st;
+  const int Himg = (int)((nby - 1) * st + 16), Wimg = a.W;
+  for (int i = threadIdx.x; i < PP; i += blockDim.x) {
+    const int y = i / PW, x = i - (i / PW) * PW;
+    const int gy = y0 + y, gx = x0 + x;
+    P[i] = (gy < Himg && gx < Wimg) ? __ldg(a.src + (int64_t)gy * Wimg + gx) : 0;
+  }
+  __syncthreads();
+  // scale 2 cells at every patch position
+  for (int i = threadIdx.x; i < PP; i += blockDim.x) {
+    const int y = i / PW, x = i - (i / PW) * PW;
+    if (y < PW - 1 && x < PW - 1) {
+      const int p0 = P[i], p1 = P[i + 1], p2 = P[i + PW], p3 = P[i + PW + 1];
+      const int mx = max(max(p0, p1), max(p2, p3)), mn = min(min(p0, p1), min(p2, p3));
+      X2[i] = (uint8_t)mx;
+      N2[i] = (uint8_t)mn;
+      C2[i] = (uint8_t)(quot[0][mx] - quot[0][mn]);
+    }
+  }
+  __syncthreads();
+  // scale 4 from four scale-2 cells
+  for (int i = threadIdx.x; i < PP; i += blockDim.x) {
+    const int y = i / PW, x = i - (i / PW) * PW;
+    if (y < PW - 3 && x < PW - 3) {
+      const int mx = max(max(X2[i], X2[i + 2]), max(X2[i + 2 * PW], X2[i + 2 * PW + 2]));
+      const int mn = min(min(N2[i], N2[i + 2]), min(N2[i + 2 * PW], N2[i + 2 * PW + 2]));
+      X4[i] = (uint8_t)mx;
+      N4[i] = (uint8_t)mn;
+      C4[i] = (uint8_t)(quot[1][mx] - quot[1][mn]);
+    }
+  }
+  __syncthreads();
+  // scale 8 from four scale-4 cells
+  for (int i = threadIdx.x; i < PP; i += blockDim.x) {
+    const int y = i / PW, x = i - (i / PW) * PW;
+    if (y < PW - 7 && x < PW - 7) {
+      const int mx = max(max(X4[i], X4[i + 4]), max(X4[i + 4 * PW], X4[i + 4 * PW + 4]));
+      const int mn = min(min(N4[i], N4[i + 4]), min(N4[i + 4 * PW], N4[i + 4 * PW + 4]));
+      C8[i] = (uint8_t)(quot[2][mx] - quot[2][mn]);
+    }
+  }
+  __syncthreads();
+  // row sums over each block's cells: H_s[y][lx] = sum_j C_s[y][lx*st + s*j]
+  for (int i = threadIdx.x; i < PW * T; i += blockDim.x) {
+    const int y = i / T, lx = i - (i / T) * T;
+    const uint8_t* r2 = C2 + y * PW + lx * st;
+    int h2 = 0, h4 = 0, h8 = 0;
+    if (y < PW - 1) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) h2 += r2[2 * j];
+    }
+    if (y < PW - 3) {
+      const uint8_t* r4 = C4 + y * PW + lx * st;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) h4 += r4[4 * j];
+    }
+    if (y < PW - 7) {
+      const uint8_t* r8 = C8 + y * PW + lx * st;
+      h8 = r8[0] + r8[8];
+    }
+    H2[i] = (uint16_t)h2;
+    H4[i] = (uint16_t)h4;
+    H8[i] = (uint16_t)h8;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < T * T; i += blockDim.x) {
+    const int ly = i / T, lx = i - (i / T) * T;
+    const int ky = ky0 + ly, kx = kx0 + lx;
+    if (ky >= nby || kx >= a.nbx) continue;
+    const int Y = ly * st;
+    int cnt[3] = {0, 0, 0};
+#pragma unroll
+    for (int r = 0; r < 8; ++r) cnt[0] += H2[(Y + 2 * r) * T + lx];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) cnt[1] += H4[(Y + 4 * r) * T + lx];
+    cnt[2] = H8[Y * T + lx] + H8[(Y + 8) * T + lx];
+    double f = 0.0;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      const int k = 16 >> (j + 1);
+      const int c = min(cnt[j] + k * k, a.ln_len - 1);
+      const double t = __dmul_rn(__ldg(a.ln + c), __ldg(a.w + j));
+      f = (j == 0) ? t : __dadd_rn(f, t);
+    }
+    if (a.clamp) f = fmin(fmax(f, 2.0), 3.0);
+    const int64_t b = (int64_t)ky * a.nbx + kx;
+    if (a.fd) a.fd[b] = f;
+    if (a.key) a.key[b] = (unsigned long long)__double_as_longlong(f);
+    if (a.combo || a.rank) {
+      uint32_t c = 0;
+#pragma unroll
+      for (int j = 0; j < 3; ++j) c += (uint32_t)cnt[j] * (uint32_t)a.cstride[j];
+      if (a.rank_of_combo)
+        a.rank[b] = __ldg(a.rank_of_combo + c);
+      else
+        a.combo[b] = c;
+    }
+    if (a.iota) a.iota[b] = (uint32_t)b;
+  }
+}
+
+static size_t fd16_tile_smem(int T, int st) {
+  const int PW = (T - 1) * st + 16, PP = PW * PW;
+  return (size_t)((8 * PP + 15) & ~15) + (size_t)3 * PW * T * sizeof(uint16_t);
 }
 
 // Generic path (coarsest scale >= 16): direct per-cell scan, slower.
@@ -158,15 +298,36 @@ __global__ void k_fd_generic(FdArgs a) {
     f = (j == 0) ? t : __dadd_rn(f, t);
   }
   if (a.clamp) f = fmin(fmax(f, 2.0), 3.0);
-  a.fd[b] = f;
+  if (a.fd) a.fd[b] = f;
   if (a.key) a.key[b] = (unsigned long long)__double_as_longlong(f);
+  if (a.iota) a.iota[b] = (uint32_t)b;
 }
 
 void launch_fd(const FdArgs& a, cudaStream_t s) {
   if (a.n == 0) return;
   int threads = 256;
   int64_t blocks = cdiv(a.n, threads);
-  if (a.smax == 4 && a.J == 2)
+  const bool tile_ok = a.mode == FD_IMAGE && a.side == 16 && a.J == 3 && a.smax == 8 &&
+                       a.bst >= 1 && a.bst <= 4 && !getenv("FIC_FD_DIRECT");
+  if (tile_ok) {
+    const int64_t nby = a.n / a.nbx;
+    if (a.bst == 1) {
+      constexpr int T = 32;
+      dim3 grid((unsigned)cdiv(a.nbx, T), (unsigned)cdiv(nby, T));
+      k_fd16_tile<T><<<grid, 256, fd16_tile_smem(T, 1), s>>>(a);
+    } else {
+      constexpr int T = 16;
+      const size_t smem = fd16_tile_smem(T, a.bst);
+      static bool attr = false;
+      if (!attr) {
+        FIC_CUDA(cudaFuncSetAttribute(k_fd16_tile<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)fd16_tile_smem(T, 4)));
+        attr = true;
+      }
+      dim3 grid((unsigned)cdiv(a.nbx, T), (unsigned)cdiv(nby, T));
+      k_fd16_tile<T><<<grid, 256, smem, s>>>(a);
+    }
+  } else if (a.smax == 4 && a.J == 2)
     k_fd<4><<<(unsigned)blocks, threads, 0, s>>>(a);
   else if (a.smax == 8 && a.J == 3)
     k_fd<8><<<(unsigned)blocks, threads, 0, s>>>(a);
@@ -199,32 +360,68 @@ __device__ __forceinline__ int64_t upper_bound(const double* k, int64_t n, doubl
   return lo;
 }
 
+// Sorted-key access: either the key array or, in rank form, a lookup of the
+// rank's value; searches in rank form run over the (few) distinct values and
+// map back to positions through rank_start -- the same positions, since the
+// values are strictly increasing in the rank.
+struct Keys {
+  const SlabArgs& a;
+  __device__ __forceinline__ double at(int64_t p) const {
+    return a.keys ? a.keys[p] : __ldg(a.fd_of_rank + __ldg(a.rk + p));
+  }
+  __device__ __forceinline__ int64_t lower(double v) const {
+    if (a.keys) return lower_bound(a.keys, a.D, v);
+    return __ldg(a.rank_start + lower_bound(a.fd_of_rank, a.n_rank, v));
+  }
+  __device__ __forceinline__ int64_t upper(double v) const {
+    if (a.keys) return upper_bound(a.keys, a.D, v);
+    return __ldg(a.rank_start + upper_bound(a.fd_of_rank, a.n_rank, v));
+  }
+};
+
 __global__ void k_slab_scalars(SlabArgs a) {
   if (threadIdx.x || blockIdx.x) return;
-  double fmn = a.keys[0], fmx = a.keys[a.D - 1];  // fdim.py:93-100
+  Keys k{a};
+  double fmn = k.at(0), fmx = k.at(a.D - 1);  // fdim.py:93-100
   a.scal[0] = fmn;
   a.scal[1] = fmx;
   if (a.strategy == FIC_STATIC2) {
     double mid = __ddiv_rn(__dadd_rn(fmn, fmx), 2.0);
     a.scal[2] = mid;
-    a.scal[3] = (double)lower_bound(a.keys, a.D, mid);
+    a.scal[3] = (double)k.lower(mid);
   } else {
     a.scal[2] = a.has_delta ? a.delta : __ddiv_rn(__dsub_rn(fmx, fmn), 3.0);
     a.scal[3] = 0.0;
   }
 }
 
-__device__ int64_t nearest_fd(const double* keys, const uint32_t* ids, int64_t n, double v) {
+__device__ int64_t nearest_fd(const Keys& k, const uint32_t* ids, int64_t n, double v) {
   // codec.py:267-287
-  int64_t pos = lower_bound(keys, n, v);
+  int64_t pos = k.lower(v);
   int64_t pl = pos > 0 ? pos - 1 : 0;
   int64_t pr = pos < n - 1 ? pos : n - 1;
-  int64_t left = lower_bound(keys, n, keys[pl]);
-  int64_t right = lower_bound(keys, n, keys[pr]);
-  double d_lo = pos > 0 ? __dsub_rn(v, keys[pl]) : INFINITY;
-  double d_hi = pos < n ? __dsub_rn(keys[pr], v) : INFINITY;
+  const double kl = k.at(pl), kr = k.at(pr);
+  int64_t left = k.lower(kl);
+  int64_t right = k.lower(kr);
+  double d_lo = pos > 0 ? __dsub_rn(v, kl) : INFINITY;
+  double d_hi = pos < n ? __dsub_rn(kr, v) : INFINITY;
   bool take_left = (d_lo < d_hi) || (d_lo == d_hi && ids[left] < ids[right]);
   return take_left ? left : right;
+}
+
+// rank_start[r] = first sorted position whose rank is >= r, for r in [0, n_rank]
+__global__ void k_rank_start(const uint32_t* rks, int64_t D, int n_rank, uint32_t* start) {
+  int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p > D) return;
+  const int r = p < D ? (int)rks[p] : n_rank;
+  const int prev = p > 0 ? (int)rks[p - 1] : -1;
+  for (int q = prev + 1; q <= r; ++q) start[q] = (uint32_t)p;
+}
+
+void launch_rank_start(const uint32_t* rks, int64_t D, int n_rank, uint32_t* start,
+                       cudaStream_t s) {
+  k_rank_start<<<(unsigned)cdiv(D + 1, 256), 256, 0, s>>>(rks, D, n_rank, start);
+  FIC_CHECK_LAUNCH();
 }
 
 __device__ __forceinline__ int64_t floordiv(int64_t a, int64_t b) {
@@ -264,11 +461,12 @@ __global__ void k_slabs(SlabArgs a) {
       hi = below ? b : a.D;
     } else {
       double half = a.scal[2];
-      lo = lower_bound(a.keys, a.D, __dsub_rn(f, half));
-      hi = upper_bound(a.keys, a.D, __dadd_rn(f, half));
+      Keys k{a};
+      lo = k.lower(__dsub_rn(f, half));
+      hi = k.upper(__dadd_rn(f, half));
     }
     if (hi <= lo) {
-      lo = nearest_fd(a.keys, a.ids, a.D, f);
+      lo = nearest_fd(Keys{a}, a.ids, a.D, f);
       hi = lo + 1;
     }
   }

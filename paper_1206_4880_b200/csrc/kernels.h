@@ -25,6 +25,9 @@ struct FdArgs {
   unsigned long long* key;  // [n] optional: fd bits for sorting
   uint32_t* combo;          // [n] optional: index of the count combination (k_fd<SMAX> only)
   int cstride[7];           // combination index stride per scale (0 = scale not indexed)
+  const uint32_t* rank_of_combo;  // optional [C]: write rank_of_combo[combo] to `rank`
+  uint32_t* rank;                 // [n] (with rank_of_combo; replaces combo)
+  uint32_t* iota;                 // [n] optional: iota[b] = b (sort payload)
 };
 // Builds host-side tables for block side `side` into `quot` (J*256), returns
 // J and the coarsest scale and the ln-table length required.
@@ -33,7 +36,13 @@ void launch_fd(const FdArgs& a, cudaStream_t s);
 
 // ---- K3: FD index + slabs (avltree.py:150-189, codec.py:343-375) ------------
 struct SlabArgs {
-  const double* keys;      // sorted domain FDs (pool order)
+  const double* keys;      // sorted domain FDs (pool order); nullptr = rank form below
+  // rank form (compact FD sort): key of pool position p = fd_of_rank[rk[p]],
+  // rank_start[r] = first pool position with rank >= r (r <= n_rank)
+  const uint32_t* rk;
+  const double* fd_of_rank;
+  const uint32_t* rank_start;
+  int n_rank;
   const uint32_t* ids;     // raster id per pool position
   const double* fd_rng;    // [R]
   int64_t D;
@@ -48,6 +57,8 @@ struct SlabArgs {
   int H, W, rs, ds, st, nrx, ndx;
 };
 void launch_slabs(const SlabArgs& a, cudaStream_t s);
+void launch_rank_start(const uint32_t* rks, int64_t D, int n_rank, uint32_t* start,
+                       cudaStream_t s);
 
 // ---- K1: pool builder (blocks.py:75-82, codec.py:136-145) -------------------
 struct PoolArgs {

@@ -85,6 +85,41 @@ def test_plan_fd_and_slabs_bit_exact(name):
     assert np.array_equal(p["slab_hi"], ENC[f"{name}.slab_hi"])
 
 
+@pytest.mark.parametrize("stride", [1, 2, 3, 4, 5])
+@pytest.mark.parametrize("shape,seed", [((96, 136), 7), ((120, 80), 8), ((64, 64), 9)])
+def test_plan_tiled_fd_matches_oracle(stride, shape, seed):
+    """The tiled DBC kernel (16x16 domains, strides 1-4; stride 5 takes the
+    per-block kernel) gives the oracle's FD bits, order and slabs on images
+    whose domain grid ends inside a tile, for both strategies that use FD."""
+    rng = np.random.default_rng(seed)
+    img = synth.to_u8(synth.fbm(max(shape), 0.2 + 0.1 * (seed - 7), rng))[:shape[0], :shape[1]]
+    img = np.ascontiguousarray(img)
+    # a flat patch and a checkerboard patch (zero and maximal counts)
+    img[:24, :24] = 77
+    img[-20:, -20:] = np.where((np.indices((20, 20)).sum(0) % 2) == 0, 0, 255)
+    for strat, delta in (("dynamic_fd", None), ("dynamic_fd", 0.05), ("static2", None)):
+        p = codec.plan(img, strat, stride=stride, delta=delta)
+        ref = orc.plan_pools(img, strat, 8, 16, stride, delta=delta)
+        assert np.array_equal(p["fd_dom"], ref.fd_dom), (strat, delta)
+        assert np.array_equal(p["fd_rng"], ref.fd_rng), (strat, delta)
+        assert np.array_equal(p["order"], ref.order), (strat, delta)
+        assert np.array_equal(p["slab_lo"], ref.lo), (strat, delta)
+        assert np.array_equal(p["slab_hi"], ref.hi), (strat, delta)
+
+
+def test_plan_tiled_fd_equals_direct_at_cfg3(monkeypatch):
+    """Full-size property: the tiled DBC kernel and the per-block kernel
+    (FIC_FD_DIRECT) agree bit for bit on all 1,018,081 cfg3 domains, and the
+    rank-keyed sort equals the 52-bit FD sort (FIC_FD_WIDE_SORT)."""
+    img = synth.CONFIGS["cfg3"].make()
+    a = codec.plan(img, "dynamic_fd", stride=1, delta=0.05)
+    monkeypatch.setenv("FIC_FD_DIRECT", "1")
+    monkeypatch.setenv("FIC_FD_WIDE_SORT", "1")
+    b = codec.plan(img, "dynamic_fd", stride=1, delta=0.05)
+    for k in ("fd_dom", "fd_rng", "order", "slab_lo", "slab_hi"):
+        assert np.array_equal(a[k], b[k]), k
+
+
 def test_dbc_grid_known_answers():
     for side in (8, 16, 32):
         assert np.array_equal(codec.dbc_grid(FD[f"rand{side}.blocks"]), FD[f"rand{side}.fd"])
