@@ -181,6 +181,23 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def _pool_roofline(stats, peak_gbs, src):
+    """HBM roofline of the pool builder K1 (k_boxplanes + k_pool, DESIGN.md
+    section 4): algorithmic bytes = the image read once + per domain the 4 B
+    order entry read and 3K + 20 B written (raw K u8, fp16 B row 2K,
+    inv_den 8, sums 8, ids 4), over the device time of the two launches
+    (timed with events on the side stream they run on, concurrent with the
+    planning kernels)."""
+    D, K, HW = 1009 * 1009, 64, 1024 * 1024
+    ms = float(np.mean([s["ms_pool"] for s in stats]))
+    nbytes = HW + D * (4 + 3 * K + 20)
+    gbs = nbytes / (ms / 1e3) / 1e9 if ms > 0 else 0.0
+    return {"bound": "hbm", "kernel": "k_boxplanes + k_pool (pool builder K1)", "achieved": gbs,
+            "peak": peak_gbs, "unit": "GB/s", "frac": gbs / peak_gbs,
+            "peak_source": f"{src} copy bandwidth", "algorithmic_bytes_per_launch": nbytes,
+            "ms_per_launch": ms, "traffic": None}
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -271,6 +288,7 @@ def run_ours(args):
                      "frac": achieved / peak_tf, "peak_source": f"{src} bf16 dense burst "
                      "(fp16 same rate)", "algorithmic_flops_per_launch": 2 * 64 * tcomp,
                      "ms_per_launch": ms_t, "traffic": _traffic_from_profile()},
+        "roofline_hbm": _pool_roofline(stats, peak_gbs, src),
         "e2e": {"value": comps / e2e_s, "unit": UNIT, "encode_ms": 1e3 * e2e_s,
                 "h2d_bytes_per_step": int(img.nbytes),
                 "d2h_bytes_per_step": n_r * (7 + 8 + 8 + 8)},

@@ -502,7 +502,7 @@ struct PlanBufs {
 };
 
 static PlanBufs make_plan(Scratch& sc, cudaStream_t s, const uint8_t* img, const Geo& g,
-                          const fic_params_t& p, bool want_fd_dom) {
+                          const fic_params_t& p, bool want_fd_dom, bool stable_order) {
   PlanBufs pb;
   pb.lo = sc.get<int32_t>(g.R);
   pb.hi = sc.get<int32_t>(g.R);
@@ -575,17 +575,30 @@ static PlanBufs make_plan(Scratch& sc, cudaStream_t s, const uint8_t* img, const
     RankTable rt;
     uint32_t* rk = nullptr;
     unsigned long long* kin = nullptr;
+    uint32_t* hist = nullptr;
+    bool count_sort = false;
     if (compact) {
       rt = make_rank_table(td, fc, fa.clamp);
       rk = sc.get<uint32_t>(g.D);
       fa.rank_of_combo = rt.rank_of_combo;
       fa.rank = rk;
       for (int j = 0; j < td.J; ++j) fa.cstride[j] = fc.cstride[j];
+      // encode does not need the reference's order among equal FDs (see
+      // k_rank_scatter); plan() returns it, so it keeps the stable sort
+      count_sort = !stable_order && rt.n_rank <= kCountSortMaxRanks && !getenv("FIC_FD_STABLE");
+      if (count_sort) {
+        hist = sc.get<uint32_t>(2 * rt.n_rank);
+        FIC_CUDA(cudaMemsetAsync(hist, 0, rt.n_rank * sizeof(uint32_t), s));
+        FIC_CUDA(cudaMemsetAsync(hist + rt.n_rank, 0xff, rt.n_rank * sizeof(uint32_t), s));
+        fa.rank_hist = hist;
+        fa.rank_minid = hist + rt.n_rank;
+        fa.n_rank = rt.n_rank;
+      }
     } else {
       kin = sc.get<unsigned long long>(g.D);
       fa.key = kin;
     }
-    fa.iota = iin;
+    fa.iota = count_sort ? nullptr : iin;
     launch_fd(fa, s);
     FdArgs fr{};
     fr.src = img;
@@ -606,18 +619,22 @@ static PlanBufs make_plan(Scratch& sc, cudaStream_t s, const uint8_t* img, const
     launch_fd(fr, s);
     // K3: stable sort of domains by FD (== AvlTree flatten, avltree.py:150-189)
     if (compact) {
-      // stable sort of the domains by rank (same order as by FD value)
-      uint32_t* rks = sc.get<uint32_t>(g.D);
-      int rbits = 1;
-      while ((1 << rbits) < rt.n_rank) ++rbits;
-      cub_call(sc, [&](void* t, size_t& b) {
-        return cub::DeviceRadixSort::SortPairs(t, b, rk, rks, iin, pb.order, (int64_t)g.D, 0,
-                                               rbits, s);
-      });
       uint32_t* rstart = sc.get<uint32_t>(rt.n_rank + 1);
-      launch_rank_start(rks, g.D, rt.n_rank, rstart, s);
+      if (count_sort) {
+        uint32_t* cursor = sc.get<uint32_t>(rt.n_rank);
+        launch_count_sort(rk, g.D, rt.n_rank, hist, hist + rt.n_rank, rstart, cursor, pb.order, s);
+      } else {
+        // stable sort of the domains by rank (same order as by FD value)
+        uint32_t* rks = sc.get<uint32_t>(g.D);
+        int rbits = 1;
+        while ((1 << rbits) < rt.n_rank) ++rbits;
+        cub_call(sc, [&](void* t, size_t& b) {
+          return cub::DeviceRadixSort::SortPairs(t, b, rk, rks, iin, pb.order, (int64_t)g.D, 0,
+                                                 rbits, s);
+        });
+        launch_rank_start(rks, g.D, rt.n_rank, rstart, s);
+      }
       sa.keys = nullptr;
-      sa.rk = rks;
       sa.fd_of_rank = rt.fd_of_rank;
       sa.rank_start = rstart;
       sa.n_rank = rt.n_rank;
@@ -713,7 +730,7 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
   FIC_CUDA(cudaStreamWaitEvent(side.s2, side.ev[0], 0));
   launch_ranges(ra, side.s2);
 
-  PlanBufs pb = make_plan(sc, s, img, g, p, false);
+  PlanBufs pb = make_plan(sc, s, img, g, p, false, false);
   tm.mark();  // 1
 
   // K1 pool builder (side stream: needs the FD order, overlaps the planning)
@@ -932,7 +949,7 @@ static void plan_impl(const uint8_t* img, int H, int W, const fic_params_t& p, d
     check_dbc_side(g.rs);
   }
   Scratch sc(s);
-  PlanBufs pb = make_plan(sc, s, img, g, p, fd_dom != nullptr);
+  PlanBufs pb = make_plan(sc, s, img, g, p, fd_dom != nullptr, true);
   if (fd_dom && pb.fd_dom)
     FIC_CUDA(cudaMemcpyAsync(fd_dom, pb.fd_dom, g.D * sizeof(double), cudaMemcpyDeviceToDevice, s));
   if (fd_rng && pb.fd_rng)

@@ -1,6 +1,7 @@
 // Setup kernels of the encoder hot path: FD (K2), slabs (K3), pool builder
 // (K1), range preparation.  sm_100a.  See DESIGN.md §Kernels.
 #include <cuda_fp16.h>
+#include <cub/block/block_scan.cuh>
 #include <math.h>
 
 #include <algorithm>
@@ -121,10 +122,16 @@ __global__ void __launch_bounds__(256) k_fd(FdArgs a) {
     uint32_t c = 0;
 #pragma unroll
     for (int j = 0; j < J; ++j) c += (uint32_t)cnt[j] * (uint32_t)a.cstride[j];
-    if (a.rank_of_combo)
-      a.rank[b] = __ldg(a.rank_of_combo + c);
-    else
+    if (a.rank_of_combo) {
+      const uint32_t r = __ldg(a.rank_of_combo + c);
+      a.rank[b] = r;
+      if (a.rank_hist) {
+        atomicAdd(a.rank_hist + r, 1u);
+        atomicMin(a.rank_minid + r, (uint32_t)b);
+      }
+    } else {
       a.combo[b] = c;
+    }
   }
   if (a.iota) a.iota[b] = (uint32_t)b;
 }
@@ -156,6 +163,13 @@ __global__ void __launch_bounds__(256) k_fd16_tile(FdArgs a) {
   uint16_t* H2 = reinterpret_cast<uint16_t*>(sm + ((8 * PP + 15) & ~15));
   uint16_t* H4 = H2 + PW * T;
   uint16_t* H8 = H4 + PW * T;
+  uint32_t* hist = reinterpret_cast<uint32_t*>(H8 + PW * T + (PW * T & 1));  // [n_rank] if rank_hist
+  uint32_t* minid = hist + a.n_rank;                                            // [n_rank]
+  if (a.rank_hist)
+    for (int r = threadIdx.x; r < a.n_rank; r += blockDim.x) {
+      hist[r] = 0;
+      minid[r] = 0xffffffffu;
+    }
   const int64_t nby = a.n / a.nbx;
   const int kx0 = blockIdx.x * T, ky0 = blockIdx.y * T;
   const int x0 = kx0 * st, y0 = ky0 * st;
@@ -250,18 +264,33 @@ __global__ void __launch_bounds__(256) k_fd16_tile(FdArgs a) {
       uint32_t c = 0;
 #pragma unroll
       for (int j = 0; j < 3; ++j) c += (uint32_t)cnt[j] * (uint32_t)a.cstride[j];
-      if (a.rank_of_combo)
-        a.rank[b] = __ldg(a.rank_of_combo + c);
-      else
+      if (a.rank_of_combo) {
+        const uint32_t r = __ldg(a.rank_of_combo + c);
+        a.rank[b] = r;
+        if (a.rank_hist) {
+          atomicAdd(hist + r, 1u);
+          atomicMin(minid + r, (uint32_t)b);
+        }
+      } else {
         a.combo[b] = c;
+      }
     }
     if (a.iota) a.iota[b] = (uint32_t)b;
   }
+  if (a.rank_hist) {
+    __syncthreads();
+    for (int r = threadIdx.x; r < a.n_rank; r += blockDim.x)
+      if (hist[r]) {
+        atomicAdd(a.rank_hist + r, hist[r]);
+        atomicMin(a.rank_minid + r, minid[r]);
+      }
+  }
 }
 
-static size_t fd16_tile_smem(int T, int st) {
+static size_t fd16_tile_smem(int T, int st, int n_rank) {
   const int PW = (T - 1) * st + 16, PP = PW * PW;
-  return (size_t)((8 * PP + 15) & ~15) + (size_t)3 * PW * T * sizeof(uint16_t);
+  return (size_t)((8 * PP + 15) & ~15) + (size_t)(3 * PW * T + (PW * T & 1)) * sizeof(uint16_t) +
+         (size_t)2 * n_rank * sizeof(uint32_t);
 }
 
 // Generic path (coarsest scale >= 16): direct per-cell scan, slower.
@@ -311,21 +340,22 @@ void launch_fd(const FdArgs& a, cudaStream_t s) {
                        a.bst >= 1 && a.bst <= 4 && !getenv("FIC_FD_DIRECT");
   if (tile_ok) {
     const int64_t nby = a.n / a.nbx;
+    const int nr = a.rank_hist ? a.n_rank : 0;
+    static bool attr = false;
+    if (!attr) {
+      const int mx = (int)fd16_tile_smem(16, 4, kCountSortMaxRanks);
+      FIC_CUDA(cudaFuncSetAttribute(k_fd16_tile<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+      FIC_CUDA(cudaFuncSetAttribute(k_fd16_tile<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+      attr = true;
+    }
     if (a.bst == 1) {
       constexpr int T = 32;
       dim3 grid((unsigned)cdiv(a.nbx, T), (unsigned)cdiv(nby, T));
-      k_fd16_tile<T><<<grid, 256, fd16_tile_smem(T, 1), s>>>(a);
+      k_fd16_tile<T><<<grid, 256, fd16_tile_smem(T, 1, nr), s>>>(a);
     } else {
       constexpr int T = 16;
-      const size_t smem = fd16_tile_smem(T, a.bst);
-      static bool attr = false;
-      if (!attr) {
-        FIC_CUDA(cudaFuncSetAttribute(k_fd16_tile<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)fd16_tile_smem(T, 4)));
-        attr = true;
-      }
       dim3 grid((unsigned)cdiv(a.nbx, T), (unsigned)cdiv(nby, T));
-      k_fd16_tile<T><<<grid, 256, smem, s>>>(a);
+      k_fd16_tile<T><<<grid, 256, fd16_tile_smem(T, a.bst, nr), s>>>(a);
     }
   } else if (a.smax == 4 && a.J == 2)
     k_fd<4><<<(unsigned)blocks, threads, 0, s>>>(a);
@@ -360,6 +390,15 @@ __device__ __forceinline__ int64_t upper_bound(const double* k, int64_t n, doubl
   return lo;
 }
 
+__device__ __forceinline__ int64_t upper_bound_u32(const uint32_t* k, int64_t n, uint32_t v) {
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    int64_t m = (lo + hi) >> 1;
+    if (k[m] <= v) lo = m + 1; else hi = m;
+  }
+  return lo;
+}
+
 // Sorted-key access: either the key array or, in rank form, a lookup of the
 // rank's value; searches in rank form run over the (few) distinct values and
 // map back to positions through rank_start -- the same positions, since the
@@ -367,7 +406,9 @@ __device__ __forceinline__ int64_t upper_bound(const double* k, int64_t n, doubl
 struct Keys {
   const SlabArgs& a;
   __device__ __forceinline__ double at(int64_t p) const {
-    return a.keys ? a.keys[p] : __ldg(a.fd_of_rank + __ldg(a.rk + p));
+    if (a.keys) return a.keys[p];
+    // rank of position p: the last r with rank_start[r] <= p
+    return __ldg(a.fd_of_rank + (upper_bound_u32(a.rank_start, a.n_rank + 1, (uint32_t)p) - 1));
   }
   __device__ __forceinline__ int64_t lower(double v) const {
     if (a.keys) return lower_bound(a.keys, a.D, v);
@@ -421,6 +462,86 @@ __global__ void k_rank_start(const uint32_t* rks, int64_t D, int n_rank, uint32_
 void launch_rank_start(const uint32_t* rks, int64_t D, int n_rank, uint32_t* start,
                        cudaStream_t s) {
   k_rank_start<<<(unsigned)cdiv(D + 1, 256), 256, 0, s>>>(rks, D, n_rank, start);
+  FIC_CHECK_LAUNCH();
+}
+
+// Counting sort of the domains by FD rank: the FD kernel counted the ranks
+// (rank_hist); one block turns the counts into bucket starts (= rank_start),
+// then each block of the scatter reserves, per rank, a run inside the bucket
+// with one global atomic and places its domains there.  Ties (equal FD) end
+// up in an unspecified order -- the pools are the same sets (slabs cover
+// whole runs of equal keys) and the matcher's tie rule uses the raster id,
+// so the encode result does not depend on it -- except the nearest-FD
+// fallback (codec.py:267-287), which takes a run's first element, the
+// smallest raster index in the stable order: that one is placed first.
+__global__ void __launch_bounds__(1024) k_rank_scan(const uint32_t* hist, int n_rank, int64_t D,
+                                                    uint32_t* start, uint32_t* cursor) {
+  using Scan = cub::BlockScan<uint32_t, 1024>;
+  __shared__ typename Scan::TempStorage tmp;
+  constexpr int IPT = kCountSortMaxRanks / 1024;
+  uint32_t v[IPT];
+#pragma unroll
+  for (int i = 0; i < IPT; ++i) {
+    const int r = threadIdx.x * IPT + i;
+    v[i] = r < n_rank ? hist[r] : 0u;
+  }
+  Scan(tmp).ExclusiveSum(v, v);
+#pragma unroll
+  for (int i = 0; i < IPT; ++i) {
+    const int r = threadIdx.x * IPT + i;
+    if (r < n_rank) {
+      start[r] = v[i];
+      cursor[r] = v[i] + 1u;  // slot v[i] holds the bucket's smallest index
+    }
+  }
+  if (threadIdx.x == 0) start[n_rank] = (uint32_t)D;
+}
+
+__global__ void __launch_bounds__(1024) k_rank_scatter(const uint32_t* rank, int64_t D, int n_rank,
+                                                       const uint32_t* minid, const uint32_t* start,
+                                                       uint32_t* cursor, uint32_t* order) {
+  extern __shared__ uint32_t cnt[];  // [n_rank] counts, then bases
+  constexpr int IPT = 4;
+  for (int r = threadIdx.x; r < n_rank; r += blockDim.x) cnt[r] = 0;
+  __syncthreads();
+  const int64_t b0 = (int64_t)blockIdx.x * blockDim.x * IPT;
+  uint32_t rk[IPT], loc[IPT];
+#pragma unroll
+  for (int i = 0; i < IPT; ++i) {
+    const int64_t b = b0 + (int64_t)i * blockDim.x + threadIdx.x;
+    rk[i] = b < D ? __ldg(rank + b) : 0xffffffffu;
+    loc[i] = 0xffffffffu;
+    if (b < D) {
+      if ((uint32_t)b == __ldg(minid + rk[i]))
+        order[__ldg(start + rk[i])] = (uint32_t)b;  // the bucket's first slot
+      else
+        loc[i] = atomicAdd(cnt + rk[i], 1u);
+    }
+  }
+  __syncthreads();
+  for (int r = threadIdx.x; r < n_rank; r += blockDim.x)
+    if (cnt[r]) cnt[r] = atomicAdd(cursor + r, cnt[r]);
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < IPT; ++i) {
+    const int64_t b = b0 + (int64_t)i * blockDim.x + threadIdx.x;
+    if (b < D && loc[i] != 0xffffffffu) order[cnt[rk[i]] + loc[i]] = (uint32_t)b;
+  }
+}
+
+void launch_count_sort(const uint32_t* rank, int64_t D, int n_rank, const uint32_t* hist,
+                       const uint32_t* minid, uint32_t* start, uint32_t* cursor, uint32_t* order,
+                       cudaStream_t s) {
+  k_rank_scan<<<1, 1024, 0, s>>>(hist, n_rank, D, start, cursor);
+  FIC_CHECK_LAUNCH();
+  static bool attr = false;
+  if (!attr) {
+    FIC_CUDA(cudaFuncSetAttribute(k_rank_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  kCountSortMaxRanks * (int)sizeof(uint32_t)));
+    attr = true;
+  }
+  k_rank_scatter<<<(unsigned)cdiv(D, 4096), 1024, n_rank * sizeof(uint32_t), s>>>(
+      rank, D, n_rank, minid, start, cursor, order);
   FIC_CHECK_LAUNCH();
 }
 
@@ -513,56 +634,103 @@ __device__ __forceinline__ unsigned long long bytes8(const uint8_t* row, int k) 
   return sh ? ((lo >> sh) | (hi << (64 - sh))) : lo;
 }
 
+// One warp builds 32 consecutive pool positions.  Pass 1: RS lanes per
+// domain, one decimated row each (a short read from a box-floor plane), so a
+// warp instruction moves 32/RS whole domains: raw rows are stored as one
+// contiguous run, and the row sums are reduced across the RS lanes and
+// handed to lane j (domain p0 + j).  Lane j then does the per-domain fp64
+// work once (den, 1/den as codec.py:141-145, the row scale) and writes the
+// per-domain scalars coalesced.  Pass 2 converts the rows kept in registers
+// into fp16 B rows, again one contiguous run per instruction.
+//   B_k = fp16(fp32(K d_k - sum_d) * fp32(1 / sqrt(K den)))
+// fp32 rounding before the fp16 rounding is far inside the screen's error
+// budget (fic_tc.cu: eps has 2^-12 + 2^-13 of slack beyond fp16's 2^-11).
 template <int RS>
 __global__ void __launch_bounds__(256, 4) k_pool(PoolArgs a) {
   constexpr int K = RS * RS;
-  int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= a.D) return;
-  uint32_t id = a.order ? a.order[p] : (uint32_t)p;
-  int dy = (int)(id / (uint32_t)a.ndx), dx = (int)(id - (uint32_t)dy * a.ndx);
-  const int Y = dy * a.st, X = dx * a.st;
-  const uint8_t* plane = a.planes + (int64_t)(X & 1) * a.plane_rows * a.pitch;
-  uint32_t w[K / 4];
-  uint32_t sd = 0, sdd = 0;
+  constexpr int DPI = 32 / RS;  // domains per instruction
+  constexpr int NIT = RS;       // instructions per 32 domains
+  const int lane = threadIdx.x & 31;
+  const int64_t p0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32;
+  if (p0 >= a.D) return;
+  const int g = lane / RS, i = lane % RS;
+  const uint32_t ndx = (uint32_t)a.ndx, D = (uint32_t)a.D;
+  const uint32_t ip = (uint32_t)(2 * i) * (uint32_t)a.pitch;
+  const uint32_t plane_sz = (uint32_t)a.plane_rows * (uint32_t)a.pitch;
+  uint32_t w0[NIT], w1[NIT];  // the row's decimated bytes (RS == 4: w0 only)
+  uint32_t ks[NIT];           // domain sums of instruction k's domain g
+  uint32_t my_sd = 0, my_sdd = 0;
 #pragma unroll
-  for (int i = 0; i < RS; ++i) {
-    unsigned long long r8 = bytes8(plane + (int64_t)(Y + 2 * i) * a.pitch, X >> 1);
-#pragma unroll
-    for (int j = 0; j < RS; ++j) {
-      uint32_t x = (uint32_t)(r8 >> (8 * j)) & 255u;
-      sd += x;
-      sdd += x * x;
-    }
+  for (int k = 0; k < NIT; ++k) {
+    const uint32_t p = (uint32_t)p0 + k * DPI + g;
+    const bool ok = p < D;
+    const uint32_t id = ok ? (a.order ? __ldg(a.order + p) : p) : 0u;
+    const uint32_t dy = id / ndx, dx = id - dy * ndx;
+    const uint32_t Y = dy * a.st, X = dx * a.st;
+    const uint8_t* rowp = a.planes + (X & 1) * plane_sz + Y * a.pitch + ip;
+    const unsigned long long r = ok ? bytes8(rowp, X >> 1) : 0ull;
+    w0[k] = (uint32_t)r;
+    w1[k] = RS == 8 ? (uint32_t)(r >> 32) : 0u;
+    // row sums with byte dot products: sum x and sum x^2
+    uint32_t sd = __dp4a(w0[k], 0x01010101u, 0u), sdd = __dp4a(w0[k], w0[k], 0u);
     if (RS == 8) {
-      w[2 * i] = (uint32_t)r8;
-      w[2 * i + 1] = (uint32_t)(r8 >> 32);
-    } else {
-      w[i] = (uint32_t)r8;
+      sd = __dp4a(w1[k], 0x01010101u, sd);
+      sdd = __dp4a(w1[k], w1[k], sdd);
+    }
+#pragma unroll
+    for (int m = 1; m < RS; m <<= 1) {
+      sd += __shfl_xor_sync(0xffffffffu, sd, m);
+      sdd += __shfl_xor_sync(0xffffffffu, sdd, m);
+    }
+    ks[k] = sd;
+    const int src = ((lane - k * DPI) * RS) & 31;
+    const uint32_t t_sd = __shfl_sync(0xffffffffu, sd, src);
+    const uint32_t t_sdd = __shfl_sync(0xffffffffu, sdd, src);
+    if (lane / DPI == k) {
+      my_sd = t_sd;
+      my_sdd = t_sdd;
+    }
+    if (ok) {
+      if (RS == 8)
+        reinterpret_cast<uint2*>(a.raw + (size_t)p * K)[i] = make_uint2(w0[k], w1[k]);
+      else
+        reinterpret_cast<uint32_t*>(a.raw + (size_t)p * K)[i] = w0[k];
     }
   }
-  int64_t den = (int64_t)K * sdd - (int64_t)sd * sd;
-  a.inv_den[p] = den != 0 ? __ddiv_rn(1.0, (double)den) : 0.0;
-  a.sums[p] = make_uint2(sd, sdd);
-  a.ids[p] = id;
-  uint4* rw = reinterpret_cast<uint4*>(a.raw + p * K);
+  const uint32_t pm = (uint32_t)p0 + lane;
+  const int64_t den = (int64_t)K * my_sdd - (int64_t)my_sd * my_sd;
+  float my_scale = 0.0f;
+  if (pm < D) {
+    a.inv_den[pm] = den != 0 ? __ddiv_rn(1.0, (double)den) : 0.0;
+    a.sums[pm] = make_uint2(my_sd, my_sdd);
+    a.ids[pm] = a.order ? __ldg(a.order + pm) : pm;
+    my_scale = den > 0 ? (float)__drcp_rn(__dsqrt_rn((double)K * (double)den)) : 0.0f;
+  }
+  if (!a.bh) return;
+  // fp32 of byte x: 0x4B0000xx - 2^23 = x (exact), then K x - sum_d is an
+  // exact FFMA (|.| < 2^24)
 #pragma unroll
-  for (int q = 0; q < K / 16; ++q) rw[q] = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
-  if (a.bh) {
-    const double scale = den > 0 ? __drcp_rn(__dsqrt_rn((double)K * (double)den)) : 0.0;
-    uint4* bw = reinterpret_cast<uint4*>(a.bh + p * K);
+  for (int k = 0; k < NIT; ++k) {
+    const uint32_t p = (uint32_t)p0 + k * DPI + g;
+    const float sc = __shfl_sync(0xffffffffu, my_scale, (k * DPI + g) & 31);
+    const float off = -(float)ks[k];
+    uint32_t h[RS / 2];
 #pragma unroll
-    for (int q = 0; q < K / 8; ++q) {
-      uint32_t h[4];
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int k0 = 8 * q + 2 * e;
-        const int v0 = (w[k0 >> 2] >> (8 * (k0 & 3))) & 255, v1 = (w[(k0 + 1) >> 2] >> (8 * ((k0 + 1) & 3))) & 255;
-        const float f0 = (float)((double)(K * v0 - (int)sd) * scale);
-        const float f1 = (float)((double)(K * v1 - (int)sd) * scale);
-        __half2 hv = __floats2half2_rn(f0, f1);
-        h[e] = *reinterpret_cast<uint32_t*>(&hv);
-      }
-      bw[q] = make_uint4(h[0], h[1], h[2], h[3]);
+    for (int e = 0; e < RS / 2; ++e) {
+      const uint32_t w = e < 2 ? w0[k] : w1[k];
+      const int b0 = (2 * e) & 3;
+      const float m0 = __fsub_rn(__uint_as_float(__byte_perm(w, 0x4B000000u, 0x7640 + b0)), 8388608.0f);
+      const float m1 = __fsub_rn(__uint_as_float(__byte_perm(w, 0x4B000000u, 0x7640 + b0 + 1)), 8388608.0f);
+      const float f0 = __fmul_rn(__fmaf_rn((float)K, m0, off), sc);
+      const float f1 = __fmul_rn(__fmaf_rn((float)K, m1, off), sc);
+      __half2 hv = __floats2half2_rn(f0, f1);
+      h[e] = *reinterpret_cast<uint32_t*>(&hv);
+    }
+    if (p < D) {
+      if (RS == 8)
+        reinterpret_cast<uint4*>(a.bh + (size_t)p * K)[i] = make_uint4(h[0], h[1], h[2], h[3]);
+      else
+        reinterpret_cast<uint2*>(a.bh + (size_t)p * K)[i] = make_uint2(h[0], h[1]);
     }
   }
 }

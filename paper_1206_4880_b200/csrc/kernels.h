@@ -28,6 +28,9 @@ struct FdArgs {
   const uint32_t* rank_of_combo;  // optional [C]: write rank_of_combo[combo] to `rank`
   uint32_t* rank;                 // [n] (with rank_of_combo; replaces combo)
   uint32_t* iota;                 // [n] optional: iota[b] = b (sort payload)
+  uint32_t* rank_hist;            // optional [n_rank]: global histogram of `rank` (atomics)
+  uint32_t* rank_minid;           // with rank_hist [n_rank]: smallest block index per rank
+  int n_rank;
 };
 // Builds host-side tables for block side `side` into `quot` (J*256), returns
 // J and the coarsest scale and the ln-table length required.
@@ -37,9 +40,8 @@ void launch_fd(const FdArgs& a, cudaStream_t s);
 // ---- K3: FD index + slabs (avltree.py:150-189, codec.py:343-375) ------------
 struct SlabArgs {
   const double* keys;      // sorted domain FDs (pool order); nullptr = rank form below
-  // rank form (compact FD sort): key of pool position p = fd_of_rank[rk[p]],
-  // rank_start[r] = first pool position with rank >= r (r <= n_rank)
-  const uint32_t* rk;
+  // rank form (compact FD sort): rank_start[r] = first pool position with
+  // rank >= r (r <= n_rank), key of pool position p = fd_of_rank[rank of p]
   const double* fd_of_rank;
   const uint32_t* rank_start;
   int n_rank;
@@ -58,6 +60,13 @@ struct SlabArgs {
 };
 void launch_slabs(const SlabArgs& a, cudaStream_t s);
 void launch_rank_start(const uint32_t* rks, int64_t D, int n_rank, uint32_t* start,
+                       cudaStream_t s);
+// Counting sort by rank (ranks < n_rank <= kCountSortMaxRanks): hist and
+// minid (from launch_fd) -> start/cursor, scatter.  Each bucket starts with
+// its smallest index, the rest of a bucket is in unspecified order.
+constexpr int kCountSortMaxRanks = 8192;
+void launch_count_sort(const uint32_t* rank, int64_t D, int n_rank, const uint32_t* hist,
+                       const uint32_t* minid, uint32_t* start, uint32_t* cursor, uint32_t* order,
                        cudaStream_t s);
 
 // ---- K1: pool builder (blocks.py:75-82, codec.py:136-145) -------------------

@@ -120,6 +120,38 @@ def test_plan_tiled_fd_equals_direct_at_cfg3(monkeypatch):
         assert np.array_equal(a[k], b[k]), k
 
 
+@pytest.mark.parametrize("delta", [1e-4, 0.02])
+def test_encode_count_sorted_pools_match_oracle(delta):
+    """encode() orders equal-FD domains by a counting sort (unspecified order
+    inside a run of equal FDs, smallest raster index first).  With a tiny
+    delta most windows are empty and take the nearest-FD fallback, which
+    reads exactly that first element (codec.py:267-287)."""
+    rng = np.random.default_rng(11)
+    img = np.ascontiguousarray(synth.to_u8(synth.fbm(128, 0.35, rng)))
+    kw = dict(range_size=8, domain_size=16, stride=2, isometries=True, delta=delta)
+    code, st = codec.encode(img, "dynamic_fd", **kw)
+    ref = orc.encode(img, "dynamic_fd", **kw)
+    assert np.array_equal(code.records, ref.records)
+    assert np.array_equal(st.post_rms, ref.post_rms) and np.array_equal(st.pre_rms, ref.pre_rms)
+    assert np.array_equal(st.pool_sizes, ref.pool_sizes)
+
+
+def test_encode_count_sort_equals_stable_sort_at_cfg3(monkeypatch):
+    """Full size: the counting-sorted pool order and the stable (reference)
+    order give identical encodes, also with mostly empty windows."""
+    import torch
+    img = torch.from_numpy(synth.CONFIGS["cfg3"].make()).cuda()
+    for delta in (0.05, 1e-5):
+        kw = dict(range_size=8, domain_size=16, stride=1, isometries=True, delta=delta)
+        a = codec.encode_device(img, "dynamic_fd", **kw)
+        monkeypatch.setenv("FIC_FD_STABLE", "1")
+        b = codec.encode_device(img, "dynamic_fd", **kw)
+        monkeypatch.delenv("FIC_FD_STABLE")
+        assert torch.equal(a.records, b.records), delta
+        assert torch.equal(a.post_rms, b.post_rms) and torch.equal(a.pre_rms, b.pre_rms), delta
+        assert torch.equal(a.pool_sizes, b.pool_sizes), delta
+
+
 def test_dbc_grid_known_answers():
     for side in (8, 16, 32):
         assert np.array_equal(codec.dbc_grid(FD[f"rand{side}.blocks"]), FD[f"rand{side}.fd"])
