@@ -239,6 +239,8 @@ __global__ void k_bits_to_double(const unsigned long long* k, double* o, int64_t
   if (i < n) o[i] = __longlong_as_double((long long)k[i]);
 }
 
+constexpr int kMaxRangeBins = 2 * (kCountSortMaxRanks + 1);
+
 struct ClassifyArgs {
   const int32_t* lo;
   const int32_t* hi;
@@ -250,6 +252,12 @@ struct ClassifyArgs {
   uint32_t* rid;
   int64_t* pool_out;           // may be null
   unsigned long long* pool_sum;
+  // optional counting-sort bins (rank form of the FD order): bin = class *
+  // (n_rank + 1) + rank of lo, with the histogram of the bins
+  const uint32_t* rank_start;
+  int n_rank;
+  uint32_t* bin;
+  uint32_t* bin_hist;
 };
 
 __global__ void k_classify(ClassifyArgs a) {
@@ -261,6 +269,17 @@ __global__ void k_classify(ClassifyArgs a) {
     unsigned long long cls = (a.tensor_ok && (int64_t)pool >= a.small_pool) ? 0ull : 1ull;
     a.key[r] = (cls << 63) | ((unsigned long long)(uint32_t)lo << 32) | (uint32_t)hi;
     a.rid[r] = r;
+    if (a.bin) {
+      // rank of pool position lo: the last q with rank_start[q] <= lo
+      int q0 = 0, q1 = a.n_rank + 1;
+      while (q0 < q1) {
+        const int m = (q0 + q1) >> 1;
+        if (a.rank_start[m] <= (uint32_t)lo) q0 = m + 1; else q1 = m;
+      }
+      const uint32_t b = (uint32_t)cls * (uint32_t)(a.n_rank + 1) + (uint32_t)(q0 - 1);
+      a.bin[r] = b;
+      atomicAdd(a.bin_hist + b, 1u);
+    }
     if (a.pool_out) a.pool_out[r] = (int64_t)pool;
   }
   for (int m = 16; m >= 1; m >>= 1) pool += __shfl_xor_sync(0xffffffffu, pool, m);
@@ -303,6 +322,73 @@ __global__ void k_shard(const unsigned long long* key, const unsigned long long*
   } else {
     out->shard_begin = first_with_shard_ge(shard);
     out->shard_end = first_with_shard_ge(shard + 1);
+  }
+}
+
+// Counting sort of the ranges by bin (class, rank of lo): the same grouping
+// as the (class, lo) radix sort -- lo is a pure function of the rank -- in
+// one scan block and one scatter pass.  Order inside a bin is unspecified;
+// it only shapes the tiles, never the result.
+__global__ void __launch_bounds__(1024) k_bin_scan(const uint32_t* hist, int nb, uint32_t* cursor,
+                                                   int class1_bin, int R, PlanCounts* pc) {
+  using Scan = cub::BlockScan<uint32_t, 1024>;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ uint32_t s_carry;
+  constexpr int IPT = 8;
+  uint32_t carry = 0;
+  for (int base = 0; base < nb; base += 1024 * IPT) {
+    uint32_t v[IPT];
+#pragma unroll
+    for (int i = 0; i < IPT; ++i) {
+      const int b = base + threadIdx.x * IPT + i;
+      v[i] = b < nb ? hist[b] : 0u;
+    }
+    uint32_t total = 0;
+    Scan(tmp).ExclusiveSum(v, v, total);
+#pragma unroll
+    for (int i = 0; i < IPT; ++i) {
+      const int b = base + threadIdx.x * IPT + i;
+      if (b < nb) cursor[b] = carry + v[i];
+      if (b == class1_bin) s_carry = carry + v[i];
+    }
+    carry += total;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {  // single shard: the whole sorted list, tensor class first
+    pc->shard_begin = 0;
+    pc->shard_end = R;
+    pc->n_tensor = class1_bin < nb ? (int64_t)s_carry : R;
+    pc->pool_sum = 0;
+  }
+}
+
+__global__ void __launch_bounds__(1024) k_range_scatter(const uint32_t* bin, const unsigned long long* key,
+                                                        int R, int nb, uint32_t* cursor,
+                                                        unsigned long long* key_s, uint32_t* rid_s) {
+  extern __shared__ uint32_t cnt[];  // [nb]
+  constexpr int IPT = 4;
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) cnt[b] = 0;
+  __syncthreads();
+  const int r0 = blockIdx.x * blockDim.x * IPT;
+  uint32_t bb[IPT], loc[IPT];
+#pragma unroll
+  for (int i = 0; i < IPT; ++i) {
+    const int r = r0 + i * blockDim.x + threadIdx.x;
+    bb[i] = r < R ? bin[r] : 0u;
+    if (r < R) loc[i] = atomicAdd(cnt + bb[i], 1u);
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < nb; b += blockDim.x)
+    if (cnt[b]) cnt[b] = atomicAdd(cursor + b, cnt[b]);
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < IPT; ++i) {
+    const int r = r0 + i * blockDim.x + threadIdx.x;
+    if (r < R) {
+      const uint32_t pos = cnt[bb[i]] + loc[i];
+      key_s[pos] = key[r];
+      rid_s[pos] = (uint32_t)r;
+    }
   }
 }
 
@@ -358,6 +444,49 @@ __global__ void k_exact_segs(const unsigned long long* key, const uint32_t* rid,
 struct Totals {
   int64_t n_titems, n_eitems, n_slots;
 };
+
+// Exclusive scans of the per-tile and per-exact-range segment counts and of
+// the per-range slot counts (int64), plus their totals, in one block.
+template <class T, class U>
+__device__ void block_exclusive_scan(const T* in, U* out, int64_t n, U* total) {
+  using Scan = cub::BlockScan<U, 1024>;
+  __shared__ typename Scan::TempStorage tmp;
+  U carry = 0;
+  for (int64_t base = 0; base < n; base += 1024 * 4) {
+    U v[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int64_t k = base + threadIdx.x * 4 + i;
+      v[i] = k < n ? (U)in[k] : (U)0;
+    }
+    U t = 0;
+    Scan(tmp).ExclusiveSum(v, v, t);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int64_t k = base + threadIdx.x * 4 + i;
+      if (k < n) out[k] = carry + v[i];
+    }
+    carry += t;
+    __syncthreads();
+  }
+  *total = carry;
+}
+
+__global__ void __launch_bounds__(1024) k_plan_scans(const int32_t* tnseg, int32_t* tbase, int64_t ntt,
+                                                     const int32_t* enseg, int32_t* ebase, int64_t ner,
+                                                     const int32_t* nslots, int64_t* sbase, int R,
+                                                     Totals* out) {
+  int32_t t1 = 0, t2 = 0;
+  int64_t t3 = 0;
+  block_exclusive_scan<int32_t, int32_t>(tnseg, tbase, ntt, &t1);
+  block_exclusive_scan<int32_t, int32_t>(enseg, ebase, ner, &t2);
+  block_exclusive_scan<int32_t, int64_t>(nslots, sbase, R, &t3);
+  if (threadIdx.x == 0) {
+    out->n_titems = t1;
+    out->n_eitems = t2;
+    out->n_slots = t3;
+  }
+}
 
 __global__ void k_totals(const int32_t* tnseg, const int32_t* tbase, int64_t ntt,
                          const int32_t* enseg, const int32_t* ebase, int64_t ner,
@@ -492,6 +621,8 @@ static void cub_call(Scratch& sc, F f) {
 // pool planning shared by encode and plan
 // ---------------------------------------------------------------------------
 struct PlanBufs {
+  const uint32_t* rank_start = nullptr;  // [n_rank + 1] rank form of the FD order (else null)
+  int n_rank = 0;
   double* fd_dom = nullptr;      // [D] (dynamic/static2)
   double* fd_rng = nullptr;      // [R]
   double* keys = nullptr;        // [D] sorted FDs
@@ -635,6 +766,8 @@ static PlanBufs make_plan(Scratch& sc, cudaStream_t s, const uint8_t* img, const
         launch_rank_start(rks, g.D, rt.n_rank, rstart, s);
       }
       sa.keys = nullptr;
+      pb.rank_start = rstart;
+      pb.n_rank = rt.n_rank;
       sa.fd_of_rank = rt.fd_of_rank;
       sa.rank_start = rstart;
       sa.n_rank = rt.n_rank;
@@ -770,23 +903,54 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
   uint32_t* rid_s = sc.get<uint32_t>(g.R);
   ClassifyArgs ca{pb.lo, pb.hi, g.R, g.n_iso, small_pool, tensor_ok ? 1 : 0, key, rid,
                   pool_sizes, counters + 2};
+  // counting sort by (class, rank of lo) when the FD order is in rank form
+  const int nb = pb.rank_start ? 2 * (pb.n_rank + 1) : 0;
+  // (the shard partition is a cut of this order: every rank must compute the
+  // same one, so shards keep the deterministic stable radix sort)
+  const bool bin_sort = pb.rank_start && nb <= kMaxRangeBins && nshard == 1 && !getenv("FIC_RANGE_RADIX");
+  uint32_t* bin_hist = nullptr;
+  if (bin_sort) {
+    ca.rank_start = pb.rank_start;
+    ca.n_rank = pb.n_rank;
+    ca.bin = sc.get<uint32_t>(g.R);
+    bin_hist = sc.get<uint32_t>(nb);
+    FIC_CUDA(cudaMemsetAsync(bin_hist, 0, nb * sizeof(uint32_t), s));
+    ca.bin_hist = bin_hist;
+  }
   k_classify<<<(unsigned)cdiv(g.R, 256), 256, 0, s>>>(ca);
   FIC_CHECK_LAUNCH();
-  // order by (class, lo) only (bits 32..63; stable, so ties keep raster order):
-  // tiles need contiguous windows, and the result does not depend on the order
-  cub_call(sc, [&](void* t, size_t& b) {
-    return cub::DeviceRadixSort::SortPairs(t, b, key, key_s, rid, rid_s, g.R, 32, 64, s);
-  });
-  unsigned long long* cost = sc.get<unsigned long long>(g.R);
-  unsigned long long* cum = sc.get<unsigned long long>(g.R);
-  k_cost<<<(unsigned)cdiv(g.R, 256), 256, 0, s>>>(key_s, g.R, g.n_iso, cost);
-  FIC_CHECK_LAUNCH();
-  cub_call(sc, [&](void* t, size_t& b) {
-    return cub::DeviceScan::InclusiveSum(t, b, cost, cum, g.R, s);
-  });
   PlanCounts* d_pc = sc.get<PlanCounts>(1);
-  k_shard<<<1, 32, 0, s>>>(key_s, cum, g.R, shard, nshard, d_pc);
-  FIC_CHECK_LAUNCH();
+  if (bin_sort) {
+    uint32_t* cursor = sc.get<uint32_t>(nb);
+    k_bin_scan<<<1, 1024, 0, s>>>(bin_hist, nb, cursor, pb.n_rank + 1, g.R, d_pc);
+    FIC_CHECK_LAUNCH();
+    static bool attr = false;
+    if (!attr) {
+      FIC_CUDA(cudaFuncSetAttribute(k_range_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    kMaxRangeBins * (int)sizeof(uint32_t)));
+      attr = true;
+    }
+    k_range_scatter<<<(unsigned)cdiv(g.R, 4096), 1024, nb * sizeof(uint32_t), s>>>(
+        ca.bin, key, g.R, nb, cursor, key_s, rid_s);
+    FIC_CHECK_LAUNCH();
+  } else {
+    // order by (class, lo) only (bits 32..63; stable, so ties keep raster order):
+    // tiles need contiguous windows, and the result does not depend on the order
+    cub_call(sc, [&](void* t, size_t& b) {
+      return cub::DeviceRadixSort::SortPairs(t, b, key, key_s, rid, rid_s, g.R, 32, 64, s);
+    });
+  }
+  if (!bin_sort) {
+    unsigned long long* cost = sc.get<unsigned long long>(g.R);
+    unsigned long long* cum = sc.get<unsigned long long>(g.R);
+    k_cost<<<(unsigned)cdiv(g.R, 256), 256, 0, s>>>(key_s, g.R, g.n_iso, cost);
+    FIC_CHECK_LAUNCH();
+    cub_call(sc, [&](void* t, size_t& b) {
+      return cub::DeviceScan::InclusiveSum(t, b, cost, cum, g.R, s);
+    });
+    k_shard<<<1, 32, 0, s>>>(key_s, cum, g.R, shard, nshard, d_pc);
+    FIC_CHECK_LAUNCH();
+  }
   PlanCounts pc;
   pmark();  // 10
   FIC_CUDA(cudaMemcpyAsync(&pc, d_pc, sizeof(pc), cudaMemcpyDeviceToHost, s));
@@ -812,29 +976,14 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
     TileArgs ta{key_s, rid_s, tb, te, RT, seg_t, seg0, wlo, whi, tnseg, nslots, g.n_iso, counters + 3};
     k_tiles<<<(unsigned)cdiv(n_tt, 128), 128, 0, s>>>(ta);
     FIC_CHECK_LAUNCH();
-    cub_call(sc, [&](void* t, size_t& b) {
-      return cub::DeviceScan::ExclusiveSum(t, b, tnseg, tbase, (int)n_tt, s);
-    });
   }
   if (n_er) {
     k_exact_segs<<<(unsigned)cdiv(n_er, 256), 256, 0, s>>>(key_s, rid_s, eb, ee, seg_e, enseg,
                                                             nslots);
     FIC_CHECK_LAUNCH();
-    cub_call(sc, [&](void* t, size_t& b) {
-      return cub::DeviceScan::ExclusiveSum(t, b, enseg, ebase, (int)n_er, s);
-    });
-  }
-  {
-    // slot bases over raster ranges (int64 accumulation)
-    int64_t* ns64 = sc.get<int64_t>(g.R);
-    k_i32_to_i64<<<(unsigned)cdiv(g.R, 256), 256, 0, s>>>(nslots, ns64, g.R);
-    FIC_CHECK_LAUNCH();
-    cub_call(sc, [&](void* t, size_t& b) {
-      return cub::DeviceScan::ExclusiveSum(t, b, ns64, sbase, g.R, s);
-    });
   }
   Totals* d_tot = sc.get<Totals>(1);
-  k_totals<<<1, 32, 0, s>>>(tnseg, tbase, n_tt, enseg, ebase, n_er, nslots, sbase, g.R, d_tot);
+  k_plan_scans<<<1, 1024, 0, s>>>(tnseg, tbase, n_tt, enseg, ebase, n_er, nslots, sbase, g.R, d_tot);
   FIC_CHECK_LAUNCH();
   Totals tot;
   pmark();  // 12

@@ -137,16 +137,19 @@ def test_encode_count_sorted_pools_match_oracle(delta):
 
 
 def test_encode_count_sort_equals_stable_sort_at_cfg3(monkeypatch):
-    """Full size: the counting-sorted pool order and the stable (reference)
-    order give identical encodes, also with mostly empty windows."""
+    """Full size: the counting-sorted pool and range orders and the stable
+    radix-sorted ones (the reference's FD order) give identical encodes, also
+    with mostly empty windows."""
     import torch
     img = torch.from_numpy(synth.CONFIGS["cfg3"].make()).cuda()
     for delta in (0.05, 1e-5):
         kw = dict(range_size=8, domain_size=16, stride=1, isometries=True, delta=delta)
         a = codec.encode_device(img, "dynamic_fd", **kw)
         monkeypatch.setenv("FIC_FD_STABLE", "1")
+        monkeypatch.setenv("FIC_RANGE_RADIX", "1")
         b = codec.encode_device(img, "dynamic_fd", **kw)
         monkeypatch.delenv("FIC_FD_STABLE")
+        monkeypatch.delenv("FIC_RANGE_RADIX")
         assert torch.equal(a.records, b.records), delta
         assert torch.equal(a.post_rms, b.post_rms) and torch.equal(a.pre_rms, b.pre_rms), delta
         assert torch.equal(a.pool_sizes, b.pool_sizes), delta
