@@ -254,7 +254,7 @@ struct ClassifyArgs {
   unsigned long long* pool_sum;
   // optional counting-sort bins (rank form of the FD order): bin = class *
   // (n_rank + 1) + rank of lo, with the histogram of the bins
-  const uint32_t* rank_start;
+  const uint32_t* lo_rank;      // [R] rank index of lo (from k_slabs)
   int n_rank;
   uint32_t* bin;
   uint32_t* bin_hist;
@@ -269,21 +269,22 @@ __global__ void k_classify(ClassifyArgs a) {
     unsigned long long cls = (a.tensor_ok && (int64_t)pool >= a.small_pool) ? 0ull : 1ull;
     a.key[r] = (cls << 63) | ((unsigned long long)(uint32_t)lo << 32) | (uint32_t)hi;
     a.rid[r] = r;
-    if (a.bin) {
-      // rank of pool position lo: the last q with rank_start[q] <= lo
-      int q0 = 0, q1 = a.n_rank + 1;
-      while (q0 < q1) {
-        const int m = (q0 + q1) >> 1;
-        if (a.rank_start[m] <= (uint32_t)lo) q0 = m + 1; else q1 = m;
-      }
-      const uint32_t b = (uint32_t)cls * (uint32_t)(a.n_rank + 1) + (uint32_t)(q0 - 1);
+    if (a.bin) {  // lo_rank orders like lo (rank_start is monotone)
+      const uint32_t b = (uint32_t)cls * (uint32_t)(a.n_rank + 1) + a.lo_rank[r];
       a.bin[r] = b;
       atomicAdd(a.bin_hist + b, 1u);
     }
     if (a.pool_out) a.pool_out[r] = (int64_t)pool;
   }
   for (int m = 16; m >= 1; m >>= 1) pool += __shfl_xor_sync(0xffffffffu, pool, m);
-  if ((threadIdx.x & 31) == 0 && pool) atomicAdd(a.pool_sum, pool);
+  __shared__ unsigned long long wsum[32];
+  if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = pool;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += wsum[w];
+    if (t) atomicAdd(a.pool_sum, t);
+  }
 }
 
 __global__ void k_cost(const unsigned long long* key, int R, int n_iso, unsigned long long* cost) {
@@ -476,15 +477,19 @@ __global__ void __launch_bounds__(1024) k_plan_scans(const int32_t* tnseg, int32
                                                      const int32_t* enseg, int32_t* ebase, int64_t ner,
                                                      const int32_t* nslots, int64_t* sbase, int R,
                                                      Totals* out) {
-  int32_t t1 = 0, t2 = 0;
-  int64_t t3 = 0;
-  block_exclusive_scan<int32_t, int32_t>(tnseg, tbase, ntt, &t1);
-  block_exclusive_scan<int32_t, int32_t>(enseg, ebase, ner, &t2);
-  block_exclusive_scan<int32_t, int64_t>(nslots, sbase, R, &t3);
-  if (threadIdx.x == 0) {
-    out->n_titems = t1;
-    out->n_eitems = t2;
-    out->n_slots = t3;
+  // three independent scans, one block each
+  if (blockIdx.x == 0) {
+    int32_t t = 0;
+    block_exclusive_scan<int32_t, int32_t>(tnseg, tbase, ntt, &t);
+    if (threadIdx.x == 0) out->n_titems = t;
+  } else if (blockIdx.x == 1) {
+    int32_t t = 0;
+    block_exclusive_scan<int32_t, int32_t>(enseg, ebase, ner, &t);
+    if (threadIdx.x == 0) out->n_eitems = t;
+  } else {
+    int64_t t = 0;
+    block_exclusive_scan<int32_t, int64_t>(nslots, sbase, R, &t);
+    if (threadIdx.x == 0) out->n_slots = t;
   }
 }
 
@@ -623,6 +628,7 @@ static void cub_call(Scratch& sc, F f) {
 struct PlanBufs {
   const uint32_t* rank_start = nullptr;  // [n_rank + 1] rank form of the FD order (else null)
   int n_rank = 0;
+  const uint32_t* lo_rank = nullptr;     // [R] rank index of each slab start (dynamic_fd, rank form)
   double* fd_dom = nullptr;      // [D] (dynamic/static2)
   double* fd_rng = nullptr;      // [R]
   double* keys = nullptr;        // [D] sorted FDs
@@ -753,7 +759,10 @@ static PlanBufs make_plan(Scratch& sc, cudaStream_t s, const uint8_t* img, const
       uint32_t* rstart = sc.get<uint32_t>(rt.n_rank + 1);
       if (count_sort) {
         uint32_t* cursor = sc.get<uint32_t>(rt.n_rank);
-        launch_count_sort(rk, g.D, rt.n_rank, hist, hist + rt.n_rank, rstart, cursor, pb.order, s);
+        ScalArgs scl{rt.fd_of_rank, p.strategy, p.has_delta, p.delta, pb.scal};
+        launch_count_sort(rk, g.D, rt.n_rank, hist, hist + rt.n_rank, rstart, cursor, pb.order, scl,
+                          s);
+        sa.scal_ready = 1;
       } else {
         // stable sort of the domains by rank (same order as by FD value)
         uint32_t* rks = sc.get<uint32_t>(g.D);
@@ -768,6 +777,11 @@ static PlanBufs make_plan(Scratch& sc, cudaStream_t s, const uint8_t* img, const
       sa.keys = nullptr;
       pb.rank_start = rstart;
       pb.n_rank = rt.n_rank;
+      if (p.strategy == FIC_DYNAMIC_FD) {
+        uint32_t* lr = sc.get<uint32_t>(g.R);
+        sa.lo_rank = lr;
+        pb.lo_rank = lr;
+      }
       sa.fd_of_rank = rt.fd_of_rank;
       sa.rank_start = rstart;
       sa.n_rank = rt.n_rank;
@@ -907,10 +921,10 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
   const int nb = pb.rank_start ? 2 * (pb.n_rank + 1) : 0;
   // (the shard partition is a cut of this order: every rank must compute the
   // same one, so shards keep the deterministic stable radix sort)
-  const bool bin_sort = pb.rank_start && nb <= kMaxRangeBins && nshard == 1 && !getenv("FIC_RANGE_RADIX");
+  const bool bin_sort = pb.lo_rank && nb <= kMaxRangeBins && nshard == 1 && !getenv("FIC_RANGE_RADIX");
   uint32_t* bin_hist = nullptr;
   if (bin_sort) {
-    ca.rank_start = pb.rank_start;
+    ca.lo_rank = pb.lo_rank;
     ca.n_rank = pb.n_rank;
     ca.bin = sc.get<uint32_t>(g.R);
     bin_hist = sc.get<uint32_t>(nb);
@@ -983,7 +997,7 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
     FIC_CHECK_LAUNCH();
   }
   Totals* d_tot = sc.get<Totals>(1);
-  k_plan_scans<<<1, 1024, 0, s>>>(tnseg, tbase, n_tt, enseg, ebase, n_er, nslots, sbase, g.R, d_tot);
+  k_plan_scans<<<3, 1024, 0, s>>>(tnseg, tbase, n_tt, enseg, ebase, n_er, nslots, sbase, g.R, d_tot);
   FIC_CHECK_LAUNCH();
   Totals tot;
   pmark();  // 12

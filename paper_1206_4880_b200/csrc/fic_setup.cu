@@ -1,6 +1,7 @@
 // Setup kernels of the encoder hot path: FD (K2), slabs (K3), pool builder
 // (K1), range preparation.  sm_100a.  See DESIGN.md §Kernels.
 #include <cuda_fp16.h>
+#include <cub/block/block_reduce.cuh>
 #include <cub/block/block_scan.cuh>
 #include <math.h>
 
@@ -408,7 +409,7 @@ struct Keys {
   __device__ __forceinline__ double at(int64_t p) const {
     if (a.keys) return a.keys[p];
     // rank of position p: the last r with rank_start[r] <= p
-    return __ldg(a.fd_of_rank + (upper_bound_u32(a.rank_start, a.n_rank + 1, (uint32_t)p) - 1));
+    return a.fd_of_rank[upper_bound_u32(a.rank_start, a.n_rank + 1, (uint32_t)p) - 1];  // may be shared memory
   }
   __device__ __forceinline__ int64_t lower(double v) const {
     if (a.keys) return lower_bound(a.keys, a.D, v);
@@ -474,16 +475,36 @@ void launch_rank_start(const uint32_t* rks, int64_t D, int n_rank, uint32_t* sta
 // so the encode result does not depend on it -- except the nearest-FD
 // fallback (codec.py:267-287), which takes a run's first element, the
 // smallest raster index in the stable order: that one is placed first.
+// The block also derives the slab scalars (k_slab_scalars) from the counts:
+// f_min / f_max are the values of the first / last occupied rank
+// (fdim.py:93-100), the static2 boundary is the bucket start of the first
+// rank whose value is >= the midpoint.
 __global__ void __launch_bounds__(1024) k_rank_scan(const uint32_t* hist, int n_rank, int64_t D,
-                                                    uint32_t* start, uint32_t* cursor) {
+                                                    uint32_t* start, uint32_t* cursor, ScalArgs sa) {
   using Scan = cub::BlockScan<uint32_t, 1024>;
+  using Red = cub::BlockReduce<int, 1024>;
   __shared__ typename Scan::TempStorage tmp;
+  __shared__ typename Red::TempStorage rtmp;
+  __shared__ int s_first, s_last, s_lb;
+  __shared__ double s_mid;
   constexpr int IPT = kCountSortMaxRanks / 1024;
   uint32_t v[IPT];
+  int first = n_rank, last = -1;
 #pragma unroll
   for (int i = 0; i < IPT; ++i) {
     const int r = threadIdx.x * IPT + i;
     v[i] = r < n_rank ? hist[r] : 0u;
+    if (v[i]) {
+      first = min(first, r);
+      last = max(last, r);
+    }
+  }
+  first = Red(rtmp).Reduce(first, cuda::minimum<>{});
+  __syncthreads();
+  last = Red(rtmp).Reduce(last, cuda::maximum<>{});
+  if (threadIdx.x == 0) {
+    s_first = first;
+    s_last = last;
   }
   Scan(tmp).ExclusiveSum(v, v);
 #pragma unroll
@@ -495,6 +516,34 @@ __global__ void __launch_bounds__(1024) k_rank_scan(const uint32_t* hist, int n_
     }
   }
   if (threadIdx.x == 0) start[n_rank] = (uint32_t)D;
+  if (!sa.scal) return;
+  __syncthreads();
+  const double fmn = sa.fd_of_rank[s_first], fmx = sa.fd_of_rank[s_last];
+  if (sa.strategy == FIC_STATIC2) {
+    const double mid = __ddiv_rn(__dadd_rn(fmn, fmx), 2.0);
+    int below = 0;  // ranks with a value < mid (values increase with the rank)
+    for (int r = threadIdx.x; r < n_rank; r += blockDim.x) below += sa.fd_of_rank[r] < mid ? 1 : 0;
+    below = Red(rtmp).Reduce(below, cuda::std::plus<>{});
+    if (threadIdx.x == 0) {
+      s_lb = below;
+      s_mid = mid;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < IPT; ++i)
+      if (threadIdx.x * IPT + i == s_lb && s_lb < n_rank) sa.scal[3] = (double)v[i];
+    if (threadIdx.x == 0) {
+      if (s_lb >= n_rank) sa.scal[3] = (double)D;
+      sa.scal[0] = fmn;
+      sa.scal[1] = fmx;
+      sa.scal[2] = s_mid;
+    }
+  } else if (threadIdx.x == 0) {
+    sa.scal[0] = fmn;
+    sa.scal[1] = fmx;
+    sa.scal[2] = sa.has_delta ? sa.delta : __ddiv_rn(__dsub_rn(fmx, fmn), 3.0);
+    sa.scal[3] = 0.0;
+  }
 }
 
 __global__ void __launch_bounds__(1024) k_rank_scatter(const uint32_t* rank, int64_t D, int n_rank,
@@ -531,8 +580,8 @@ __global__ void __launch_bounds__(1024) k_rank_scatter(const uint32_t* rank, int
 
 void launch_count_sort(const uint32_t* rank, int64_t D, int n_rank, const uint32_t* hist,
                        const uint32_t* minid, uint32_t* start, uint32_t* cursor, uint32_t* order,
-                       cudaStream_t s) {
-  k_rank_scan<<<1, 1024, 0, s>>>(hist, n_rank, D, start, cursor);
+                       const ScalArgs& sa, cudaStream_t s) {
+  k_rank_scan<<<1, 1024, 0, s>>>(hist, n_rank, D, start, cursor, sa);
   FIC_CHECK_LAUNCH();
   static bool attr = false;
   if (!attr) {
@@ -561,6 +610,13 @@ __device__ int64_t nosearch_axis(int extent, int top, int rs, int ds, int st) {
 }
 
 __global__ void k_slabs(SlabArgs a) {
+  if (a.fd_of_rank && !a.keys) {  // rank form: the (few) distinct values in shared memory
+    extern __shared__ double fdr[];
+#pragma unroll 8
+    for (int i = threadIdx.x; i < a.n_rank; i += blockDim.x) fdr[i] = __ldg(a.fd_of_rank + i);
+    __syncthreads();
+    a.fd_of_rank = fdr;
+  }
   int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= a.R) return;
   int64_t lo, hi;
@@ -583,12 +639,20 @@ __global__ void k_slabs(SlabArgs a) {
     } else {
       double half = a.scal[2];
       Keys k{a};
-      lo = k.lower(__dsub_rn(f, half));
+      if (a.lo_rank) {  // rank form: keep the rank index of lo for the range sort
+        const int64_t q = lower_bound(a.fd_of_rank, a.n_rank, __dsub_rn(f, half));
+        lo = __ldg(a.rank_start + q);
+        a.lo_rank[r] = (uint32_t)q;
+      } else {
+        lo = k.lower(__dsub_rn(f, half));
+      }
       hi = k.upper(__dadd_rn(f, half));
     }
     if (hi <= lo) {
       lo = nearest_fd(Keys{a}, a.ids, a.D, f);
       hi = lo + 1;
+      if (a.lo_rank)  // the last rank whose bucket starts at or before lo
+        a.lo_rank[r] = (uint32_t)(upper_bound_u32(a.rank_start, a.n_rank + 1, (uint32_t)lo) - 1);
     }
   }
   a.lo[r] = (int32_t)lo;
@@ -596,11 +660,19 @@ __global__ void k_slabs(SlabArgs a) {
 }
 
 void launch_slabs(const SlabArgs& a, cudaStream_t s) {
-  if (a.strategy == FIC_STATIC2 || a.strategy == FIC_DYNAMIC_FD) {
+  if ((a.strategy == FIC_STATIC2 || a.strategy == FIC_DYNAMIC_FD) && !a.scal_ready) {
     k_slab_scalars<<<1, 32, 0, s>>>(a);
     FIC_CHECK_LAUNCH();
   }
-  k_slabs<<<(unsigned)cdiv(a.R, 256), 256, 0, s>>>(a);
+  const bool rank_form = (a.strategy == FIC_STATIC2 || a.strategy == FIC_DYNAMIC_FD) && !a.keys;
+  const size_t smem = rank_form ? (size_t)a.n_rank * sizeof(double) : 0;
+  static bool attr = false;
+  if (!attr) {
+    FIC_CUDA(cudaFuncSetAttribute(k_slabs, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  kCountSortMaxRanks * (int)sizeof(double)));
+    attr = true;
+  }
+  k_slabs<<<(unsigned)cdiv(a.R, 128), 128, smem, s>>>(a);
   FIC_CHECK_LAUNCH();
 }
 

@@ -53,6 +53,8 @@ struct SlabArgs {
   int has_delta;
   double delta;
   double* scal;            // [4] out: f_min, f_max, half / mid, boundary
+  int scal_ready;          // scal already written (by the counting sort's scan)
+  uint32_t* lo_rank;       // [R] optional (rank form, dynamic_fd): rank index q with lo = rank_start[q]
   int32_t* lo;             // [R] out
   int32_t* hi;             // [R] out
   // geometry for nosearch (codec.py:430-447)
@@ -65,9 +67,15 @@ void launch_rank_start(const uint32_t* rks, int64_t D, int n_rank, uint32_t* sta
 // minid (from launch_fd) -> start/cursor, scatter.  Each bucket starts with
 // its smallest index, the rest of a bucket is in unspecified order.
 constexpr int kCountSortMaxRanks = 8192;
+struct ScalArgs {          // slab scalars computed by the counting sort's scan (optional)
+  const double* fd_of_rank;
+  int strategy, has_delta;
+  double delta;
+  double* scal;            // nullptr = skip
+};
 void launch_count_sort(const uint32_t* rank, int64_t D, int n_rank, const uint32_t* hist,
                        const uint32_t* minid, uint32_t* start, uint32_t* cursor, uint32_t* order,
-                       cudaStream_t s);
+                       const ScalArgs& sa, cudaStream_t s);
 
 // ---- K1: pool builder (blocks.py:75-82, codec.py:136-145) -------------------
 struct PoolArgs {
