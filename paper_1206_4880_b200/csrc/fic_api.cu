@@ -406,6 +406,7 @@ struct TileArgs {
   int32_t* nslots;                // [R]
   int n_iso;
   unsigned long long* useful;     // sum(pool) * n_iso over tensor ranges
+  int nsub;                       // partial slots per segment (tail splitting, TcArgs::nsub)
 };
 
 __global__ void k_tiles(TileArgs a) {
@@ -423,7 +424,7 @@ __global__ void k_tiles(TileArgs a) {
   a.nseg[t] = ns;
   unsigned long long u = 0;
   for (int64_t i = b; i < e; ++i) {
-    a.nslots[a.rid[i]] = ns;
+    a.nslots[a.rid[i]] = ns * a.nsub;
     unsigned long long k = a.key[i];
     u += (uint32_t)k - (uint32_t)((k >> 32) & 0x7fffffffu);
   }
@@ -844,6 +845,8 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
   // a short one seeds thresholds early but measured no faster at cfg3
   const int seg0 = getenv("FIC_SEG0") ? std::max(128, atoi(getenv("FIC_SEG0")) / 128 * 128) : seg_t;
   const int seg_e = 4096;
+  // tail splitting of the tensor work items (TcArgs::nsub); FIC_TC_SPLIT=1 disables
+  const int nsub = getenv("FIC_TC_SPLIT") ? std::max(1, atoi(getenv("FIC_TC_SPLIT"))) : 4;
   const int RT = (tensor_ok ? tc_tile_rows(K) : 128) / g.n_iso;
 
   g_launches = 0;
@@ -987,7 +990,8 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
   int32_t* ebase = sc.get<int32_t>(n_er);
   int64_t* sbase = sc.get<int64_t>(g.R);
   if (n_tt) {
-    TileArgs ta{key_s, rid_s, tb, te, RT, seg_t, seg0, wlo, whi, tnseg, nslots, g.n_iso, counters + 3};
+    TileArgs ta{key_s, rid_s, tb, te, RT, seg_t, seg0, wlo, whi, tnseg, nslots, g.n_iso, counters + 3,
+                nsub};
     k_tiles<<<(unsigned)cdiv(n_tt, 128), 128, 0, s>>>(ta);
     FIC_CHECK_LAUNCH();
   }
@@ -1008,6 +1012,8 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
   int2* titems = sc.get<int2>(tot.n_titems);
   int2* eitems = sc.get<int2>(tot.n_eitems);
   Partial* partials = sc.get<Partial>(tot.n_slots);
+  if (nsub > 1)  // tensor slots of pieces that never run stay invalid
+    FIC_CUDA(cudaMemsetAsync(partials, 0, tot.n_slots * sizeof(Partial), s));
   if (n_tt) {
     // segment-major order: every tile's first segment runs before any second
     // segment, so later segments start from the thresholds the earlier ones found
@@ -1030,13 +1036,36 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
     FIC_CHECK_LAUNCH();
     TcArgs ta{titems, tot.n_titems, rid_s + tb, n_tr, wlo, whi, seg_t, seg0, RT, sbase, partials,
               counters, counters + 15, thr_g, 0, nullptr};
+    ta.nsub = nsub;
+    ta.n_split = nsub > 1 ? std::min<int64_t>(tot.n_titems, 2 * 148) : 0;
     const char* dbg_env = getenv("FIC_TC_DEBUG");
-    if (dbg_env && (atoi(dbg_env) & 32)) {
+    if (dbg_env && (atoi(dbg_env) & (32 | 8192))) {
       ta.dbg = sc.get<unsigned long long>(64 * 24);
       FIC_CUDA(cudaMemsetAsync(ta.dbg, 0, 64 * 24 * 8, s));
     }
     launch_tc(P, Rv, ta, s);
-    if (ta.dbg) {
+    if (ta.dbg && (atoi(dbg_env) & 8192)) {  // per-CTA start / end: the tail of the persistent grid
+      std::vector<unsigned long long> h(64 * 24);
+      FIC_CUDA(cudaMemcpyAsync(h.data(), ta.dbg, h.size() * 8, cudaMemcpyDeviceToHost, s));
+      FIC_CUDA(cudaStreamSynchronize(s));
+      int n = 0;
+      unsigned long long s0 = ~0ull, s1 = 0, e0 = ~0ull, e1 = 0;
+      double em = 0, im = 0;
+      unsigned long long imin = ~0ull, imax = 0;
+      for (int b = 0; b < 512 && h[2 * b + 1]; ++b, ++n) {
+        s0 = std::min(s0, h[2 * b]);
+        s1 = std::max(s1, h[2 * b]);
+        e0 = std::min(e0, h[2 * b + 1]);
+        e1 = std::max(e1, h[2 * b + 1]);
+        em += (double)h[2 * b + 1];
+        im += (double)h[1024 + b];
+        imin = std::min(imin, h[1024 + b]);
+        imax = std::max(imax, h[1024 + b]);
+      }
+      if (n)
+        fprintf(stderr, "tc tail: %d CTAs, start spread %.1f us, end min %.1f mean %.1f max %.1f us after first start; items/CTA %llu..%llu mean %.1f\n",
+                n, (s1 - s0) / 1e3, (e0 - s0) / 1e3, (em / n - (double)s0) / 1e3, (e1 - s0) / 1e3, imin, imax, im / n);
+    } else if (ta.dbg) {
       std::vector<unsigned long long> h(64 * 24);
       FIC_CUDA(cudaMemcpyAsync(h.data(), ta.dbg, h.size() * 8, cudaMemcpyDeviceToHost, s));
       FIC_CUDA(cudaStreamSynchronize(s));

@@ -383,6 +383,8 @@ __global__ void __maxnreg__(MAXREG)
   unsigned long long evals = 0, seed_rounds = 0, hit_rounds = 0, hit_lanes = 0;
   long long tw0 = 0, tw1 = 0, tw2 = 0, tw3 = 0, tw4 = 0;  // stall cycles (debug & 4)
   const long long tstart = TCLK();
+  unsigned long long gt_start = 0;  // debug & 8192: per-CTA start / end (globaltimer, ns)
+  if (DBG && (debug & 8192) && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt_start));
 
   // exact rescoring of pool position p (codec.py:218-258 via eval_candidate)
   auto exact = [&](int64_t p, int erow, double esr, double esrr) -> Cand {
@@ -417,18 +419,40 @@ __global__ void __maxnreg__(MAXREG)
   }
   int npre = 0;        // producer: B tiles of the current item issued during the previous one
   uint32_t kitem = 0;  // items this CTA started
-  for (int64_t it = (CG == 1) ? (int64_t)s_item[0] : (int64_t)(blockIdx.x / CG); it < a.n_items;
+  // virtual items: the last n_split items are each cut into nsub column
+  // pieces (own partial slots), so the grid's last wave is short
+  const int64_t n_whole = a.n_items - a.n_split;
+  const int64_t n_virt = n_whole + a.n_split * a.nsub;
+  auto item_cols = [&](int64_t v, int& tile, int& slot, int64_t& c0, int64_t& c1) {
+    int64_t i = v;
+    int sub = 0;
+    if (v >= n_whole) {
+      i = n_whole + (v - n_whole) / a.nsub;
+      sub = (int)((v - n_whole) % a.nsub);
+    }
+    const int2 item = a.items[i];
+    tile = item.x;
+    slot = item.y * a.nsub + sub;
+    const int64_t wlo = a.wlo[tile], whi = a.whi[tile];
+    // segment 0 is short (a.seg0 columns): run first for every tile
+    // (segment-major order), it seeds the per-range thresholds cheaply
+    c0 = item.y == 0 ? wlo : wlo + a.seg0 + (int64_t)(item.y - 1) * a.seg_len;
+    c1 = min(whi, item.y == 0 ? c0 + a.seg0 : c0 + a.seg_len);
+    if (v >= n_whole) {
+      const int64_t piece = cdiv(cdiv(c1 - c0, (int64_t)a.nsub), (int64_t)BN) * BN;
+      const int64_t p0 = min(c1, c0 + sub * piece);
+      c1 = min(c1, p0 + piece);
+      c0 = p0;
+    }
+  };
+  for (int64_t it = (CG == 1) ? (int64_t)s_item[0] : (int64_t)(blockIdx.x / CG); it < n_virt;
        it = (CG == 1) ? (int64_t)s_item[kitem & 1] : it + gridDim.x / CG) {
     const long long ti0 = TCLK();
     ++nitems;
     if (CG == 1 && threadIdx.x == 0) s_item[(kitem + 1) & 1] = (long long)atomicAdd(a.item_ctr, 1ull);
-    const int2 item = a.items[it];
-    const int tile = item.x;
-    const int64_t wlo = a.wlo[tile], whi = a.whi[tile];
-    // segment 0 is short (a.seg0 columns): run first for every tile
-    // (segment-major order), it seeds the per-range thresholds cheaply
-    const int64_t c0 = item.y == 0 ? wlo : wlo + a.seg0 + (int64_t)(item.y - 1) * a.seg_len;
-    const int64_t c1 = min(whi, item.y == 0 ? c0 + a.seg0 : c0 + a.seg_len);
+    int tile = 0, slot = 0;
+    int64_t c0 = 0, c1 = 0;
+    item_cols(it, tile, slot, c0, c1);
     const int nt = (int)cdiv(c1 - c0, BN);
 
     if (tile != prev_tile) {
@@ -518,11 +542,10 @@ __global__ void __maxnreg__(MAXREG)
       npre = 0;
       if (CG == 1 && !(debug & 16)) {
         const int64_t nit = s_item[(kitem + 1) & 1];
-        if (nit < a.n_items) {
-          const int2 nx = a.items[nit];
-          const int64_t nlo = a.wlo[nx.x], nhi = a.whi[nx.x];
-          const int64_t n0 = nx.y == 0 ? nlo : nlo + a.seg0 + (int64_t)(nx.y - 1) * a.seg_len;
-          const int64_t n1 = min(nhi, nx.y == 0 ? n0 + a.seg0 : n0 + a.seg_len);
+        if (nit < n_virt) {
+          int ntile = 0, nslot = 0;
+          int64_t n0 = 0, n1 = 0;
+          item_cols(nit, ntile, nslot, n0, n1);
           const int nnt = (int)cdiv(n1 - n0, BN);
           const int pre = min(nnt, C::NST / 2);
           for (int j = 0; j < pre; ++j) {
@@ -850,7 +873,7 @@ __global__ void __maxnreg__(MAXREG)
           out.sq = (uint8_t)sq;
           out.oq = (uint8_t)oq;
           out.valid = (dom != 0xffffffffu) ? 1 : 0;
-          a.partials[a.slot_base[a.tlist[g]] + item.y] = out;
+          a.partials[a.slot_base[a.tlist[g]] + slot] = out;
         }
       }
     }
@@ -891,6 +914,13 @@ __global__ void __maxnreg__(MAXREG)
     atomicAdd(a.counters + 6, (unsigned long long)tw2);
   }
   cta_sync<CG>();
+  if (DBG && (debug & 8192) && threadIdx.x == 0) {
+    unsigned long long gt_end;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt_end));
+    a.dbg[2 * blockIdx.x] = gt_start;
+    a.dbg[2 * blockIdx.x + 1] = gt_end;
+    a.dbg[1024 + blockIdx.x] = (unsigned long long)nitems;
+  }
   if (warp == 0) {
     fence_after();
     if constexpr (CG == 1)
@@ -959,7 +989,7 @@ static void launch_tc_k(const PoolView& P, const RangeView& Rv, const TcArgs& a,
   int dev = 0, sms = 148;
   FIC_CUDA(cudaGetDevice(&dev));
   FIC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  const int64_t clusters = std::min<int64_t>(a.n_items, sms / CG);
+  const int64_t clusters = std::min<int64_t>(a.n_items + a.n_split * (a.nsub - 1), sms / CG);
   TcArgs aa = a;
   const char* dbg = getenv("FIC_TC_DEBUG");
   aa.debug = dbg ? atoi(dbg) : 0;

@@ -56,6 +56,8 @@ struct TcArgs {
                                // the items (segments) of a range; any value is a valid bound
   int debug;                   // FIC_TC_DEBUG (timing experiments only; results invalid if != 0)
   unsigned long long* dbg;     // timeline buffer (debug & 32)
+  int64_t n_split;             // the last n_split items run as nsub column pieces each
+  int nsub;                    // partial slots per segment (slot = segment * nsub + piece)
 };
 bool tc_supported(int K);
 int tc_tile_rows(int K);
