@@ -413,6 +413,8 @@ __global__ void __maxnreg__(MAXREG)
   // s_item[k & 1] holds the k-th item of this CTA; the (k+1)-th is fetched
   // when the k-th starts, so the TMA producer can prefetch its first B tiles
   __shared__ long long s_item[2];
+  __shared__ uint32_t s_rid[BM];  // CTA-local range kl -> range id (0xffffffff: none)
+  __shared__ int32_t s_rho[BM];
   if (CG == 1) {
     if (threadIdx.x == 0) s_item[0] = (long long)atomicAdd(a.item_ctr, 1ull);
     __syncthreads();
@@ -455,35 +457,55 @@ __global__ void __maxnreg__(MAXREG)
     item_cols(it, tile, slot, c0, c1);
     const int nt = (int)cdiv(c1 - c0, BN);
 
-    if (tile != prev_tile) {
-      // A operand: row j = (range k = j / n_iso, iso i = j % n_iso), a = rv - rho
-      for (int u = threadIdx.x; u < BM * (K / 8); u += NTHREADS) {
-        int j = u / (K / 8), c = u % (K / 8);
-        int k = (j + rbase) / n_iso, i = (j + rbase) - k * n_iso;
-        int64_t g = (int64_t)tile * a.RT + k;
-        uint32_t h[4] = {0, 0, 0, 0};
-        uint2 raw8 = make_uint2(0, 0);
-        if (k < a.RT && g < a.n_tr) {
-          uint32_t r = a.tlist[g];
-          int rho = Rv.info[r].rho;
-          const uint8_t* src = Rv.rows + ((int64_t)r * n_iso + i) * K + c * 8;
-          raw8 = *reinterpret_cast<const uint2*>(src);
+    // item setup, two dependent rounds of global loads: (1) the tile's
+    // range ids and rho (CTA-local range kl = row / n_iso), (2) everything
+    // indexed by them (range rows -> A operand, row info, thresholds)
+    const bool new_tile = tile != prev_tile;
+    if (new_tile && threadIdx.x < BM) {
+      const int kl = (int)threadIdx.x, kt = kl + rbase / n_iso;
+      const int64_t g = (int64_t)tile * a.RT + kt;
+      uint32_t r = 0xffffffffu;
+      int rho = 0;
+      if (kl < BM / n_iso && kt < a.RT && g < a.n_tr) {
+        r = __ldg(a.tlist + g);
+        rho = Rv.info[r].rho;
+      }
+      s_rid[kl] = r;
+      s_rho[kl] = rho;
+    }
+    __syncthreads();
+    if (new_tile) {
+      // A operand: row j = (range kl = j / n_iso, iso i = j % n_iso), a = rv - rho
+      constexpr int UNITS = BM * (K / 8), ROUNDS = (UNITS + NTHREADS - 1) / NTHREADS;
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            __half2 hv = __floats2half2_rn((float)((int)src[2 * e] - rho),
-                                           (float)((int)src[2 * e + 1] - rho));
-            h[e] = *reinterpret_cast<uint32_t*>(&hv);
+      for (int q = 0; q < ROUNDS; ++q) {
+        const int u = (int)threadIdx.x + q * NTHREADS;
+        if (u < UNITS) {
+          const int j = u / (K / 8), c = u % (K / 8);
+          const int kl = j / n_iso, i = j - kl * n_iso;
+          const uint32_t r = s_rid[kl];
+          uint32_t h[4] = {0, 0, 0, 0};
+          uint2 raw8 = make_uint2(0, 0);
+          if (r != 0xffffffffu) {
+            const int rho = s_rho[kl];
+            raw8 = __ldg(reinterpret_cast<const uint2*>(Rv.rows + ((int64_t)r * n_iso + i) * K + c * 8));
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const uint32_t w = e < 2 ? raw8.x : raw8.y;
+              const int b0 = (int)((w >> (16 * (e & 1))) & 255u), b1 = (int)((w >> (16 * (e & 1) + 8)) & 255u);
+              __half2 hv = __floats2half2_rn((float)(b0 - rho), (float)(b1 - rho));
+              h[e] = *reinterpret_cast<uint32_t*>(&hv);
+            }
           }
+          *reinterpret_cast<uint4*>(sA + swz<K>(j, c)) = make_uint4(h[0], h[1], h[2], h[3]);
+          *reinterpret_cast<uint2*>(sRows + j * K + c * 8) = raw8;
         }
-        *reinterpret_cast<uint4*>(sA + swz<K>(j, c)) = make_uint4(h[0], h[1], h[2], h[3]);
-        *reinterpret_cast<uint2*>(sRows + j * K + c * 8) = raw8;
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       if (is_scr) {
-        int64_t g = (int64_t)tile * a.RT + rk_tile;
-        rvalid = (rk_tile < a.RT) && (g < a.n_tr);
+        rvalid = s_rid[rk] != 0xffffffffu;
         if (rvalid) {
-          rid = a.tlist[g];
+          rid = s_rid[rk];
           RangeInfo inf = Rv.info[rid];
           sr = inf.sr;
           srr = inf.srr;
@@ -501,13 +523,11 @@ __global__ void __maxnreg__(MAXREG)
       prev_tile = tile;
     }
     if (threadIdx.x < BM) {  // per-range thresholds: start from what other segments found
-      unsigned long long tb = 0x7ff0000000000000ull;  // +inf
       // thr_s is indexed by the CTA-local range (row / n_iso); the peer CTA
       // of a pair holds the tile's ranges from rbase / n_iso on
-      const int kl = (int)threadIdx.x, kt = kl + rbase / n_iso;
-      const int64_t g = (int64_t)tile * a.RT + kt;
-      if (kl < BM / n_iso && kt < a.RT && g < a.n_tr) tb = a.thr_g[a.tlist[g]];
-      thr_s[threadIdx.x] = tb;
+      const int kl = (int)threadIdx.x;
+      const uint32_t r = kl < BM / n_iso ? s_rid[kl] : 0xffffffffu;
+      thr_s[threadIdx.x] = r != 0xffffffffu ? a.thr_g[r] : 0x7ff0000000000000ull;  // +inf
     }
     for (int i = threadIdx.x; i < NSLICE * BM; i += NTHREADS) {
       qtail[i] = 0;
