@@ -861,6 +861,26 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
   tm.mark();  // 0
   SideStream& side = SideStream::get();
 
+  // flat ranges (fic_flat.cu): detected up front, counted at the first sync
+  FlatArgs fl{};
+  const bool flat_path = p.strategy != FIC_NOSEARCH && !getenv("FIC_NO_FLAT");
+  unsigned long long* flat_ctr = sc.get<unsigned long long>(2);  // [0] count, [1] low word: canon
+  if (flat_path) {
+    fl.img = img;
+    fl.W = g.W;
+    fl.rs = g.rs;
+    fl.nrx = g.nrx;
+    fl.R = g.R;
+    fl.K = K;
+    fl.D = g.D;
+    fl.flat_c = sc.get<int16_t>(g.R);
+    fl.n_flat = flat_ctr;
+    fl.canon = reinterpret_cast<uint32_t*>(flat_ctr + 1);
+    FIC_CUDA(cudaMemsetAsync(flat_ctr, 0, 8, s));
+    FIC_CUDA(cudaMemsetAsync(flat_ctr + 1, 0xff, 8, s));
+    launch_flat_detect(fl, s);
+  }
+
   // ranges (side stream: needs only the image)
   std::vector<int> perm(8 * K), inv(8 * K);
   iso_tables(g.rs, perm.data(), inv.data());
@@ -971,6 +991,8 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
   PlanCounts pc;
   pmark();  // 10
   FIC_CUDA(cudaMemcpyAsync(&pc, d_pc, sizeof(pc), cudaMemcpyDeviceToHost, s));
+  unsigned long long n_flat = 0;
+  if (flat_path) FIC_CUDA(cudaMemcpyAsync(&n_flat, flat_ctr, 8, cudaMemcpyDeviceToHost, s));
   FIC_CUDA(cudaStreamSynchronize(s));
   pmark();  // 11
 
@@ -1037,6 +1059,10 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
     TcArgs ta{titems, tot.n_titems, rid_s + tb, n_tr, wlo, whi, seg_t, seg0, RT, sbase, partials,
               counters, counters + 15, thr_g, 0, nullptr};
     ta.nsub = nsub;
+    if (n_flat) {
+      ta.flat_c = fl.flat_c;
+      ta.flat_canon = fl.canon;
+    }
     ta.n_split = nsub > 1 ? std::min<int64_t>(tot.n_titems, 2 * 148) : 0;
     const char* dbg_env = getenv("FIC_TC_DEBUG");
     if (dbg_env && (atoi(dbg_env) & (32 | 8192))) {
@@ -1086,6 +1112,19 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
   tm.mark();  // 5
   MergeArgs ma{g.R, sbase, nslots, partials, records, pre_rms, post_rms, (double)K};
   launch_merge(ma, s);
+  if (n_flat) {  // flat ranges on the canonical slab: one reduction per pixel value
+    fl.lo = pb.lo;
+    fl.hi = pb.hi;
+    fl.nslots = nslots;
+    fl.present = sc.get<uint8_t>(256);
+    fl.nchunk = (int)cdiv(g.D, 4096);
+    fl.part = sc.get<FlatArgs::Best>((size_t)256 * fl.nchunk);
+    fl.best = sc.get<FlatArgs::Best>(256);
+    fl.records = records;
+    fl.pre_rms = pre_rms;
+    fl.post_rms = post_rms;
+    launch_flat_match(P, fl, s);
+  }
   tm.mark();  // 6
 
   unsigned long long hc[16];

@@ -380,6 +380,7 @@ __global__ void __maxnreg__(MAXREG)
   int32_t rlo = 0, rhi = 0;
   uint32_t rid = 0;
   bool rvalid = false;
+  bool rflat = false;  // flat range on the canonical slab: the flat kernels match it
   unsigned long long evals = 0, seed_rounds = 0, hit_rounds = 0, hit_lanes = 0;
   long long tw0 = 0, tw1 = 0, tw2 = 0, tw3 = 0, tw4 = 0;  // stall cycles (debug & 4)
   const long long tstart = TCLK();
@@ -504,6 +505,7 @@ __global__ void __maxnreg__(MAXREG)
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       if (is_scr) {
         rvalid = s_rid[rk] != 0xffffffffu;
+        rflat = false;
         if (rvalid) {
           rid = s_rid[rk];
           RangeInfo inf = Rv.info[rid];
@@ -512,6 +514,10 @@ __global__ void __maxnreg__(MAXREG)
           V = inf.V;
           rlo = Rv.lo[rid];
           rhi = Rv.hi[rid];
+          if (a.flat_c) {
+            const uint32_t cr = *a.flat_canon;
+            rflat = a.flat_c[rid] >= 0 && rlo == Rv.lo[cr] && rhi == Rv.hi[cr];
+          }
           // ||a||^2 = sum (r - rho)^2 = srr - 2 rho sr + K rho^2 (exact)
           double an = (double)((int64_t)srr - 2 * (int64_t)inf.rho * (int64_t)sr +
                                (int64_t)K * inf.rho * inf.rho);
@@ -757,7 +763,7 @@ __global__ void __maxnreg__(MAXREG)
           for (int h = 0; h < SW / CH; ++h) {
             const int32_t rel = j * BN + slice * SW + CH * h;
             const int32_t e_lo = lo32 - rel, e_hi = hi32 - rel;
-            const bool hit = !(debug & 8) & rvalid & (e_lo < CH) & (e_hi > 0) & (mx[h] >= s_r);
+            const bool hit = !(debug & 8) & rvalid & !rflat & (e_lo < CH) & (e_hi > 0) & (mx[h] >= s_r);
             if (__any_sync(0xffffffffu, hit)) slow_path(v + CH * h, rel, e_lo, e_hi, hit);
           }
         } else {
@@ -778,7 +784,7 @@ __global__ void __maxnreg__(MAXREG)
             // bitwise, so the max is computed unconditionally (no branch around it)
             // [rel, rel + CH) meets [lo32, hi32) (hi32 > lo32 when valid): one unsigned compare
             const bool in_window = (uint32_t)(e_hi - 1) < (uint32_t)(hi32 - lo32 + CH - 1);
-            const bool hit = !(debug & 8) & in_window & (mx >= s_r);
+            const bool hit = !(debug & 8) & in_window & !rflat & (mx >= s_r);
             if (__any_sync(0xffffffffu, hit)) slow_path(v, rel, e_lo, e_hi, hit);
           }
         }

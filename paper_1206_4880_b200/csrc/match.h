@@ -58,7 +58,39 @@ struct TcArgs {
   unsigned long long* dbg;     // timeline buffer (debug & 32)
   int64_t n_split;             // the last n_split items run as nsub column pieces each
   int nsub;                    // partial slots per segment (slot = segment * nsub + piece)
+  // flat ranges (all pixels equal) whose slab is the canonical flat slab are
+  // matched by the flat kernels (fic_flat.cu), not screened: nullptr = none
+  const int16_t* flat_c;       // [R] pixel value of a flat range, -1 otherwise
+  const uint32_t* flat_canon;  // [1] smallest flat range index (its slab is canonical)
 };
+
+// Flat ranges (every pixel equal to c): all isometries give the same row and
+// the LS fit is s = 0, o = c exactly, so each candidate's error is a function
+// of (c, sum_d, sum_dd) alone and the range's best is shared by all flat
+// ranges with the same value and slab -- one reduction per value c instead
+// of a screen that cannot prune them (its lower bound V - u^2 is 0).
+struct FlatArgs {
+  const uint8_t* img;
+  int W, rs, nrx, R;
+  int16_t* flat_c;             // [R] out (detect): c or -1
+  unsigned long long* n_flat;  // [1] out (detect): count
+  uint32_t* canon;             // [1] out (detect): smallest flat range index (init 0xffffffff)
+  const int32_t* lo;           // [R] slabs
+  const int32_t* hi;
+  const int32_t* nslots;       // [R] ranges matched by this call (> 0)
+  uint8_t* present;            // [256] values of canonical flat ranges matched here
+  struct Best { double err; uint32_t dom; int32_t sq, oq, pad; };
+  Best* part;                  // [256][nchunk] per-chunk bests
+  Best* best;                  // [256]
+  int nchunk;
+  int64_t D;
+  int K;
+  uint8_t* records;
+  double* pre_rms;
+  double* post_rms;
+};
+void launch_flat_detect(const FlatArgs& a, cudaStream_t s);
+void launch_flat_match(const PoolView& P, const FlatArgs& a, cudaStream_t s);
 bool tc_supported(int K);
 int tc_tile_rows(int K);
 void launch_tc(const PoolView& P, const RangeView& Rv, const TcArgs& a, cudaStream_t s);

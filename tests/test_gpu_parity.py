@@ -155,6 +155,27 @@ def test_encode_count_sort_equals_stable_sort_at_cfg3(monkeypatch):
         assert torch.equal(a.pool_sizes, b.pool_sizes), delta
 
 
+@pytest.mark.parametrize("strategy", ["exhaustive", "dynamic_fd"])
+def test_flat_ranges_path_equals_screened_path(strategy, monkeypatch):
+    """Flat ranges (all pixels equal) are matched by one reduction per pixel
+    value (fic_flat.cu) instead of the screen; FIC_NO_FLAT sends them through
+    the screen + exact rescoring.  Same records and RMS, on the smooth
+    gradient half of the cfg4 generator (many flat 4x4 and 8x8 ranges)."""
+    import torch
+    img = np.ascontiguousarray(synth.CONFIGS["cfg4"].make()[:256, :256])
+    d = torch.from_numpy(img).cuda()
+    for rs in (4, 8):
+        if strategy == "dynamic_fd" and rs == 4:
+            continue  # 4x4 ranges have one DBC scale (the reference raises)
+        kw = dict(range_size=rs, domain_size=2 * rs, stride=2, isometries=True)
+        a = codec.encode_device(d, strategy, **kw)
+        monkeypatch.setenv("FIC_NO_FLAT", "1")
+        b = codec.encode_device(d, strategy, **kw)
+        monkeypatch.delenv("FIC_NO_FLAT")
+        assert torch.equal(a.records, b.records), rs
+        assert torch.equal(a.post_rms, b.post_rms) and torch.equal(a.pre_rms, b.pre_rms), rs
+
+
 def test_dbc_grid_known_answers():
     for side in (8, 16, 32):
         assert np.array_equal(codec.dbc_grid(FD[f"rand{side}.blocks"]), FD[f"rand{side}.fd"])
