@@ -20,8 +20,15 @@ __global__ void k_flat_detect(FlatArgs a) {
   const uint8_t* base = a.img + (int64_t)ry * a.rs * a.W + (int64_t)rx * a.rs;
   const int c = base[0];
   bool flat = true;
-  for (int i = 0; i < a.rs && flat; ++i)
-    for (int j = 0; j < a.rs; ++j) flat = flat && (base[(int64_t)i * a.W + j] == c);
+  if (a.rs == 8 && (a.W & 7) == 0) {  // aligned 8-byte rows
+    const unsigned long long cc = 0x0101010101010101ull * (unsigned long long)c;
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      flat = flat && (__ldg(reinterpret_cast<const unsigned long long*>(base + (int64_t)i * a.W)) == cc);
+  } else {
+    for (int i = 0; i < a.rs && flat; ++i)
+      for (int j = 0; j < a.rs; ++j) flat = flat && (base[(int64_t)i * a.W + j] == c);
+  }
   a.flat_c[r] = flat ? (int16_t)c : (int16_t)-1;
   if (flat) {
     atomicAdd(a.n_flat, 1ull);
