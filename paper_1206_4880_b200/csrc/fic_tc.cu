@@ -820,39 +820,61 @@ __global__ void __maxnreg__(MAXREG)
       uint32_t hd[RROWS * NSLICE];
 #pragma unroll
       for (int q = 0; q < RROWS * NSLICE; ++q) hd[q] = 0;
+      // two candidates per pass (from any of the thread's queues), evaluated
+      // back to back so their fp64 chains overlap; updates applied in order
+      auto apply = [&](int r, const Cand& cd, uint32_t did) {
+        const int k = r / n_iso;
+        RowState st = rstate[r];
+        st.pre = fmin(st.pre, cd.pre);
+        if (better(cd.err, did, st.iso, st.err, st.dom, st.iso)) {
+          st.err = cd.err;
+          st.dom = did;
+          st.sq = (uint8_t)cd.sq;
+          st.oq = (uint8_t)cd.oq;
+        }
+        rstate[r] = st;
+        const unsigned long long eb = (unsigned long long)__double_as_longlong(fmax(cd.err, 0.0));
+        if (eb < thr_s[k]) {  // an improvement: publish to the screeners and the other segments
+          atomicMin(thr_s + k, eb);
+          atomicMin(a.thr_g + s_rid[k], eb);
+        }
+      };
       while (true) {
-        int got = -1;
-        uint32_t rel = 0;
+        int got0 = -1, got1 = -1;
+        uint32_t rel0 = 0, rel1 = 0;
 #pragma unroll
         for (int q = 0; q < RROWS * NSLICE; ++q) {
           const int r = t + RSTRIDE * (q / NSLICE), qs = q % NSLICE;
-          if (got < 0 && hd[q] != qtail[r * NSLICE + qs]) {
-            __threadfence_block();
-            rel = qbuf[(r * NSLICE + qs) * QCAP + (hd[q] & (QCAP - 1))];
-            qhead[r * NSLICE + qs] = ++hd[q];
-            got = q / NSLICE;
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const bool want = e == 0 ? got0 < 0 : (got0 >= 0 && got1 < 0);
+            if (want && hd[q] != qtail[r * NSLICE + qs]) {
+              __threadfence_block();
+              const uint32_t v = qbuf[(r * NSLICE + qs) * QCAP + (hd[q] & (QCAP - 1))];
+              qhead[r * NSLICE + qs] = ++hd[q];
+              if (e == 0) {
+                rel0 = v;
+                got0 = q / NSLICE;
+              } else {
+                rel1 = v;
+                got1 = q / NSLICE;
+              }
+            }
           }
         }
-        if (got >= 0) {
-          const int r = t + RSTRIDE * got, k = r / n_iso;
-          RowState st = rstate[r];
-          const int64_t p = c0 + rel;
-          const Cand cd = exact(p, r, st.sr, st.srr);
-          const uint32_t did = __ldg(P.ids + p);
-          st.pre = fmin(st.pre, cd.pre);
-          if (better(cd.err, did, st.iso, st.err, st.dom, st.iso)) {
-            st.err = cd.err;
-            st.dom = did;
-            st.sq = (uint8_t)cd.sq;
-            st.oq = (uint8_t)cd.oq;
+        if (got0 >= 0) {
+          const int r0 = t + RSTRIDE * got0;
+          const int r1 = got1 >= 0 ? t + RSTRIDE * got1 : r0;
+          const int64_t p0 = c0 + rel0, p1 = got1 >= 0 ? c0 + rel1 : p0;
+          const Cand cd0 = exact(p0, r0, rstate[r0].sr, rstate[r0].srr);
+          const Cand cd1 = exact(p1, r1, rstate[r1].sr, rstate[r1].srr);
+          const uint32_t did0 = __ldg(P.ids + p0), did1 = __ldg(P.ids + p1);
+          apply(r0, cd0, did0);
+          evals += 1;
+          if (got1 >= 0) {
+            apply(r1, cd1, did1);
+            evals += 1;
           }
-          rstate[r] = st;
-          const unsigned long long eb = (unsigned long long)__double_as_longlong(fmax(cd.err, 0.0));
-          if (eb < thr_s[k]) {  // an improvement: publish to the screeners and the other segments
-            atomicMin(thr_s + k, eb);
-            atomicMin(a.thr_g + a.tlist[(int64_t)tile * a.RT + (r + rbase) / n_iso], eb);
-          }
-          ++evals;
         } else if (*edone == (uint32_t)NEPI) {
           __threadfence_block();
           bool empty = true;
