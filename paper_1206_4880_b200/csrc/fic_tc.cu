@@ -839,42 +839,46 @@ __global__ void __maxnreg__(MAXREG)
           atomicMin(a.thr_g + s_rid[k], eb);
         }
       };
+      constexpr int NE = 4;  // candidates per pass
       while (true) {
-        int got0 = -1, got1 = -1;
-        uint32_t rel0 = 0, rel1 = 0;
+        int got[NE];
+        uint32_t rel[NE];
+#pragma unroll
+        for (int e = 0; e < NE; ++e) {
+          got[e] = -1;
+          rel[e] = 0;
+        }
+        int ng = 0;
 #pragma unroll
         for (int q = 0; q < RROWS * NSLICE; ++q) {
           const int r = t + RSTRIDE * (q / NSLICE), qs = q % NSLICE;
+          const uint32_t tl = qtail[r * NSLICE + qs];
 #pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const bool want = e == 0 ? got0 < 0 : (got0 >= 0 && got1 < 0);
-            if (want && hd[q] != qtail[r * NSLICE + qs]) {
+          for (int e = 0; e < NE; ++e) {
+            if (ng == e && hd[q] != tl) {
               __threadfence_block();
-              const uint32_t v = qbuf[(r * NSLICE + qs) * QCAP + (hd[q] & (QCAP - 1))];
+              rel[e] = qbuf[(r * NSLICE + qs) * QCAP + (hd[q] & (QCAP - 1))];
               qhead[r * NSLICE + qs] = ++hd[q];
-              if (e == 0) {
-                rel0 = v;
-                got0 = q / NSLICE;
-              } else {
-                rel1 = v;
-                got1 = q / NSLICE;
-              }
+              got[e] = q / NSLICE;
+              ++ng;
             }
           }
         }
-        if (got0 >= 0) {
-          const int r0 = t + RSTRIDE * got0;
-          const int r1 = got1 >= 0 ? t + RSTRIDE * got1 : r0;
-          const int64_t p0 = c0 + rel0, p1 = got1 >= 0 ? c0 + rel1 : p0;
-          const Cand cd0 = exact(p0, r0, rstate[r0].sr, rstate[r0].srr);
-          const Cand cd1 = exact(p1, r1, rstate[r1].sr, rstate[r1].srr);
-          const uint32_t did0 = __ldg(P.ids + p0), did1 = __ldg(P.ids + p1);
-          apply(r0, cd0, did0);
-          evals += 1;
-          if (got1 >= 0) {
-            apply(r1, cd1, did1);
-            evals += 1;
+        if (ng > 0) {
+          Cand cd[NE];
+          uint32_t did[NE];
+          int rr[NE];
+#pragma unroll
+          for (int e = 0; e < NE; ++e) {
+            rr[e] = got[e] >= 0 ? t + RSTRIDE * got[e] : t + RSTRIDE * got[0];
+            const int64_t p = c0 + (got[e] >= 0 ? rel[e] : rel[0]);
+            cd[e] = exact(p, rr[e], rstate[rr[e]].sr, rstate[rr[e]].srr);
+            did[e] = __ldg(P.ids + p);
           }
+#pragma unroll
+          for (int e = 0; e < NE; ++e)
+            if (e < ng) apply(rr[e], cd[e], did[e]);
+          evals += ng;
         } else if (*edone == (uint32_t)NEPI) {
           __threadfence_block();
           bool empty = true;
