@@ -182,7 +182,7 @@ def run_reference(args):
 
 
 def _pool_roofline(stats, peak_gbs, src):
-    """HBM roofline of the pool builder K1 (k_boxplanes + k_pool, DESIGN.md
+    """HBM roofline of the pool builder K1 (k_domrows + k_pool, DESIGN.md
     section 4): algorithmic bytes = the image read once + per domain the 4 B
     order entry read and 3K + 20 B written (raw K u8, fp16 B row 2K,
     inv_den 8, sums 8, ids 4), over the device time of the two launches
@@ -192,7 +192,7 @@ def _pool_roofline(stats, peak_gbs, src):
     ms = float(np.mean([s["ms_pool"] for s in stats]))
     nbytes = HW + D * (4 + 3 * K + 20)
     gbs = nbytes / (ms / 1e3) / 1e9 if ms > 0 else 0.0
-    return {"bound": "hbm", "kernel": "k_boxplanes + k_pool (pool builder K1)", "achieved": gbs,
+    return {"bound": "hbm", "kernel": "k_domrows + k_pool (pool builder K1)", "achieved": gbs,
             "peak": peak_gbs, "unit": "GB/s", "frac": gbs / peak_gbs,
             "peak_source": f"{src} copy bandwidth", "algorithmic_bytes_per_launch": nbytes,
             "ms_per_launch": ms, "traffic": None}

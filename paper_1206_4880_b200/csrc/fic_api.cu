@@ -911,7 +911,14 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
   pa.rs = g.rs;
   pa.plane_rows = g.H - 1;
   pa.pitch = (int)align_up((size_t)(g.W / 2 + 16), 16);
-  pa.planes = sc.get<uint8_t>((size_t)2 * pa.plane_rows * pa.pitch);
+  pa.mh = g.H / 2;
+  // 8x8 ranges: per-domain-column row segments when they fit well inside L2
+  // (cfg3: 8.3 MB), else the box-floor planes (cfg5: T would be 268 MB)
+  const size_t t_bytes = (size_t)g.ndx * 2 * pa.mh * 8;
+  if (g.rs == 8 && g.st <= 16 && t_bytes <= ((size_t)48 << 20) && !getenv("FIC_POOL_PLANES"))
+    pa.trows = sc.get<unsigned long long>(t_bytes / 8);
+  else
+    pa.planes = sc.get<uint8_t>((size_t)2 * pa.plane_rows * pa.pitch);
   pa.st = g.st;
   pa.ndx = g.ndx;
   pa.D = g.D;

@@ -706,19 +706,110 @@ __device__ __forceinline__ unsigned long long bytes8(const uint8_t* row, int k) 
   return sh ? ((lo >> sh) | (hi << (64 - sh))) : lo;
 }
 
-// One warp builds 32 consecutive pool positions.  Pass 1: RS lanes per
-// domain, one decimated row each (a short read from a box-floor plane), so a
-// warp instruction moves 32/RS whole domains: raw rows are stored as one
-// contiguous run, and the row sums are reduced across the RS lanes and
-// handed to lane j (domain p0 + j).  Lane j then does the per-domain fp64
-// work once (den, 1/den as codec.py:141-145, the row scale) and writes the
-// per-domain scalars coalesced.  Pass 2 converts the rows kept in registers
-// into fp16 B rows, again one contiguous run per instruction.
-//   B_k = fp16(fp32(K d_k - sum_d) * fp32(1 / sqrt(K den)))
+// One warp builds 32 consecutive pool positions: RS lanes per domain, one
+// decimated row each (a short read from a box-floor plane), so every warp
+// instruction moves 32/RS whole domains -- raw rows and fp16 B rows are
+// stored as contiguous runs.  Row sums are reduced across the RS lanes
+// (dp4a + xor shuffles) and also handed to lane j (domain p0 + j), which
+// does the per-domain fp64 work once (1/den as codec.py:141-145) and writes
+// the per-domain scalars coalesced.
+//   B_k = fp16(fp32(K d_k - sum_d) * rsqrt(K den))
 // fp32 rounding before the fp16 rounding is far inside the screen's error
 // budget (fic_tc.cu: eps has 2^-12 + 2^-13 of slack beyond fp16's 2^-11).
+// 8 bytes starting at byte address q (8-byte aligned loads + funnel shift)
+__device__ __forceinline__ unsigned long long bytes8_at(const uint8_t* q) {
+  const uintptr_t u = reinterpret_cast<uintptr_t>(q);
+  const unsigned long long* w = reinterpret_cast<const unsigned long long*>(u & ~(uintptr_t)7);
+  const int sh = (int)(u & 7) * 8;
+  const unsigned long long lo = __ldg(w), hi = __ldg(w + 1);
+  return sh ? ((lo >> sh) | (hi << (64 - sh))) : lo;
+}
+
+// Domain row segments: T[dx][y & 1][y >> 1] = the 8 box-floor values
+// (I[y][x] + I[y][x+1] + I[y+1][x] + I[y+1][x+1]) >> 2 at x = X + 2j,
+// j < 8, X = dx * st (blocks.py:75-82).  Row i of the domain at (Y, X) is
+// T[dx][Y & 1][(Y >> 1) + i]: the pool builder reads a whole domain as 64
+// contiguous bytes.  Used when T fits comfortably in L2.
+// One block per 32 domain columns x 64 image rows: the image patch is staged
+// in shared memory (coalesced rows), each warp computes 32 consecutive
+// entries of one T[dx][par][.] run from it and writes them (256 bytes).
+constexpr int DR_COLS = 32, DR_ROWS = 64;
+__global__ void __launch_bounds__(256) k_domrows(const uint8_t* img, int H, int W, int st, int ndx,
+                                                 int mh, unsigned long long* T) {
+  extern __shared__ __align__(16) uint8_t dsm[];
+  const int pw = (DR_COLS - 1) * st + 16;  // patch width (bytes)
+  const int pwa = ((pw + 3) & ~3) + 4;     // row pitch: 4-byte aligned, one spare word
+  uint8_t* patch = dsm;                    // [DR_ROWS + 1][pwa]
+  const int dx0 = blockIdx.x * DR_COLS, y0 = blockIdx.y * DR_ROWS;
+  const int X0 = dx0 * st;
+  // patch rows as 4-byte words (X0 is a multiple of 32, W of 8), all loads
+  // of a thread issued before any store
+  const int pw4 = (pw + 3) >> 2, nw = (DR_ROWS + 1) * pw4;
+  constexpr int MAXW = 12;  // words per thread for st <= 4 (65 x 36 / 256 < 10)
+  if (nw <= MAXW * 256) {
+    uint32_t v[MAXW];
+#pragma unroll
+    for (int q = 0; q < MAXW; ++q) {
+      const int i = threadIdx.x + q * 256;
+      const int yy = i / pw4, xw = i - yy * pw4;
+      const int gy = y0 + yy, gx = X0 + 4 * xw;
+      v[q] = (i < nw && gy < H && gx + 3 < W)
+                 ? __ldg(reinterpret_cast<const uint32_t*>(img + (int64_t)gy * W + gx))
+                 : 0u;
+    }
+#pragma unroll
+    for (int q = 0; q < MAXW; ++q) {
+      const int i = threadIdx.x + q * 256;
+      if (i < nw) {
+        const int yy = i / pw4, xw = i - yy * pw4;
+#pragma unroll
+        *reinterpret_cast<uint32_t*>(patch + yy * pwa + 4 * xw) = v[q];
+      }
+    }
+  } else {
+    for (int i = threadIdx.x; i < (DR_ROWS + 1) * pw; i += blockDim.x) {
+      const int yy = i / pw, xx = i - yy * pw;
+      const int gy = y0 + yy, gx = X0 + xx;
+      patch[yy * pwa + xx] = (gy < H && gx < W) ? __ldg(img + (int64_t)gy * W + gx) : 0;
+    }
+  }
+  __syncthreads();
+  // lane = m within the block's 32 rows of one parity, warp-uniform (dx, par):
+  // each warp writes one 256-byte run of T
+  const int m0 = y0 / 2;
+  for (int i = threadIdx.x; i < DR_COLS * DR_ROWS; i += blockDim.x) {
+    const int ml = i % (DR_ROWS / 2), rest = i / (DR_ROWS / 2);
+    const int par = rest & 1, c = rest >> 1;
+    const int yy = 2 * ml + par;
+    // 16 bytes of two patch rows as words (funnel-shifted to the byte
+    // offset), 2x2 floor means in 16-bit lanes: (even + odd bytes) >> 2
+    const int o0 = yy * pwa + c * st, sh = (o0 & 3) * 8;
+    const uint32_t* q0 = reinterpret_cast<const uint32_t*>(patch + (o0 & ~3));
+    const uint32_t* q1 = q0 + pwa / 4;
+    uint32_t a[5], b[5];
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+      a[k] = q0[k];
+      b[k] = q1[k];
+    }
+    uint32_t res[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t w = __funnelshift_r(a[k], a[k + 1], sh), v = __funnelshift_r(b[k], b[k + 1], sh);
+      const uint32_t sum = __byte_perm(w, 0, 0x4240) + __byte_perm(w, 0, 0x4341) +
+                           __byte_perm(v, 0, 0x4240) + __byte_perm(v, 0, 0x4341);
+      res[k] = (sum >> 2) & 0x00ff00ffu;  // means of bytes (0,1) and (2,3) at bytes 0 and 2
+    }
+    unsigned long long out = (unsigned long long)__byte_perm(res[0], res[1], 0x6420) |
+                             ((unsigned long long)__byte_perm(res[2], res[3], 0x6420) << 32);
+    const int dx = dx0 + c, m = m0 + ml;
+    if (y0 + yy >= H - 1) out = 0;
+    if (dx < ndx && m < mh) T[((int64_t)dx * 2 + par) * mh + m] = out;
+  }
+}
+
 template <int RS>
-__global__ void __launch_bounds__(256, 4) k_pool(PoolArgs a) {
+__global__ void __launch_bounds__(256, 8) k_pool(PoolArgs a) {
   constexpr int K = RS * RS;
   constexpr int DPI = 32 / RS;  // domains per instruction
   constexpr int NIT = RS;       // instructions per 32 domains
@@ -726,35 +817,40 @@ __global__ void __launch_bounds__(256, 4) k_pool(PoolArgs a) {
   const int64_t p0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32;
   if (p0 >= a.D) return;
   const int g = lane / RS, i = lane % RS;
-  const uint32_t ndx = (uint32_t)a.ndx, D = (uint32_t)a.D;
+  const uint32_t D = (uint32_t)a.D;
+  // lane j locates domain p0 + j once: byte offset of its first decimated row
+  // in the box-floor planes; the RS lanes of each row read it by shuffle
+  const uint32_t pm = (uint32_t)p0 + lane;
+  const uint32_t my_id = pm < D ? (a.order ? __ldg(a.order + pm) : pm) : 0u;
+  uint32_t my_off;
+  {
+    const uint32_t dy = my_id / (uint32_t)a.ndx, dx = my_id - dy * (uint32_t)a.ndx;
+    const uint32_t Y = dy * a.st, X = dx * a.st;
+    my_off = a.trows ? ((dx * 2u + (Y & 1u)) * (uint32_t)a.mh + (Y >> 1))
+                     : (X & 1) * (uint32_t)a.plane_rows * (uint32_t)a.pitch + Y * (uint32_t)a.pitch + (X >> 1);
+  }
   const uint32_t ip = (uint32_t)(2 * i) * (uint32_t)a.pitch;
-  const uint32_t plane_sz = (uint32_t)a.plane_rows * (uint32_t)a.pitch;
-  uint32_t w0[NIT], w1[NIT];  // the row's decimated bytes (RS == 4: w0 only)
-  uint32_t ks[NIT];           // domain sums of instruction k's domain g
   uint32_t my_sd = 0, my_sdd = 0;
+  const float2 kk = make_float2((float)K, (float)K);
 #pragma unroll
   for (int k = 0; k < NIT; ++k) {
     const uint32_t p = (uint32_t)p0 + k * DPI + g;
     const bool ok = p < D;
-    const uint32_t id = ok ? (a.order ? __ldg(a.order + p) : p) : 0u;
-    const uint32_t dy = id / ndx, dx = id - dy * ndx;
-    const uint32_t Y = dy * a.st, X = dx * a.st;
-    const uint8_t* rowp = a.planes + (X & 1) * plane_sz + Y * a.pitch + ip;
-    const unsigned long long r = ok ? bytes8(rowp, X >> 1) : 0ull;
-    w0[k] = (uint32_t)r;
-    w1[k] = RS == 8 ? (uint32_t)(r >> 32) : 0u;
+    const uint32_t off = __shfl_sync(0xffffffffu, my_off, (k * DPI + g) & 31);
+    unsigned long long r = 0ull;
+    if (ok) r = (RS == 8 && a.trows) ? __ldg(a.trows + off + i) : bytes8_at(a.planes + off + ip);
+    const uint32_t w0 = (uint32_t)r, w1 = RS == 8 ? (uint32_t)(r >> 32) : 0u;
     // row sums with byte dot products: sum x and sum x^2
-    uint32_t sd = __dp4a(w0[k], 0x01010101u, 0u), sdd = __dp4a(w0[k], w0[k], 0u);
+    uint32_t sd = __dp4a(w0, 0x01010101u, 0u), sdd = __dp4a(w0, w0, 0u);
     if (RS == 8) {
-      sd = __dp4a(w1[k], 0x01010101u, sd);
-      sdd = __dp4a(w1[k], w1[k], sdd);
+      sd = __dp4a(w1, 0x01010101u, sd);
+      sdd = __dp4a(w1, w1, sdd);
     }
 #pragma unroll
     for (int m = 1; m < RS; m <<= 1) {
       sd += __shfl_xor_sync(0xffffffffu, sd, m);
       sdd += __shfl_xor_sync(0xffffffffu, sdd, m);
     }
-    ks[k] = sd;
     const int src = ((lane - k * DPI) * RS) & 31;
     const uint32_t t_sd = __shfl_sync(0xffffffffu, sd, src);
     const uint32_t t_sdd = __shfl_sync(0xffffffffu, sdd, src);
@@ -762,48 +858,40 @@ __global__ void __launch_bounds__(256, 4) k_pool(PoolArgs a) {
       my_sd = t_sd;
       my_sdd = t_sdd;
     }
-    if (ok) {
-      if (RS == 8)
-        reinterpret_cast<uint2*>(a.raw + (size_t)p * K)[i] = make_uint2(w0[k], w1[k]);
-      else
-        reinterpret_cast<uint32_t*>(a.raw + (size_t)p * K)[i] = w0[k];
-    }
-  }
-  const uint32_t pm = (uint32_t)p0 + lane;
-  const int64_t den = (int64_t)K * my_sdd - (int64_t)my_sd * my_sd;
-  float my_scale = 0.0f;
-  if (pm < D) {
-    a.inv_den[pm] = den != 0 ? __ddiv_rn(1.0, (double)den) : 0.0;
-    a.sums[pm] = make_uint2(my_sd, my_sdd);
-    a.ids[pm] = a.order ? __ldg(a.order + pm) : pm;
-    my_scale = den > 0 ? (float)__drcp_rn(__dsqrt_rn((double)K * (double)den)) : 0.0f;
-  }
-  if (!a.bh) return;
-  // fp32 of byte x: 0x4B0000xx - 2^23 = x (exact), then K x - sum_d is an
-  // exact FFMA (|.| < 2^24)
-#pragma unroll
-  for (int k = 0; k < NIT; ++k) {
-    const uint32_t p = (uint32_t)p0 + k * DPI + g;
-    const float sc = __shfl_sync(0xffffffffu, my_scale, (k * DPI + g) & 31);
-    const float off = -(float)ks[k];
+    if (!ok) continue;
+    if (RS == 8)
+      reinterpret_cast<uint2*>(a.raw + (size_t)p * K)[i] = make_uint2(w0, w1);
+    else
+      reinterpret_cast<uint32_t*>(a.raw + (size_t)p * K)[i] = w0;
+    if (!a.bh) continue;
+    // B row: fp16(fp32(K x - sum_d) * rsqrt(K den)); x from the byte via
+    // 0x4B0000xx - 2^23 (exact), K x - sum_d by an exact FMA (|.| < 2^24),
+    // packed fp32 pairs.  rsqrtf's ~2 ulp are far inside the screen's slack.
+    const int den = K * (int)sdd - (int)sd * (int)sd;  // < 2^31
+    const float sc = den > 0 ? rsqrtf((float)K * (float)den) : 0.0f;
+    const float2 sc2 = make_float2(sc, sc), offs = make_float2(-(float)sd, -(float)sd);
     uint32_t h[RS / 2];
 #pragma unroll
     for (int e = 0; e < RS / 2; ++e) {
-      const uint32_t w = e < 2 ? w0[k] : w1[k];
+      const uint32_t w = e < 2 ? w0 : w1;
       const int b0 = (2 * e) & 3;
-      const float m0 = __fsub_rn(__uint_as_float(__byte_perm(w, 0x4B000000u, 0x7640 + b0)), 8388608.0f);
-      const float m1 = __fsub_rn(__uint_as_float(__byte_perm(w, 0x4B000000u, 0x7640 + b0 + 1)), 8388608.0f);
-      const float f0 = __fmul_rn(__fmaf_rn((float)K, m0, off), sc);
-      const float f1 = __fmul_rn(__fmaf_rn((float)K, m1, off), sc);
-      __half2 hv = __floats2half2_rn(f0, f1);
+      float2 m = make_float2(__uint_as_float(__byte_perm(w, 0x4B000000u, 0x7640 + b0)),
+                             __uint_as_float(__byte_perm(w, 0x4B000000u, 0x7640 + b0 + 1)));
+      m = __fadd2_rn(m, make_float2(-8388608.0f, -8388608.0f));
+      const float2 f = __fmul2_rn(__ffma2_rn(kk, m, offs), sc2);
+      __half2 hv = __floats2half2_rn(f.x, f.y);
       h[e] = *reinterpret_cast<uint32_t*>(&hv);
     }
-    if (p < D) {
-      if (RS == 8)
-        reinterpret_cast<uint4*>(a.bh + (size_t)p * K)[i] = make_uint4(h[0], h[1], h[2], h[3]);
-      else
-        reinterpret_cast<uint2*>(a.bh + (size_t)p * K)[i] = make_uint2(h[0], h[1]);
-    }
+    if (RS == 8)
+      reinterpret_cast<uint4*>(a.bh + (size_t)p * K)[i] = make_uint4(h[0], h[1], h[2], h[3]);
+    else
+      reinterpret_cast<uint2*>(a.bh + (size_t)p * K)[i] = make_uint2(h[0], h[1]);
+  }
+  if (pm < D) {
+    const int64_t den = (int64_t)K * my_sdd - (int64_t)my_sd * my_sd;
+    a.inv_den[pm] = den != 0 ? __ddiv_rn(1.0, (double)den) : 0.0;
+    a.sums[pm] = make_uint2(my_sd, my_sdd);
+    a.ids[pm] = my_id;
   }
 }
 
@@ -832,7 +920,20 @@ __global__ void k_pool_generic(PoolArgs a, int rs) {
 void launch_pool(const PoolArgs& a, cudaStream_t s) {
   if (a.D == 0) return;
   unsigned blocks = (unsigned)cdiv(a.D, 256);
-  if ((a.rs == 8 || a.rs == 4) && a.planes) {
+  if (a.rs == 8 && a.trows) {
+    const int pw = (DR_COLS - 1) * a.st + 16;
+    const size_t smem = (size_t)(DR_ROWS + 1) * (((pw + 3) & ~3) + 4) + 16;
+    static bool attr = false;
+    if (!attr) {
+      FIC_CUDA(cudaFuncSetAttribute(k_domrows, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      attr = true;
+    }
+    if (smem > 200 * 1024) invalid("domain stride too large for the row-segment pool builder");
+    dim3 grid((unsigned)cdiv(a.ndx, DR_COLS), (unsigned)cdiv(2 * a.mh, DR_ROWS));
+    k_domrows<<<grid, 256, smem, s>>>(a.img, a.H, a.W, a.st, a.ndx, a.mh, a.trows);
+    FIC_CHECK_LAUNCH();
+    k_pool<8><<<blocks, 256, 0, s>>>(a);
+  } else if ((a.rs == 8 || a.rs == 4) && a.planes) {
     const int64_t n = (int64_t)(a.H - 1) * (a.W - 1);
     k_boxplanes<<<(unsigned)cdiv(n, 256), 256, 0, s>>>(a.img, a.H, a.W, a.pitch, a.planes);
     FIC_CHECK_LAUNCH();

@@ -83,6 +83,8 @@ struct PoolArgs {
   int H, W, rs, st, ndx;
   uint8_t* planes;         // [2][plane_rows][pitch] box-floor planes (scratch)
   int plane_rows, pitch;
+  unsigned long long* trows;  // optional (RS = 8): [ndx][2][mh] decimated row segments, so a
+  int mh;                     // domain's 8 rows are 64 contiguous bytes (scratch)
   int64_t D;
   const uint32_t* order;   // raster id per pool position (nullptr = identity)
   uint8_t* raw;            // [D][K] decimated pixels, pool order

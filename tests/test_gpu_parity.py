@@ -176,6 +176,20 @@ def test_flat_ranges_path_equals_screened_path(strategy, monkeypatch):
         assert torch.equal(a.post_rms, b.post_rms) and torch.equal(a.pre_rms, b.pre_rms), rs
 
 
+def test_pool_row_segments_equal_box_planes(monkeypatch):
+    """The pool builder reads domains from per-column row segments when they
+    fit in L2 (cfg2/cfg3) and from the box-floor planes otherwise (cfg5);
+    both give the same pool, hence the same encode."""
+    import torch
+    img = torch.from_numpy(synth.CONFIGS["cfg2"].make()).cuda()
+    kw = dict(range_size=8, domain_size=16, stride=3, isometries=True, delta=0.1)
+    a = codec.encode_device(img, "dynamic_fd", **kw)
+    monkeypatch.setenv("FIC_POOL_PLANES", "1")
+    b = codec.encode_device(img, "dynamic_fd", **kw)
+    assert torch.equal(a.records, b.records)
+    assert torch.equal(a.post_rms, b.post_rms) and torch.equal(a.pre_rms, b.pre_rms)
+
+
 def test_dbc_grid_known_answers():
     for side in (8, 16, 32):
         assert np.array_equal(codec.dbc_grid(FD[f"rand{side}.blocks"]), FD[f"rand{side}.fd"])
