@@ -393,10 +393,23 @@ __global__ void __launch_bounds__(1024) k_range_scatter(const uint32_t* bin, con
   }
 }
 
+// tensor / exact positions of this shard in the sorted range list
+struct PlanRange {
+  int64_t tb, te, eb, ee;
+};
+__device__ __forceinline__ PlanRange plan_range(const PlanCounts* pc) {
+  PlanRange q;
+  q.tb = pc->shard_begin;
+  q.te = max(q.tb, min(pc->shard_end, pc->n_tensor));
+  q.eb = max(pc->shard_begin, pc->n_tensor);
+  q.ee = max(q.eb, pc->shard_end);
+  return q;
+}
+
 struct TileArgs {
   const unsigned long long* key;  // sorted
   const uint32_t* rid;            // sorted
-  int64_t tb, te;                 // tensor positions of this shard
+  const PlanCounts* pc;           // tensor positions of this shard (device)
   int RT;
   int seg;
   int seg0;
@@ -410,10 +423,11 @@ struct TileArgs {
 };
 
 __global__ void k_tiles(TileArgs a) {
+  const PlanRange q = plan_range(a.pc);
   int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  int64_t b = a.tb + t * a.RT;
-  if (b >= a.te) return;
-  int64_t e = min(a.te, b + a.RT);
+  int64_t b = q.tb + t * a.RT;
+  if (b >= q.te) return;
+  int64_t e = min(q.te, b + a.RT);
   int32_t lo = (int32_t)((a.key[b] >> 32) & 0x7fffffffu);
   int32_t hi = 0;
   for (int64_t i = b; i < e; ++i) hi = max(hi, (int32_t)(uint32_t)a.key[i]);
@@ -432,8 +446,10 @@ __global__ void k_tiles(TileArgs a) {
   atomicAdd(a.useful - 2, (unsigned long long)(hi - lo) * (unsigned long long)((e - b) * a.n_iso));
 }
 
-__global__ void k_exact_segs(const unsigned long long* key, const uint32_t* rid, int64_t eb,
-                             int64_t ee, int seg, int32_t* nseg, int32_t* nslots) {
+__global__ void k_exact_segs(const unsigned long long* key, const uint32_t* rid, const PlanCounts* pc,
+                             int seg, int32_t* nseg, int32_t* nslots) {
+  const PlanRange q = plan_range(pc);
+  const int64_t eb = q.eb, ee = q.ee;
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (eb + i >= ee) return;
   unsigned long long k = key[eb + i];
@@ -474,23 +490,37 @@ __device__ void block_exclusive_scan(const T* in, U* out, int64_t n, U* total) {
   *total = carry;
 }
 
-__global__ void __launch_bounds__(1024) k_plan_scans(const int32_t* tnseg, int32_t* tbase, int64_t ntt,
-                                                     const int32_t* enseg, int32_t* ebase, int64_t ner,
+// ... and the device-side plan (DevPlan) the matchers read their counts from.
+__global__ void __launch_bounds__(1024) k_plan_scans(const int32_t* tnseg, int32_t* tbase,
+                                                     const int32_t* enseg, int32_t* ebase,
                                                      const int32_t* nslots, int64_t* sbase, int R,
-                                                     Totals* out) {
+                                                     const PlanCounts* pc, int RT, int nsub,
+                                                     int split_cap, DevPlan* dp) {
+  const PlanRange q = plan_range(pc);
+  const int64_t n_tr = q.te - q.tb, n_er = q.ee - q.eb, ntt = cdiv(n_tr, RT);
   // three independent scans, one block each
   if (blockIdx.x == 0) {
     int32_t t = 0;
     block_exclusive_scan<int32_t, int32_t>(tnseg, tbase, ntt, &t);
-    if (threadIdx.x == 0) out->n_titems = t;
+    if (threadIdx.x == 0) {
+      dp->tb = q.tb;
+      dp->n_tr = n_tr;
+      dp->n_tt = ntt;
+      dp->n_titems = t;
+      dp->n_split = nsub > 1 ? min((int64_t)t, (int64_t)split_cap) : 0;
+    }
   } else if (blockIdx.x == 1) {
     int32_t t = 0;
-    block_exclusive_scan<int32_t, int32_t>(enseg, ebase, ner, &t);
-    if (threadIdx.x == 0) out->n_eitems = t;
+    block_exclusive_scan<int32_t, int32_t>(enseg, ebase, n_er, &t);
+    if (threadIdx.x == 0) {
+      dp->eb = q.eb;
+      dp->n_er = n_er;
+      dp->n_eitems = t;
+    }
   } else {
     int64_t t = 0;
     block_exclusive_scan<int32_t, int64_t>(nslots, sbase, R, &t);
-    if (threadIdx.x == 0) out->n_slots = t;
+    if (threadIdx.x == 0) dp->n_slots = t;
   }
 }
 
@@ -503,9 +533,9 @@ __global__ void k_totals(const int32_t* tnseg, const int32_t* tbase, int64_t ntt
   out->n_slots = R ? sbase[R - 1] + nslots[R - 1] : 0;
 }
 
-__global__ void k_expand(const int32_t* nseg, const int32_t* base, int64_t n, int2* items) {
+__global__ void k_expand(const int32_t* nseg, const int32_t* base, const DevPlan* dp, int2* items) {
   int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= n) return;
+  if (t >= dp->n_er) return;
   int32_t b = base[t];
   for (int s = 0; s < nseg[t]; ++s) items[b + s] = make_int2((int)t, s);
 }
@@ -513,7 +543,9 @@ __global__ void k_expand(const int32_t* nseg, const int32_t* base, int64_t n, in
 // Work items in segment-major order: (tile t, segment s) sorted by (s, t).
 // One block: for each segment index, a block-wide scan of "tile t has a
 // segment s" gives the rank of t among those tiles.
-__global__ void __launch_bounds__(1024) k_items_segmajor(const int32_t* nseg, int64_t n, int2* items) {
+__global__ void __launch_bounds__(1024) k_items_segmajor(const int32_t* nseg, const DevPlan* dp,
+                                                         int2* items) {
+  const int64_t n = dp->n_tt;
   using Scan = cub::BlockScan<int, 1024>;
   using Reduce = cub::BlockReduce<int, 1024>;
   __shared__ typename Scan::TempStorage scan_tmp;
@@ -640,11 +672,12 @@ struct PlanBufs {
 };
 
 static PlanBufs make_plan(Scratch& sc, cudaStream_t s, const uint8_t* img, const Geo& g,
-                          const fic_params_t& p, bool want_fd_dom, bool stable_order) {
+                          const fic_params_t& p, bool want_fd_dom, bool stable_order,
+                          double* scal_buf = nullptr) {
   PlanBufs pb;
   pb.lo = sc.get<int32_t>(g.R);
   pb.hi = sc.get<int32_t>(g.R);
-  pb.scal = sc.get<double>(4);
+  pb.scal = scal_buf ? scal_buf : sc.get<double>(4);
   FIC_CUDA(cudaMemsetAsync(pb.scal, 0, 4 * sizeof(double), s));
   SlabArgs sa{};
   sa.R = g.R;
@@ -856,7 +889,7 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
   const bool ptime = getenv("FIC_PLAN_TIMING") != nullptr;
   int pn = 8;
   auto pmark = [&]() {
-    if (ptime && pn < 24) FIC_CUDA(cudaEventRecord(tm.ev[pn++], s));
+    if (ptime && pn < 23) FIC_CUDA(cudaEventRecord(tm.ev[pn++], s));
   };
   tm.mark();  // 0
   SideStream& side = SideStream::get();
@@ -864,7 +897,16 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
   // flat ranges (fic_flat.cu): detected up front, counted at the first sync
   FlatArgs fl{};
   const bool flat_path = p.strategy != FIC_NOSEARCH && !getenv("FIC_NO_FLAT");
-  unsigned long long* flat_ctr = sc.get<unsigned long long>(2);  // [0] count, [1] low word: canon
+  // everything read back at the end, in one block (one copy)
+  struct Readback {
+    unsigned long long counters[16];
+    double scal[4];
+    DevPlan plan;
+    unsigned long long flat[2];  // [0] flat count, [1] low word: canonical flat range
+  };
+  Readback* d_rb = sc.get<Readback>(1);
+  FIC_CUDA(cudaMemsetAsync(d_rb, 0, sizeof(Readback), s));
+  unsigned long long* flat_ctr = d_rb->flat;
   if (flat_path) {
     fl.img = img;
     fl.W = g.W;
@@ -876,7 +918,6 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
     fl.flat_c = sc.get<int16_t>(g.R);
     fl.n_flat = flat_ctr;
     fl.canon = reinterpret_cast<uint32_t*>(flat_ctr + 1);
-    FIC_CUDA(cudaMemsetAsync(flat_ctr, 0, 8, s));
     FIC_CUDA(cudaMemsetAsync(flat_ctr + 1, 0xff, 8, s));
     launch_flat_detect(fl, s);
   }
@@ -900,7 +941,7 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
   FIC_CUDA(cudaStreamWaitEvent(side.s2, side.ev[0], 0));
   launch_ranges(ra, side.s2);
 
-  PlanBufs pb = make_plan(sc, s, img, g, p, false, false);
+  PlanBufs pb = make_plan(sc, s, img, g, p, false, false, d_rb->scal);
   tm.mark();  // 1
 
   // K1 pool builder (side stream: needs the FD order, overlaps the planning)
@@ -939,8 +980,7 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
   pmark();  // 9
 
   // plan: classify, sort by (class, lo, hi), shard by cost
-  unsigned long long* counters = sc.get<unsigned long long>(16);
-  FIC_CUDA(cudaMemsetAsync(counters, 0, 16 * sizeof(unsigned long long), s));
+  unsigned long long* counters = d_rb->counters;  // zeroed with the readback block
   unsigned long long* key = sc.get<unsigned long long>(g.R);
   unsigned long long* key_s = sc.get<unsigned long long>(g.R);
   uint32_t* rid = sc.get<uint32_t>(g.R);
@@ -995,82 +1035,82 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
     k_shard<<<1, 32, 0, s>>>(key_s, cum, g.R, shard, nshard, d_pc);
     FIC_CHECK_LAUNCH();
   }
-  PlanCounts pc;
   pmark();  // 10
-  FIC_CUDA(cudaMemcpyAsync(&pc, d_pc, sizeof(pc), cudaMemcpyDeviceToHost, s));
-  unsigned long long n_flat = 0;
-  if (flat_path) FIC_CUDA(cudaMemcpyAsync(&n_flat, flat_ctr, 8, cudaMemcpyDeviceToHost, s));
-  FIC_CUDA(cudaStreamSynchronize(s));
   pmark();  // 11
-
-  const int64_t tb = pc.shard_begin, te = std::min(pc.shard_end, pc.n_tensor);
-  const int64_t eb = std::max(pc.shard_begin, pc.n_tensor), ee = pc.shard_end;
-  const int64_t n_tr = std::max<int64_t>(0, te - tb);
-  const int64_t n_er = std::max<int64_t>(0, ee - eb);
-  const int64_t n_tt = cdiv(n_tr, RT);
-
+  // Everything below is enqueued without waiting for the device: counts
+  // live in PlanCounts / DevPlan, allocations use upper bounds.
+  const int64_t n_tt_max = tensor_ok ? cdiv(g.R, RT) : 0;
+  const int64_t n_er_max = g.R;
   int32_t* nslots = sc.get<int32_t>(g.R);
   FIC_CUDA(cudaMemsetAsync(nslots, 0, g.R * sizeof(int32_t), s));
-  int32_t* wlo = sc.get<int32_t>(n_tt);
-  int32_t* whi = sc.get<int32_t>(n_tt);
-  int32_t* tnseg = sc.get<int32_t>(n_tt);
-  int32_t* tbase = sc.get<int32_t>(n_tt);
-  int32_t* enseg = sc.get<int32_t>(n_er);
-  int32_t* ebase = sc.get<int32_t>(n_er);
+  int32_t* wlo = sc.get<int32_t>(n_tt_max);
+  int32_t* whi = sc.get<int32_t>(n_tt_max);
+  int32_t* tnseg = sc.get<int32_t>(n_tt_max);
+  int32_t* tbase = sc.get<int32_t>(n_tt_max);
+  int32_t* enseg = sc.get<int32_t>(n_er_max);
+  int32_t* ebase = sc.get<int32_t>(n_er_max);
   int64_t* sbase = sc.get<int64_t>(g.R);
-  if (n_tt) {
-    TileArgs ta{key_s, rid_s, tb, te, RT, seg_t, seg0, wlo, whi, tnseg, nslots, g.n_iso, counters + 3,
+  if (n_tt_max) {
+    TileArgs ta{key_s, rid_s, d_pc, RT, seg_t, seg0, wlo, whi, tnseg, nslots, g.n_iso, counters + 3,
                 nsub};
-    k_tiles<<<(unsigned)cdiv(n_tt, 128), 128, 0, s>>>(ta);
+    k_tiles<<<(unsigned)cdiv(n_tt_max, 128), 128, 0, s>>>(ta);
     FIC_CHECK_LAUNCH();
   }
-  if (n_er) {
-    k_exact_segs<<<(unsigned)cdiv(n_er, 256), 256, 0, s>>>(key_s, rid_s, eb, ee, seg_e, enseg,
-                                                            nslots);
-    FIC_CHECK_LAUNCH();
-  }
-  Totals* d_tot = sc.get<Totals>(1);
-  k_plan_scans<<<3, 1024, 0, s>>>(tnseg, tbase, n_tt, enseg, ebase, n_er, nslots, sbase, g.R, d_tot);
+  k_exact_segs<<<(unsigned)cdiv(n_er_max, 256), 256, 0, s>>>(key_s, rid_s, d_pc, seg_e, enseg, nslots);
   FIC_CHECK_LAUNCH();
-  Totals tot;
+  constexpr int kSplitCap = 2 * 148;  // tail items run as pieces (TcArgs::n_split)
+  DevPlan* d_plan = &d_rb->plan;
+  k_plan_scans<<<3, 1024, 0, s>>>(tnseg, tbase, enseg, ebase, nslots, sbase, g.R, d_pc, RT, nsub,
+                                  kSplitCap, d_plan);
+  FIC_CHECK_LAUNCH();
   pmark();  // 12
-  FIC_CUDA(cudaMemcpyAsync(&tot, d_tot, sizeof(tot), cudaMemcpyDeviceToHost, s));
-  FIC_CUDA(cudaStreamSynchronize(s));
+  // upper bounds of the item / slot counts (a shard or class can only be smaller)
+  const int64_t segs_max = 1 + cdiv(std::max<int64_t>(g.D - seg0, 0), seg_t);
+  const int64_t esegs_max = tensor_ok ? std::max<int64_t>(1, cdiv(std::min<int64_t>(small_pool - 1, g.D), seg_e))
+                                      : cdiv(g.D, seg_e);
+  int64_t titems_n = n_tt_max * segs_max, eitems_n = n_er_max * esegs_max;
+  int64_t slots_n = (int64_t)g.R * std::max<int64_t>(segs_max * nsub, esegs_max);
+  const double bound_bytes = 8.0 * (titems_n + eitems_n) + (double)sizeof(Partial) * slots_n;
+  if (bound_bytes > (double)(1ll << 30) || getenv("FIC_PLAN_SYNC")) {
+    // bounds too loose (e.g. the exact matcher on a large image): read the counts
+    DevPlan hp;
+    FIC_CUDA(cudaMemcpyAsync(&hp, d_plan, sizeof(hp), cudaMemcpyDeviceToHost, s));
+    FIC_CUDA(cudaStreamSynchronize(s));
+    titems_n = hp.n_titems;
+    eitems_n = hp.n_eitems;
+    slots_n = hp.n_slots;
+  }
   pmark();  // 13
-
-  int2* titems = sc.get<int2>(tot.n_titems);
-  int2* eitems = sc.get<int2>(tot.n_eitems);
-  Partial* partials = sc.get<Partial>(tot.n_slots);
-  if (nsub > 1)  // tensor slots of pieces that never run stay invalid
-    FIC_CUDA(cudaMemsetAsync(partials, 0, tot.n_slots * sizeof(Partial), s));
-  if (n_tt) {
+  int2* titems = sc.get<int2>(titems_n);
+  int2* eitems = sc.get<int2>(eitems_n);
+  Partial* partials = sc.get<Partial>(slots_n);
+  if (n_tt_max) {
     // segment-major order: every tile's first segment runs before any second
     // segment, so later segments start from the thresholds the earlier ones found
-    k_items_segmajor<<<1, 1024, 0, s>>>(tnseg, n_tt, titems);
+    k_items_segmajor<<<1, 1024, 0, s>>>(tnseg, d_plan, titems);
     FIC_CHECK_LAUNCH();
   }
-  if (n_er) {
-    k_expand<<<(unsigned)cdiv(n_er, 128), 128, 0, s>>>(enseg, ebase, n_er, eitems);
-    FIC_CHECK_LAUNCH();
-  }
+  k_expand<<<(unsigned)cdiv(n_er_max, 128), 128, 0, s>>>(enseg, ebase, d_plan, eitems);
+  FIC_CHECK_LAUNCH();
 
   pmark();  // 14
   FIC_CUDA(cudaStreamWaitEvent(s, side.ev[2], 0));  // join: pool + ranges
   PoolView P{pa.raw, pa.bh, pa.inv_den, pa.sums, pa.ids, g.D};
   RangeView Rv{ra.info, ra.rows, pb.lo, pb.hi, g.n_iso, K};
   tm.mark();  // 3
-  if (tot.n_titems) {
+  if (n_tt_max && titems_n) {
     unsigned long long* thr_g = sc.get<unsigned long long>(g.R);
     k_fill_u64<<<(unsigned)cdiv(g.R, 256), 256, 0, s>>>(thr_g, 0x7ff0000000000000ull, g.R);
     FIC_CHECK_LAUNCH();
-    TcArgs ta{titems, tot.n_titems, rid_s + tb, n_tr, wlo, whi, seg_t, seg0, RT, sbase, partials,
+    TcArgs ta{titems, titems_n, rid_s, n_tt_max * RT, wlo, whi, seg_t, seg0, RT, sbase, partials,
               counters, counters + 15, thr_g, 0, nullptr};
     ta.nsub = nsub;
-    if (n_flat) {
+    ta.n_split = nsub > 1 ? std::min<int64_t>(titems_n, kSplitCap) : 0;  // bound
+    ta.plan = d_plan;
+    if (flat_path) {
       ta.flat_c = fl.flat_c;
       ta.flat_canon = fl.canon;
     }
-    ta.n_split = nsub > 1 ? std::min<int64_t>(tot.n_titems, 2 * 148) : 0;
     const char* dbg_env = getenv("FIC_TC_DEBUG");
     if (dbg_env && (atoi(dbg_env) & (32 | 8192))) {
       ta.dbg = sc.get<unsigned long long>(64 * 24);
@@ -1112,13 +1152,23 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
     }
   }
   tm.mark();  // 4
-  if (tot.n_eitems) {
-    ExactArgs ea{eitems, tot.n_eitems, rid_s + eb, seg_e, sbase, partials, counters};
+  if (eitems_n) {
+    ExactArgs ea{eitems, eitems_n, rid_s, seg_e, sbase, partials, counters, d_plan};
     launch_exact(P, Rv, ea, s);
   }
   tm.mark();  // 5
   MergeArgs ma{g.R, sbase, nslots, partials, records, pre_rms, post_rms, (double)K};
   launch_merge(ma, s);
+  tm.mark();  // 6
+
+  Readback hrb;
+  FIC_CUDA(cudaMemcpyAsync(&hrb, d_rb, sizeof(hrb), cudaMemcpyDeviceToHost, s));
+  tm.mark();  // 7
+  FIC_CUDA(cudaStreamSynchronize(s));
+  const unsigned long long* hc = hrb.counters;
+  const double* hs = hrb.scal;
+  const DevPlan& hp = hrb.plan;
+  const unsigned long long n_flat = flat_path ? hrb.flat[0] : 0;
   if (n_flat) {  // flat ranges on the canonical slab: one reduction per pixel value
     fl.lo = pb.lo;
     fl.hi = pb.hi;
@@ -1131,15 +1181,9 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
     fl.pre_rms = pre_rms;
     fl.post_rms = post_rms;
     launch_flat_match(P, fl, s);
+    FIC_CUDA(cudaEventRecord(tm.ev[23], s));  // end of the flat fix-up (event 23: not a plan mark)
+    FIC_CUDA(cudaStreamSynchronize(s));
   }
-  tm.mark();  // 6
-
-  unsigned long long hc[16];
-  double hs[4];
-  FIC_CUDA(cudaMemcpyAsync(hc, counters, sizeof(hc), cudaMemcpyDeviceToHost, s));
-  FIC_CUDA(cudaMemcpyAsync(hs, pb.scal, sizeof(hs), cudaMemcpyDeviceToHost, s));
-  tm.mark();  // 7
-  FIC_CUDA(cudaStreamSynchronize(s));
   if (ptime && pn == 15) {
     fprintf(stderr, "plan timing (ms): fd %.3f pool(side) %.3f | fork %.3f - %.3f classify..shard %.3f sync1 %.3f "
             "tiles..totals %.3f sync2 %.3f items %.3f | tensor %.3f exact %.3f merge %.3f readback %.3f | seed rounds %llu hit rounds %llu hit lanes %llu\n",
@@ -1164,13 +1208,13 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
     st->ms_match = tm.ms(3, 6);
     st->ms_tensor = tm.ms(3, 4);
     st->ms_exact = tm.ms(4, 5);
-    st->ms_total = tm.ms(0, 7);
+    st->ms_total = n_flat ? tm.ms(0, 23) : tm.ms(0, 7);
     st->exact_evals = (int64_t)hc[0];
     st->tensor_candidates = (int64_t)hc[1];
     st->tensor_comparisons = (int64_t)hc[3];
-    st->tensor_tiles = (int32_t)n_tt;
-    st->exact_tiles = (int32_t)n_er;
-    st->work_items = (int32_t)(tot.n_titems + tot.n_eitems);
+    st->tensor_tiles = (int32_t)hp.n_tt;
+    st->exact_tiles = (int32_t)hp.n_er;
+    st->work_items = (int32_t)(hp.n_titems + hp.n_eitems);
     st->kernel_launches = g_launches;
     if ((getenv("FIC_TC_DEBUG") && (atoi(getenv("FIC_TC_DEBUG")) & 4)) || getenv("FIC_TC_PROF"))
       fprintf(stderr, "tc cycles: producer-empty %.3g  mma-tempty %.3g  mma-full %.3g  epi-tfull %.3g  epi-slow %.3g  epi-total %.3g  mma-loop %.3g  setup %.3g  teardown(tma warp) %.3g  items %.0f\n",

@@ -6,6 +6,8 @@
 // fp64 op is an explicit round-to-nearest intrinsic (no FMA), so results are
 // bit-identical to numpy's.  Used for small pools (fallback ranges, nosearch)
 // and as the device-side oracle (FIC_MATCH_EXACT).
+#include <algorithm>
+
 #include "match.h"
 
 namespace fic {
@@ -52,10 +54,15 @@ __global__ void __launch_bounds__(256) k_exact(PoolView P, RangeView Rv, ExactAr
   constexpr int KW = K / 4;  // 32-bit words per row
   __shared__ uint32_t srow[8][KW];
   __shared__ Best sbest[8];
-  int64_t it = blockIdx.x;
-  if (it >= a.n_items) return;
+  int64_t n_items = a.n_items;
+  const uint32_t* elist = a.elist;
+  if (a.plan) {  // device-side work count (n_items is then a bound)
+    n_items = a.plan->n_eitems;
+    elist = a.elist + a.plan->eb;
+  }
+  for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
   int2 item = a.items[it];
-  uint32_t r = a.elist[item.x];
+  uint32_t r = elist[item.x];
   int64_t lo = Rv.lo[r], hi = Rv.hi[r];
   int64_t c0 = lo + (int64_t)item.y * a.seg_len;
   int64_t c1 = min(hi, c0 + a.seg_len);
@@ -118,6 +125,8 @@ __global__ void __launch_bounds__(256) k_exact(PoolView P, RangeView Rv, ExactAr
     out.valid = (c1 > c0) ? 1 : 0;
     a.partials[a.slot_base[r] + item.y] = out;
   }
+  __syncthreads();  // shared rows / bests are reused by the next item
+  }
 }
 
 // Generic K (any range size whose K is a multiple of 4, K <= 1024).
@@ -125,10 +134,15 @@ __global__ void __launch_bounds__(256) k_exact_generic(PoolView P, RangeView Rv,
   extern __shared__ uint32_t dyn[];
   __shared__ Best sbest[8];
   const int K = Rv.K, KW = K / 4;
-  int64_t it = blockIdx.x;
-  if (it >= a.n_items) return;
+  int64_t n_items = a.n_items;
+  const uint32_t* elist = a.elist;
+  if (a.plan) {  // device-side work count (n_items is then a bound)
+    n_items = a.plan->n_eitems;
+    elist = a.elist + a.plan->eb;
+  }
+  for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
   int2 item = a.items[it];
-  uint32_t r = a.elist[item.x];
+  uint32_t r = elist[item.x];
   int64_t lo = Rv.lo[r], hi = Rv.hi[r];
   int64_t c0 = lo + (int64_t)item.y * a.seg_len;
   int64_t c1 = min(hi, c0 + a.seg_len);
@@ -180,12 +194,16 @@ __global__ void __launch_bounds__(256) k_exact_generic(PoolView P, RangeView Rv,
     out.valid = (c1 > c0) ? 1 : 0;
     a.partials[a.slot_base[r] + item.y] = out;
   }
+  __syncthreads();  // shared rows / bests are reused by the next item
+  }
 }
 
 void launch_exact(const PoolView& P, const RangeView& Rv, const ExactArgs& a, cudaStream_t s) {
   if (a.n_items == 0) return;
   if (Rv.K % 4) invalid("range_size * range_size must be a multiple of 4 on the GPU path");
-  unsigned grid = (unsigned)a.n_items;
+  // one block per item; with a device-side count, a grid-stride loop over
+  // at most 4 blocks per SM
+  unsigned grid = (unsigned)(a.plan ? std::min<int64_t>(a.n_items, 148 * 4) : a.n_items);
   if (Rv.K == 64)
     k_exact<64><<<grid, 256, 0, s>>>(P, Rv, a);
   else if (Rv.K == 16)

@@ -424,8 +424,17 @@ __global__ void __maxnreg__(MAXREG)
   uint32_t kitem = 0;  // items this CTA started
   // virtual items: the last n_split items are each cut into nsub column
   // pieces (own partial slots), so the grid's last wave is short
-  const int64_t n_whole = a.n_items - a.n_split;
-  const int64_t n_virt = n_whole + a.n_split * a.nsub;
+  // work counts: from the device-side plan when there is one
+  int64_t n_items = a.n_items, n_tr = a.n_tr, n_split = a.n_split;
+  const uint32_t* tlist = a.tlist;
+  if (a.plan) {
+    n_items = a.plan->n_titems;
+    n_tr = a.plan->n_tr;
+    n_split = a.plan->n_split;
+    tlist = a.tlist + a.plan->tb;
+  }
+  const int64_t n_whole = n_items - n_split;
+  const int64_t n_virt = n_whole + n_split * a.nsub;
   auto item_cols = [&](int64_t v, int& tile, int& slot, int64_t& c0, int64_t& c1) {
     int64_t i = v;
     int sub = 0;
@@ -467,8 +476,8 @@ __global__ void __maxnreg__(MAXREG)
       const int64_t g = (int64_t)tile * a.RT + kt;
       uint32_t r = 0xffffffffu;
       int rho = 0;
-      if (kl < BM / n_iso && kt < a.RT && g < a.n_tr) {
-        r = __ldg(a.tlist + g);
+      if (kl < BM / n_iso && kt < a.RT && g < n_tr) {
+        r = __ldg(tlist + g);
         rho = Rv.info[r].rho;
       }
       s_rid[kl] = r;
@@ -808,10 +817,10 @@ __global__ void __maxnreg__(MAXREG)
         st.dom = 0xffffffffu;
         st.sq = st.oq = 0;
         st.iso = (uint8_t)(r + rbase - k * n_iso);
-        st.valid = (k < a.RT && g < a.n_tr) ? 1 : 0;
+        st.valid = (k < a.RT && g < n_tr) ? 1 : 0;
         st.sr = st.srr = 0.0;
         if (st.valid) {
-          const RangeInfo inf = Rv.info[a.tlist[g]];
+          const RangeInfo inf = Rv.info[tlist[g]];
           st.sr = inf.sr;
           st.srr = inf.srr;
         }
@@ -925,7 +934,10 @@ __global__ void __maxnreg__(MAXREG)
           out.sq = (uint8_t)sq;
           out.oq = (uint8_t)oq;
           out.valid = (dom != 0xffffffffu) ? 1 : 0;
-          a.partials[a.slot_base[a.tlist[g]] + slot] = out;
+          Partial* dst = a.partials + a.slot_base[tlist[g]] + slot;
+          *dst = out;
+          if (it < n_whole)  // a whole segment: its piece slots stay empty
+            for (int q = 1; q < a.nsub; ++q) dst[q].valid = 0;
         }
       }
     }

@@ -23,6 +23,16 @@ struct RangeView {
   int n_iso, K;
 };
 
+// Work counts of one encode, computed on the device by the planner
+// (k_plan_scans) and read by the matchers: the host enqueues everything
+// without waiting for them (its allocations use upper bounds).
+struct DevPlan {
+  int64_t tb, n_tr, n_tt;      // tensor ranges: first sorted position, count, tiles
+  int64_t eb, n_er;            // exact ranges: first sorted position, count
+  int64_t n_titems, n_eitems, n_slots;
+  int64_t n_split;             // tensor items run as pieces (tail splitting)
+};
+
 // Exact CUDA-core matcher: one work item = (range, segment of its slab).
 struct ExactArgs {
   const int2* items;           // (index into elist, segment)
@@ -32,6 +42,7 @@ struct ExactArgs {
   const int64_t* slot_base;    // [R]
   Partial* partials;
   unsigned long long* counters;  // [0] exact evaluations
+  const DevPlan* plan;         // non-null: n_items = plan->n_eitems, elist += plan->eb (n_items: bound)
 };
 void launch_exact(const PoolView& P, const RangeView& Rv, const ExactArgs& a,
                   cudaStream_t s);
@@ -62,6 +73,7 @@ struct TcArgs {
   // matched by the flat kernels (fic_flat.cu), not screened: nullptr = none
   const int16_t* flat_c;       // [R] pixel value of a flat range, -1 otherwise
   const uint32_t* flat_canon;  // [1] smallest flat range index (its slab is canonical)
+  const DevPlan* plan;         // non-null: n_items / n_tr / n_split / tlist offset from the device
 };
 
 // Flat ranges (every pixel equal to c): all isometries give the same row and

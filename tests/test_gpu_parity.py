@@ -190,6 +190,24 @@ def test_pool_row_segments_equal_box_planes(monkeypatch):
     assert torch.equal(a.post_rms, b.post_rms) and torch.equal(a.pre_rms, b.pre_rms)
 
 
+def test_plan_counts_read_back_equals_device_plan(monkeypatch):
+    """The planner's counts stay on the device (allocations use bounds);
+    FIC_PLAN_SYNC reads them back first and allocates exactly -- the path a
+    call with very loose bounds takes.  Same results, also for the exact
+    matcher and for a shard."""
+    import torch
+    img = torch.from_numpy(synth.CONFIGS["cfg2"].make()).cuda()
+    kw = dict(range_size=8, domain_size=16, stride=4, isometries=True, delta=0.1)
+    for extra in ({}, {"matcher": "exact"}, {"shard": (1, 3)}):
+        a = codec.encode_device(img, "dynamic_fd", **kw, **extra)
+        monkeypatch.setenv("FIC_PLAN_SYNC", "1")
+        b = codec.encode_device(img, "dynamic_fd", **kw, **extra)
+        monkeypatch.delenv("FIC_PLAN_SYNC")
+        assert torch.equal(a.records, b.records), extra
+        assert torch.equal(a.post_rms, b.post_rms) and torch.equal(a.pre_rms, b.pre_rms), extra
+        assert a.stats["work_items"] == b.stats["work_items"] > 0, extra
+
+
 def test_dbc_grid_known_answers():
     for side in (8, 16, 32):
         assert np.array_equal(codec.dbc_grid(FD[f"rand{side}.blocks"]), FD[f"rand{side}.fd"])
