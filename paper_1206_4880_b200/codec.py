@@ -158,9 +158,26 @@ def validate(image, strategy, range_size, domain_size, stride, fd_source):
     return image, int(height), int(width)
 
 
+_PARAMS: dict = {}
+
+
 def make_params(strategy, range_size, domain_size, stride, isometries, fd_source,
                 delta, matcher, shard, max_segment=0, small_pool=0):
-    """Fill the C ``fic_params_t`` (keeps numpy-side tables alive on it)."""
+    """The C ``fic_params_t`` for these arguments (cached: the library only
+    reads it, and it keeps the numpy-side tables alive)."""
+    key = (strategy, range_size, domain_size, stride, bool(isometries), fd_source, delta, matcher,
+           tuple(shard), max_segment, small_pool)
+    p = _PARAMS.get(key)
+    if p is None:
+        if len(_PARAMS) > 64:
+            _PARAMS.clear()
+        p = _PARAMS[key] = _make_params(strategy, range_size, domain_size, stride, isometries,
+                                        fd_source, delta, matcher, shard, max_segment, small_pool)
+    return p
+
+
+def _make_params(strategy, range_size, domain_size, stride, isometries, fd_source,
+                 delta, matcher, shard, max_segment=0, small_pool=0):
     if matcher not in MATCHERS:
         raise ValueError(f"unknown matcher {matcher!r}; use one of {tuple(MATCHERS)}")
     p = _lib.FicParams()
@@ -304,7 +321,7 @@ def encode(image, strategy: str = "dynamic_fd", *, range_size: int = 8,
             stage.h_img.numpy()[...] = image
             stage.d_img.copy_(stage.h_img, non_blocking=True)
             img_dev = stage.d_img
-        stage.d_out.zero_()
+        # (no clearing: a full encode writes every range's outputs)
         res = encode_device(img_dev, strategy, range_size=range_size, domain_size=domain_size,
                             stride=stride, isometries=isometries, fd_source=fd_source,
                             delta=delta, matcher=matcher, out=stage.result())

@@ -161,6 +161,7 @@ struct DbcTables {
   double* w = nullptr;
   double hw[7] = {};   // host copies: slope weights, max count increment per scale
   int hqmax[7] = {};
+  int qshift[7] = {-1, -1, -1, -1, -1, -1, -1};  // quotient table == v >> qshift (else -1)
   const std::vector<double>* hln = nullptr;  // host copy of the ln table (cached, never freed)
 };
 
@@ -200,6 +201,11 @@ static DbcTables make_dbc(Scratch& sc, cudaStream_t s, int side, const double* h
   for (int j = 0; j < t.J; ++j) {
     t.hw[j] = w[j];
     t.hqmax[j] = q[j * 256 + 255] - q[j * 256 + 0];
+    for (int sh = 0; sh < 8 && t.qshift[j] < 0; ++sh) {
+      bool ok = true;
+      for (int v = 0; v < 256 && ok; ++v) ok = q[j * 256 + v] == (v >> sh);
+      if (ok) t.qshift[j] = sh;
+    }
   }
   // the tables depend only on (device, side, ln values, weights): upload once
   // and keep them (a few KB per block side) instead of copying every call
@@ -722,6 +728,7 @@ static PlanBufs make_plan(Scratch& sc, cudaStream_t s, const uint8_t* img, const
     fa.ln = td.ln;
     fa.ln_len = td.ln_len;
     fa.w = td.w;
+    for (int j = 0; j < 7; ++j) fa.qshift[j] = td.qshift[j];
     fa.fd = pb.fd_dom;
     // compact-key path: enumerate the count combinations of the scales with
     // a nonzero weight (a zero weight adds +0.0 whatever the count)

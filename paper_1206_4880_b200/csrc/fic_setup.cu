@@ -145,7 +145,7 @@ __global__ void __launch_bounds__(256) k_fd(FdArgs a) {
 // per-cell count increments floor(max/h) - floor(min/h) are stored, and each
 // block's count is a strided sum of them, done separably (rows, then
 // columns).  Same integer counts as k_fd, hence the same FD bits.
-template <int T>
+template <int T, bool POW2>
 __global__ void __launch_bounds__(256) k_fd16_tile(FdArgs a) {
   extern __shared__ __align__(16) uint8_t sm[];
   __shared__ uint16_t quot[3][256];
@@ -175,45 +175,75 @@ __global__ void __launch_bounds__(256) k_fd16_tile(FdArgs a) {
   const int kx0 = blockIdx.x * T, ky0 = blockIdx.y * T;
   const int x0 = kx0 * st, y0 = ky0 * st;
   const int Himg = (int)((nby - 1) * st + 16), Wimg = a.W;
-  for (int i = threadIdx.x; i < PP; i += blockDim.x) {
-    const int y = i / PW, x = i - (i / PW) * PW;
-    const int gy = y0 + y, gx = x0 + x;
-    P[i] = (gy < Himg && gx < Wimg) ? __ldg(a.src + (int64_t)gy * Wimg + gx) : 0;
+  // 2-D loops: rows over warps, columns over lanes (no index division)
+  const int wp = threadIdx.x >> 5, ln = threadIdx.x & 31;
+  auto for_xy = [&](int ny, int nx, auto&& f) {
+    for (int y = wp; y < ny; y += 8)
+      for (int x = ln; x < nx; x += 32) f(y, x);
+  };
+  // floor(v / h_j): a shift when h_j is a power of two (side 16: 32, 64, 128)
+  const int sh0 = a.qshift[0], sh1 = a.qshift[1], sh2 = a.qshift[2];
+  auto qd = [&](int j, int mx, int mn) -> int {
+    if (POW2) {
+      const int sh = j == 0 ? sh0 : (j == 1 ? sh1 : sh2);
+      return (mx >> sh) - (mn >> sh);
+    }
+    return quot[j][mx] - quot[j][mn];
+  };
+  // the image patch as 4-byte words (x0 is a multiple of 32, W of 8; a word
+  // never straddles the right edge), every load issued before any store
+  {
+    const int pw4 = (PW + 3) >> 2, nw = PW * pw4;
+    constexpr int MAXW = 8;  // 76 x 19 words (stride 4) < 8 x 256
+    uint32_t v[MAXW];
+#pragma unroll
+    for (int q = 0; q < MAXW; ++q) {
+      const int i = (int)threadIdx.x + 256 * q;
+      const int y = i / pw4, xw = i - y * pw4;
+      const int gy = y0 + y, gx = x0 + 4 * xw;
+      v[q] = (i < nw && gy < Himg && gx < Wimg)
+                 ? __ldg(reinterpret_cast<const uint32_t*>(a.src + (int64_t)gy * Wimg + gx))
+                 : 0u;
+    }
+#pragma unroll
+    for (int q = 0; q < MAXW; ++q) {
+      const int i = (int)threadIdx.x + 256 * q;
+      if (i < nw) {
+        const int y = i / pw4, xw = i - y * pw4;
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+          if (4 * xw + b < PW) P[y * PW + 4 * xw + b] = (uint8_t)(v[q] >> (8 * b));
+      }
+    }
   }
   __syncthreads();
   // scale 2 cells at every patch position
-  for (int i = threadIdx.x; i < PP; i += blockDim.x) {
-    const int y = i / PW, x = i - (i / PW) * PW;
-    if (y < PW - 1 && x < PW - 1) {
-      const int p0 = P[i], p1 = P[i + 1], p2 = P[i + PW], p3 = P[i + PW + 1];
-      const int mx = max(max(p0, p1), max(p2, p3)), mn = min(min(p0, p1), min(p2, p3));
-      X2[i] = (uint8_t)mx;
-      N2[i] = (uint8_t)mn;
-      C2[i] = (uint8_t)(quot[0][mx] - quot[0][mn]);
-    }
-  }
+  for_xy(PW - 1, PW - 1, [&](int y, int x) {
+    const int i = y * PW + x;
+    const int p0 = P[i], p1 = P[i + 1], p2 = P[i + PW], p3 = P[i + PW + 1];
+    const int mx = max(max(p0, p1), max(p2, p3)), mn = min(min(p0, p1), min(p2, p3));
+    X2[i] = (uint8_t)mx;
+    N2[i] = (uint8_t)mn;
+    C2[i] = (uint8_t)qd(0, mx, mn);
+  });
   __syncthreads();
   // scale 4 from four scale-2 cells
-  for (int i = threadIdx.x; i < PP; i += blockDim.x) {
-    const int y = i / PW, x = i - (i / PW) * PW;
-    if (y < PW - 3 && x < PW - 3) {
-      const int mx = max(max(X2[i], X2[i + 2]), max(X2[i + 2 * PW], X2[i + 2 * PW + 2]));
-      const int mn = min(min(N2[i], N2[i + 2]), min(N2[i + 2 * PW], N2[i + 2 * PW + 2]));
-      X4[i] = (uint8_t)mx;
-      N4[i] = (uint8_t)mn;
-      C4[i] = (uint8_t)(quot[1][mx] - quot[1][mn]);
-    }
-  }
+  for_xy(PW - 3, PW - 3, [&](int y, int x) {
+    const int i = y * PW + x;
+    const int mx = max(max(X2[i], X2[i + 2]), max(X2[i + 2 * PW], X2[i + 2 * PW + 2]));
+    const int mn = min(min(N2[i], N2[i + 2]), min(N2[i + 2 * PW], N2[i + 2 * PW + 2]));
+    X4[i] = (uint8_t)mx;
+    N4[i] = (uint8_t)mn;
+    C4[i] = (uint8_t)qd(1, mx, mn);
+  });
   __syncthreads();
   // scale 8 from four scale-4 cells
-  for (int i = threadIdx.x; i < PP; i += blockDim.x) {
-    const int y = i / PW, x = i - (i / PW) * PW;
-    if (y < PW - 7 && x < PW - 7) {
-      const int mx = max(max(X4[i], X4[i + 4]), max(X4[i + 4 * PW], X4[i + 4 * PW + 4]));
-      const int mn = min(min(N4[i], N4[i + 4]), min(N4[i + 4 * PW], N4[i + 4 * PW + 4]));
-      C8[i] = (uint8_t)(quot[2][mx] - quot[2][mn]);
-    }
-  }
+  for_xy(PW - 7, PW - 7, [&](int y, int x) {
+    const int i = y * PW + x;
+    const int mx = max(max(X4[i], X4[i + 4]), max(X4[i + 4 * PW], X4[i + 4 * PW + 4]));
+    const int mn = min(min(N4[i], N4[i + 4]), min(N4[i + 4 * PW], N4[i + 4 * PW + 4]));
+    C8[i] = (uint8_t)qd(2, mx, mn);
+  });
   __syncthreads();
   // row sums over each block's cells: H_s[y][lx] = sum_j C_s[y][lx*st + s*j]
   for (int i = threadIdx.x; i < PW * T; i += blockDim.x) {
@@ -269,8 +299,14 @@ __global__ void __launch_bounds__(256) k_fd16_tile(FdArgs a) {
         const uint32_t r = __ldg(a.rank_of_combo + c);
         a.rank[b] = r;
         if (a.rank_hist) {
-          atomicAdd(hist + r, 1u);
-          atomicMin(minid + r, (uint32_t)b);
+          // neighbouring domains share ranks: one shared-memory update per
+          // group of equal ranks in the warp (ids increase with the lane, so
+          // the group's lowest lane holds its smallest id)
+          const unsigned grp = __match_any_sync(__activemask(), r);
+          if ((int)(threadIdx.x & 31) == __ffs(grp) - 1) {
+            atomicAdd(hist + r, (uint32_t)__popc(grp));
+            atomicMin(minid + r, (uint32_t)b);
+          }
         }
       } else {
         a.combo[b] = c;
@@ -338,25 +374,34 @@ void launch_fd(const FdArgs& a, cudaStream_t s) {
   int threads = 256;
   int64_t blocks = cdiv(a.n, threads);
   const bool tile_ok = a.mode == FD_IMAGE && a.side == 16 && a.J == 3 && a.smax == 8 &&
-                       a.bst >= 1 && a.bst <= 4 && !getenv("FIC_FD_DIRECT");
+                       a.bst >= 1 && a.bst <= 4 && (a.W & 3) == 0 && !getenv("FIC_FD_DIRECT");
   if (tile_ok) {
     const int64_t nby = a.n / a.nbx;
     const int nr = a.rank_hist ? a.n_rank : 0;
+    const bool pow2 = a.qshift[0] >= 0 && a.qshift[1] >= 0 && a.qshift[2] >= 0;
     static bool attr = false;
     if (!attr) {
       const int mx = (int)fd16_tile_smem(16, 4, kCountSortMaxRanks);
-      FIC_CUDA(cudaFuncSetAttribute(k_fd16_tile<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
-      FIC_CUDA(cudaFuncSetAttribute(k_fd16_tile<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+      FIC_CUDA(cudaFuncSetAttribute(k_fd16_tile<16, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+      FIC_CUDA(cudaFuncSetAttribute(k_fd16_tile<32, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+      FIC_CUDA(cudaFuncSetAttribute(k_fd16_tile<16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+      FIC_CUDA(cudaFuncSetAttribute(k_fd16_tile<32, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
       attr = true;
     }
     if (a.bst == 1) {
       constexpr int T = 32;
       dim3 grid((unsigned)cdiv(a.nbx, T), (unsigned)cdiv(nby, T));
-      k_fd16_tile<T><<<grid, 256, fd16_tile_smem(T, 1, nr), s>>>(a);
+      if (pow2)
+        k_fd16_tile<T, true><<<grid, 256, fd16_tile_smem(T, 1, nr), s>>>(a);
+      else
+        k_fd16_tile<T, false><<<grid, 256, fd16_tile_smem(T, 1, nr), s>>>(a);
     } else {
       constexpr int T = 16;
       dim3 grid((unsigned)cdiv(a.nbx, T), (unsigned)cdiv(nby, T));
-      k_fd16_tile<T><<<grid, 256, fd16_tile_smem(T, a.bst, nr), s>>>(a);
+      if (pow2)
+        k_fd16_tile<T, true><<<grid, 256, fd16_tile_smem(T, a.bst, nr), s>>>(a);
+      else
+        k_fd16_tile<T, false><<<grid, 256, fd16_tile_smem(T, a.bst, nr), s>>>(a);
     }
   } else if (a.smax == 4 && a.J == 2)
     k_fd<4><<<(unsigned)blocks, threads, 0, s>>>(a);

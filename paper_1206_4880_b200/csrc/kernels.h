@@ -28,6 +28,7 @@ struct FdArgs {
   const uint32_t* rank_of_combo;  // optional [C]: write rank_of_combo[combo] to `rank`
   uint32_t* rank;                 // [n] (with rank_of_combo; replaces combo)
   uint32_t* iota;                 // [n] optional: iota[b] = b (sort payload)
+  int qshift[7];                  // floor(v / h_j) == v >> qshift[j] for all v (else -1)
   uint32_t* rank_hist;            // optional [n_rank]: global histogram of `rank` (atomics)
   uint32_t* rank_minid;           // with rank_hist [n_rank]: smallest block index per rank
   int n_rank;
