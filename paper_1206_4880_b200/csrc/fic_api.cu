@@ -530,14 +530,6 @@ __global__ void __launch_bounds__(1024) k_plan_scans(const int32_t* tnseg, int32
   }
 }
 
-__global__ void k_totals(const int32_t* tnseg, const int32_t* tbase, int64_t ntt,
-                         const int32_t* enseg, const int32_t* ebase, int64_t ner,
-                         const int32_t* nslots, const int64_t* sbase, int R, Totals* out) {
-  if (threadIdx.x || blockIdx.x) return;
-  out->n_titems = ntt ? (int64_t)tbase[ntt - 1] + tnseg[ntt - 1] : 0;
-  out->n_eitems = ner ? (int64_t)ebase[ner - 1] + enseg[ner - 1] : 0;
-  out->n_slots = R ? sbase[R - 1] + nslots[R - 1] : 0;
-}
 
 __global__ void k_expand(const int32_t* nseg, const int32_t* base, const DevPlan* dp, int2* items) {
   int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
