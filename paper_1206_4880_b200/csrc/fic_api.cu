@@ -465,10 +465,6 @@ __global__ void k_exact_segs(const unsigned long long* key, const uint32_t* rid,
   nslots[rid[eb + i]] = ns;
 }
 
-struct Totals {
-  int64_t n_titems, n_eitems, n_slots;
-};
-
 // Exclusive scans of the per-tile and per-exact-range segment counts and of
 // the per-range slot counts (int64), plus their totals, in one block.
 template <class T, class U>
