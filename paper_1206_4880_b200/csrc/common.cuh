@@ -108,7 +108,14 @@ __device__ __forceinline__ Cand eval_candidate(double cross, double sd, double s
   s = fmin(fmax(s, -1.0), 1.0);
   double o = __dmul_rn(s, sd);
   o = __dsub_rn(sr, o);
-  o = __ddiv_rn(o, n);
+  // o / n: for n a power of two (K = 16, 64, ...) the quotient is the exact
+  // scaling o * 2^-k, so the multiply gives the division's bits without its
+  // long Newton sequence
+  const unsigned long long nb = (unsigned long long)__double_as_longlong(n);
+  if ((nb & 0x000fffffffffffffull) == 0)
+    o = __dmul_rn(o, __longlong_as_double((long long)((2046ull - (nb >> 52)) << 52)));
+  else
+    o = __ddiv_rn(o, n);
   c.pre = sq_err(s, o, sd, sdd, cross, sr, srr, n);
   o = fmin(fmax(o, -255.0), 255.0);
   double sq = rint(__dmul_rn(__dadd_rn(s, 1.0), 15.5));
