@@ -108,6 +108,7 @@ typedef struct fic_stats {
   int64_t tensor_comparisons; /* useful candidates of tensor-path ranges: sum(pool) * n_iso */
   int32_t tensor_tiles, exact_tiles, work_items;
   int32_t kernel_launches;   /* kernels this call launched (library-internal CUB passes excluded) */
+  double ms_pool_main;       /* device time of the pool builder's main kernel (k_pool) alone */
 } fic_stats_t;
 
 /* Replaces fic.codec.encode (codec.py:290-427) for one image already in

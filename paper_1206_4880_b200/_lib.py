@@ -63,6 +63,7 @@ class FicStats(ctypes.Structure):
         ("exact_tiles", ctypes.c_int32),
         ("work_items", ctypes.c_int32),
         ("kernel_launches", ctypes.c_int32),
+        ("ms_pool_main", ctypes.c_double),
     ]
 
     def as_dict(self) -> dict:

@@ -88,7 +88,7 @@ struct Timer {
 // the caller's stream; event-ordered both ways.
 struct SideStream {
   cudaStream_t s2 = nullptr;
-  cudaEvent_t ev[6] = {};  // 0 fork (after ranges alloc), 1 fork (order ready), 2 join, 3..4 pool timing
+  cudaEvent_t ev[6] = {};  // 0 fork (after ranges alloc), 1 fork (order ready), 2 join, 3..5 pool timing
   static SideStream& get() {
     static thread_local std::map<int, SideStream> m;
     int dev = 0;
@@ -964,11 +964,16 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
   pa.inv_den = sc.get<double>(g.D);
   pa.sums = sc.get<uint2>(g.D);
   pa.ids = sc.get<uint32_t>(g.D);
+  // FIC_POOL_SERIAL: the pool builder on the caller's stream (a measurement
+  // of K1 without the planning kernels running beside it)
+  const bool pool_serial = getenv("FIC_POOL_SERIAL") != nullptr;
+  cudaStream_t ps = pool_serial ? s : side.s2;
+  pa.ev_main = side.ev[5];
   FIC_CUDA(cudaEventRecord(side.ev[1], s));
   FIC_CUDA(cudaStreamWaitEvent(side.s2, side.ev[1], 0));
-  FIC_CUDA(cudaEventRecord(side.ev[3], side.s2));
-  launch_pool(pa, side.s2);
-  FIC_CUDA(cudaEventRecord(side.ev[4], side.s2));
+  FIC_CUDA(cudaEventRecord(side.ev[3], ps));
+  launch_pool(pa, ps);
+  FIC_CUDA(cudaEventRecord(side.ev[4], ps));
   FIC_CUDA(cudaEventRecord(side.ev[2], side.s2));
   tm.mark();  // 2
   pmark();  // 8
@@ -1199,6 +1204,9 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
       float t = 0;
       cudaEventElapsedTime(&t, side.ev[3], side.ev[4]);
       st->ms_pool = t;
+      t = 0;
+      cudaEventElapsedTime(&t, side.ev[5], side.ev[4]);
+      st->ms_pool_main = t;
     }
     st->ms_match = tm.ms(3, 6);
     st->ms_tensor = tm.ms(3, 4);

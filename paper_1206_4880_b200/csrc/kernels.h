@@ -93,6 +93,7 @@ struct PoolArgs {
   double* inv_den;         // [D]
   uint2* sums;             // [D] (sum_d, sum_dd)
   uint32_t* ids;           // [D] raster id per pool position (copy of order)
+  cudaEvent_t ev_main;     // optional: recorded just before the main kernel (k_pool)
 };
 void launch_pool(const PoolArgs& a, cudaStream_t s);
 
