@@ -854,6 +854,25 @@ static int guarded(F f) {
 // ---------------------------------------------------------------------------
 // encode
 // ---------------------------------------------------------------------------
+// Inverse isometry tables (blocks.py:113-139) on the device, built and
+// uploaded once per (device, range size): a per-call pageable copy would make
+// the host wait for the work already queued on the stream.
+static const int* iso_inverse_table(int dev, int rs) {
+  static std::mutex mu;
+  static std::map<std::pair<int, int>, int*> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find({dev, rs});
+  if (it != cache.end()) return it->second;
+  const int K = rs * rs;
+  std::vector<int> perm(8 * K), inv(8 * K);
+  iso_tables(rs, perm.data(), inv.data());
+  int* d = nullptr;
+  FIC_CUDA(cudaMalloc(&d, 8 * K * sizeof(int)));
+  FIC_CUDA(cudaMemcpy(d, inv.data(), 8 * K * sizeof(int), cudaMemcpyHostToDevice));
+  cache.emplace(std::make_pair(dev, rs), d);
+  return d;
+}
+
 static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p, uint8_t* records,
                         double* pre_rms, double* post_rms, int64_t* pool_sizes,
                         fic_stats_t* st, cudaStream_t s) {
@@ -888,6 +907,8 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
   };
   tm.mark();  // 0
   SideStream& side = SideStream::get();
+  int dev_id = 0;
+  FIC_CUDA(cudaGetDevice(&dev_id));
 
   // flat ranges (fic_flat.cu): detected up front, counted at the first sync
   FlatArgs fl{};
@@ -918,10 +939,7 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
   }
 
   // ranges (side stream: needs only the image)
-  std::vector<int> perm(8 * K), inv(8 * K);
-  iso_tables(g.rs, perm.data(), inv.data());
-  int* d_inv = sc.get<int>(8 * K);
-  FIC_CUDA(cudaMemcpyAsync(d_inv, inv.data(), 8 * K * sizeof(int), cudaMemcpyHostToDevice, s));
+  const int* d_inv = iso_inverse_table(dev_id, g.rs);
   RangeArgs ra{};
   ra.img = img;
   ra.W = g.W;
