@@ -231,8 +231,9 @@ def _pool_roofline(stats, peak_gbs, src, serial_stats=None):
     written (raw K u8, fp16 B row 2K, inv_den 8, sums 8, ids 4), over its
     device time in the timed steps (CUDA events on the side stream it runs on,
     next to the planning kernels).  `isolated` repeats the measurement with
-    the pool builder on the main stream (FIC_POOL_SERIAL, untimed encodes);
-    `k1_ms` is the whole pool builder (row segments + k_pool)."""
+    the pool builder alone on the main stream (FIC_POOL_SERIAL, untimed
+    encodes); `k1_ms` is the whole pool builder (row segments + k_pool) in
+    the timed steps."""
     D, K = 1009 * 1009, 64
     nbytes = D * (4 + 3 * K + 20)
     ms = float(np.mean([s["ms_pool_main"] for s in stats]))
