@@ -987,7 +987,6 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
   const bool pool_serial = getenv("FIC_POOL_SERIAL") != nullptr;
   cudaStream_t ps = pool_serial ? s : side.s2;
   pa.ev_main = side.ev[5];
-  pa.full_grid = pool_serial ? 1 : 0;
   FIC_CUDA(cudaEventRecord(side.ev[1], s));
   FIC_CUDA(cudaStreamWaitEvent(side.s2, side.ev[1], 0));
   FIC_CUDA(cudaEventRecord(side.ev[3], ps));

@@ -859,11 +859,8 @@ __global__ void __launch_bounds__(256, 8) k_pool(PoolArgs a) {
   constexpr int DPI = 32 / RS;  // domains per instruction
   constexpr int NIT = RS;       // instructions per 32 domains
   const int lane = threadIdx.x & 31;
-  // grid-stride over 32-domain chunks: the grid may be capped (k_pool then
-  // leaves SM slots to the planning kernels running beside it)
-  const int64_t pstride = (int64_t)gridDim.x * (blockDim.x >> 5) * 32;
-  for (int64_t p0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; p0 < a.D;
-       p0 += pstride) {
+  const int64_t p0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32;
+  if (p0 >= a.D) return;
   const int g = lane / RS, i = lane % RS;
   const uint32_t D = (uint32_t)a.D;
   // lane j locates domain p0 + j once: byte offset of its first decimated row
@@ -941,7 +938,6 @@ __global__ void __launch_bounds__(256, 8) k_pool(PoolArgs a) {
     a.sums[pm] = make_uint2(my_sd, my_sdd);
     a.ids[pm] = my_id;
   }
-  }
 }
 
 __global__ void k_pool_generic(PoolArgs a, int rs) {
@@ -969,14 +965,6 @@ __global__ void k_pool_generic(PoolArgs a, int rs) {
 void launch_pool(const PoolArgs& a, cudaStream_t s) {
   if (a.D == 0) return;
   unsigned blocks = (unsigned)cdiv(a.D, 256);
-  // k_pool's grid: one block per 256 domains by default.  FIC_POOL_BLOCKS
-  // caps it (grid-stride): at 4 blocks per SM the planning kernels beside it
-  // are not queued behind it and reach the matcher ~35 us earlier at cfg3,
-  // but k_pool itself then runs at ~0.57 instead of ~0.72 of HBM bandwidth.
-  static int pool_cap = -1;
-  if (pool_cap < 0) pool_cap = getenv("FIC_POOL_BLOCKS") ? atoi(getenv("FIC_POOL_BLOCKS")) : 0;
-  const unsigned pool_blocks =
-      (pool_cap > 0 && !a.full_grid) ? std::min<unsigned>(blocks, (unsigned)pool_cap) : blocks;
   if (a.rs == 8 && a.trows) {
     const int pw = (DR_COLS - 1) * a.st + 16;
     const size_t smem = (size_t)(DR_ROWS + 1) * (((pw + 3) & ~3) + 4) + 16;
@@ -990,16 +978,16 @@ void launch_pool(const PoolArgs& a, cudaStream_t s) {
     k_domrows<<<grid, 256, smem, s>>>(a.img, a.H, a.W, a.st, a.ndx, a.mh, a.trows);
     FIC_CHECK_LAUNCH();
     if (a.ev_main) FIC_CUDA(cudaEventRecord(a.ev_main, s));
-    k_pool<8><<<pool_blocks, 256, 0, s>>>(a);
+    k_pool<8><<<blocks, 256, 0, s>>>(a);
   } else if ((a.rs == 8 || a.rs == 4) && a.planes) {
     const int64_t n = (int64_t)(a.H - 1) * (a.W - 1);
     k_boxplanes<<<(unsigned)cdiv(n, 256), 256, 0, s>>>(a.img, a.H, a.W, a.pitch, a.planes);
     FIC_CHECK_LAUNCH();
     if (a.ev_main) FIC_CUDA(cudaEventRecord(a.ev_main, s));
     if (a.rs == 8)
-      k_pool<8><<<pool_blocks, 256, 0, s>>>(a);
+      k_pool<8><<<blocks, 256, 0, s>>>(a);
     else
-      k_pool<4><<<pool_blocks, 256, 0, s>>>(a);
+      k_pool<4><<<blocks, 256, 0, s>>>(a);
   } else {
     if (a.ev_main) FIC_CUDA(cudaEventRecord(a.ev_main, s));
     k_pool_generic<<<blocks, 256, 0, s>>>(a, a.rs);

@@ -94,7 +94,6 @@ struct PoolArgs {
   uint2* sums;             // [D] (sum_d, sum_dd)
   uint32_t* ids;           // [D] raster id per pool position (copy of order)
   cudaEvent_t ev_main;     // optional: recorded just before the main kernel (k_pool)
-  int full_grid;           // 1: one k_pool block per 256 domains (nothing runs beside it)
 };
 void launch_pool(const PoolArgs& a, cudaStream_t s);
 
