@@ -182,3 +182,37 @@ def test_write_csv_and_pgm(tmp_path):
     assert runs.fidelity_psnr(img, img) == float("inf")
     with pytest.raises(ValueError, match="dimension mismatch"):
         runs.fidelity_psnr(img, img[:2])
+
+
+def test_bench_pool_roofline_arithmetic():
+    """bench.py's HBM roofline of k_pool: algorithmic bytes per domain
+    (4 B read + 3K + 20 B written) over the mean device time of the steps."""
+    import bench
+    stats = [{"ms_pool_main": 0.05, "ms_pool": 0.06}, {"ms_pool_main": 0.05, "ms_pool": 0.06}]
+    r = bench._pool_roofline(stats, 6552.3, "measured", serial_stats=[{"ms_pool_main": 0.04}])
+    d = 1009 * 1009
+    assert r["algorithmic_bytes_per_launch"] == d * (4 + 3 * 64 + 20)
+    assert abs(r["achieved"] - r["algorithmic_bytes_per_launch"] / 0.05e-3 / 1e9) < 1e-6
+    assert abs(r["frac"] - r["achieved"] / 6552.3) < 1e-12
+    assert r["bound"] == "hbm" and r["isolated"]["ms_per_launch"] == 0.04
+
+
+def test_bench_clock_summary_from_nvidia_smi_lines():
+    """The clock sampler's nvidia-smi fallback: median SM clock, max clock,
+    and the throttle reasons that were active in any sample."""
+    import bench
+    c = bench.Clocks(0)
+    c.lines = ["1965, 1965, 700.1, 0x0, Not Active, Not Active, Not Active, Not Active",
+               "1800, 1965, 990.0, 0x4, Not Active, Not Active, Not Active, Active",
+               "1900, 1965, 950.0, 0x0, Not Active, Not Active, Not Active, Not Active"]
+    s = c.summary()
+    assert s["sm_mhz"] == 1900.0 and s["sm_max_mhz"] == 1965.0 and s["samples"] == 3
+    assert s["reasons"] == ["sw_power_cap"]
+
+
+def test_params_are_cached_per_argument_tuple():
+    p1 = codec.make_params("dynamic_fd", 8, 16, 1, True, "original", 0.05, "auto", (0, 1))
+    p2 = codec.make_params("dynamic_fd", 8, 16, 1, True, "original", 0.05, "auto", (0, 1))
+    p3 = codec.make_params("dynamic_fd", 8, 16, 2, True, "original", 0.05, "auto", (0, 1))
+    assert p1 is p2 and p1 is not p3
+    assert p3.stride == 2 and p1.stride == 1
