@@ -7,11 +7,14 @@ windows, pool build, matching, records).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-N > 1 runs under torchrun, one rank per GPU: ranges are sharded (FD-sorted,
-cost-balanced) and records all-gathered over NCCL.  Rank 0 prints one JSON
-line.  ``--impl reference`` times the CPU oracle port of the reference
-algorithm on this host's cores (the reference package is pure Python and
-cannot travel to the GPU box).
+N > 1 runs one rank per GPU (re-executing itself under
+``torch.distributed.run`` when started without WORLD_SIZE): ranges are
+sharded (FD-sorted, cost-balanced, the same cut on every rank) and each
+rank's own records all-gathered over NCCL.  Rank 0 prints one JSON line.
+
+``--impl reference`` times the reference's own encoder (the unmodified
+package installed in baseline/_ref, oracle/ref_harness.py) on this host's
+cores; the oracle port stands in only when baseline/_ref is absent.
 """
 
 from __future__ import annotations
@@ -154,58 +157,129 @@ def _traffic_from_profile():
         return None
 
 
-def cpu_baseline(img, n_ranges=4, seed=123):
+def _port_rate(img, n_ranges=4, seed=123):
     """Oracle port of the reference matcher (codec.py:184-264) on a seeded
-    range subset, single BLAS thread; returns (matches/s, sample text)."""
+    range subset, one BLAS thread: (matches/s, setup s, sample text)."""
     from oracle import fic_oracle as orc
     try:
         from threadpoolctl import threadpool_limits
     except Exception:  # pragma: no cover
         threadpool_limits = None
+    t0 = time.perf_counter()
     r_blk = orc.range_blocks(img, 8)
     d_blk = orc.domain_blocks(img, 16, 1)
     d_dec = orc.decimate(d_blk)
     plan = orc.plan_pools(img, "dynamic_fd", 8, 16, 1, "original", CFG["delta"], r_blk, d_blk, d_dec)
     r_mat = r_blk.reshape(len(r_blk), -1).astype(np.float64)
     d_mat = d_dec.reshape(len(d_dec), -1).astype(np.float64)
+    setup_s = time.perf_counter() - t0
     ids = np.sort(np.random.default_rng(seed).choice(len(r_blk), n_ranges, replace=False))
     ctx = threadpool_limits(1) if threadpool_limits else None
     t0 = time.perf_counter()
     orc.match(r_mat, d_mat, plan, True, ids)
     dt = time.perf_counter() - t0
-    if ctx is not None:
-        ctx.unregister() if hasattr(ctx, "unregister") else None
+    if ctx is not None and hasattr(ctx, "unregister"):
+        ctx.unregister()
     matches = int((plan.hi[ids] - plan.lo[ids]).sum()) * 8
-    return matches / dt, (f"cfg3 oracle port, {n_ranges} seeded ranges (default_rng({seed})), "
-                          f"{matches} matches in {dt:.2f}s, 1 thread; setup excluded")
+    return matches / dt, setup_s, (f"oracle port (numpy, 8 isometries per matmul), {n_ranges} "
+                                   f"seeded cfg3 ranges, {matches} matches in {dt:.2f}s, 1 thread")
+
+
+def _ref_setup(img):
+    from oracle import ref_harness as rh
+    return rh.setup(img, "dynamic_fd", range_size=8, domain_size=16, stride=1, isometries=True,
+                    delta=CFG["delta"])
+
+
+def cpu_baseline(img, n_ranges=4, seed=123):
+    """The reference's own encoder on this host (baseline/_ref: its setup,
+    then its ``_search_chunk`` on a seeded range subset, workers=1), beside
+    the oracle port; bounded to ~15-30 s.  Returns the cpu_baseline object."""
+    from oracle import ref_harness as rh
+    port, port_setup, port_sample = _port_rate(img, n_ranges, seed)
+    comps = None
+    if rh.available():
+        ctx, r_matrix, setup_s = _ref_setup(img)
+        ids = np.sort(np.random.default_rng(seed).choice(r_matrix.shape[0], n_ranges,
+                                                         replace=False))
+        t0 = time.perf_counter()
+        rh.search(ctx, r_matrix, ids, workers=1)
+        dt = time.perf_counter() - t0
+        matches = int((ctx.slab_hi[ids] - ctx.slab_lo[ids]).sum()) * 8
+        comps = int((ctx.slab_hi - ctx.slab_lo).sum()) * 8
+        v, kind = matches / dt, "reference"
+        sample = (f"reference fic.codec._search_chunk (baseline/_ref), {n_ranges} seeded cfg3 "
+                  f"ranges (default_rng({seed})), {matches} matches in {dt:.2f}s, workers=1; "
+                  f"reference setup (codec.py:324-376) {setup_s:.1f}s, timed separately")
+    else:
+        v, kind, setup_s, sample = port, "port", port_setup, port_sample
+    out = {"value": v, "unit": UNIT, "cores": 1, "kind": kind, "sample": sample,
+           "cpu_model": rh.cpu_model(), "host_cores": os.cpu_count(), "setup_s": setup_s,
+           "port": {"value": port, "sample": port_sample, "setup_s": port_setup}}
+    if comps:
+        out["extrapolated_encode_s"] = setup_s + comps / v
+    return out
 
 
 def run_reference(args):
-    """--impl reference: the oracle port on all host cores, rank 0 only."""
+    """--impl reference: the reference's own encoder (baseline/_ref; the
+    oracle port when it is not installed) on this host's cores, rank 0 only.
+
+    Setup (codec.py:324-376) is timed once; the reference's threading is
+    GIL-bound, so ``workers`` in {1, 2, 4, ncores} is swept on a short sample
+    and the best is used for the timed steps, each `_search_chunk` over a
+    seeded subset of cfg3 ranges.  ``value`` is the matcher's matches/s;
+    ``e2e`` extrapolates a whole cfg3 encode (setup + all comparisons at
+    that rate), the figure comparable to our arm's end-to-end encode."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    from concurrent.futures import ThreadPoolExecutor
-
-    from oracle import fic_oracle as orc
+    from oracle import ref_harness as rh
     from paper_1206_4880_b200 import synth
     img = synth.cfg3_image()
-    r_blk = orc.range_blocks(img, 8)
-    d_blk = orc.domain_blocks(img, 16, 1)
-    d_dec = orc.decimate(d_blk)
-    plan = orc.plan_pools(img, "dynamic_fd", 8, 16, 1, "original", CFG["delta"], r_blk, d_blk, d_dec)
-    r_mat = r_blk.reshape(len(r_blk), -1).astype(np.float64)
-    d_mat = d_dec.reshape(len(d_dec), -1).astype(np.float64)
     cores = os.cpu_count() or 1
     rng = np.random.default_rng(7)
-    per_step = max(1, min(cores, 8))
+    per_step = 8
+    if rh.available():
+        kind = "reference"
+        ctx, r_matrix, setup_s = _ref_setup(img)
+        lo, hi = ctx.slab_lo, ctx.slab_hi
+
+        def run(ids, w):
+            rh.search(ctx, r_matrix, ids, workers=w)
+    else:  # pragma: no cover - the port when baseline/_ref is absent
+        from oracle import fic_oracle as orc
+        kind = "port"
+        t0 = time.perf_counter()
+        r_blk = orc.range_blocks(img, 8)
+        d_blk = orc.domain_blocks(img, 16, 1)
+        d_dec = orc.decimate(d_blk)
+        plan = orc.plan_pools(img, "dynamic_fd", 8, 16, 1, "original", CFG["delta"], r_blk,
+                              d_blk, d_dec)
+        r_mat = r_blk.reshape(len(r_blk), -1).astype(np.float64)
+        d_mat = d_dec.reshape(len(d_dec), -1).astype(np.float64)
+        setup_s = time.perf_counter() - t0
+        lo, hi = plan.lo, plan.hi
+
+        def run(ids, w):
+            from concurrent.futures import ThreadPoolExecutor
+            chunks = [c for c in np.array_split(ids, w * 4) if len(c)]
+            with ThreadPoolExecutor(max_workers=w) as ex:
+                list(ex.map(lambda c: orc.match(r_mat, d_mat, plan, True, c), chunks))
+    n_r = len(lo)
+    comps = int((hi - lo).sum()) * 8
+    sweep = {}
+    for w in sorted({1, 2, 4, cores}):
+        ids = np.sort(rng.choice(n_r, per_step, replace=False))
+        t0 = time.perf_counter()
+        run(ids, w)
+        sweep[w] = int((hi[ids] - lo[ids]).sum()) * 8 / (time.perf_counter() - t0)
+    best = max(sweep, key=sweep.get)
 
     def step():
-        ids = np.sort(rng.choice(len(r_blk), per_step, replace=False))
-        chunks = np.array_split(ids, min(cores, len(ids)))
-        with ThreadPoolExecutor(max_workers=cores) as ex:
-            list(ex.map(lambda c: orc.match(r_mat, d_mat, plan, True, c), chunks))
-        return int((plan.hi[ids] - plan.lo[ids]).sum()) * 8
+        ids = np.sort(rng.choice(n_r, per_step, replace=False))
+        run(ids, best)
+        return int((hi[ids] - lo[ids]).sum()) * 8
 
     for _ in range(args.warmup):
         step()
@@ -214,14 +288,20 @@ def run_reference(args):
         tot += step()
     dt = time.perf_counter() - t0
     v = tot / dt
+    enc_s = setup_s + comps / v
+    sample = (f"{kind}: codec._search_chunk on {per_step} seeded cfg3 ranges per step, "
+              f"workers={best} (best of {sorted(sweep)}); setup {setup_s:.1f}s timed once")
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": dict(CONFIG, sample=f"{per_step} seeded ranges/step"),
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
-                             "sample": f"oracle port of codec._search_chunk, {per_step} seeded "
-                                       f"cfg3 ranges per step over {cores} threads; setup excluded"},
-            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": best, "kind": kind,
+                             "sample": sample, "cpu_model": rh.cpu_model(), "host_cores": cores,
+                             "workers_sweep": {str(k): x for k, x in sweep.items()},
+                             "setup_s": setup_s},
+            "e2e": {"value": comps / enc_s, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0, "encode_s_extrapolated": enc_s,
+                    "note": "whole cfg3 encode extrapolated: setup + comparisons / value"}}
     print(json.dumps(line), flush=True)
 
 
@@ -260,6 +340,8 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -355,12 +437,24 @@ def run_ours(args):
                                                   "tensor_tiles", "exact_tiles", "work_items")},
     }
     if world == 1 and not args.no_cpu_baseline:
-        v, sample = cpu_baseline(img)
-        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": 1, "kind": "port",
-                                "sample": sample}
+        line["cpu_baseline"] = cpu_baseline(img)
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def _relaunch(args) -> int:
+    """``--gpus N`` without a torchrun environment: run this script under
+    torch.distributed.run with N local ranks (127.0.0.1 rendezvous)."""
+    import socket
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -371,6 +465,8 @@ def main():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    if args.impl == "ours" and args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(_relaunch(args))
     if args.impl == "reference":
         run_reference(args)
     else:

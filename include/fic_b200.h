@@ -146,6 +146,16 @@ int fic_decode_v1(const uint8_t* d_records, int32_t height, int32_t width,
                   int32_t iterations, double initial, const uint8_t* d_initial,
                   uint8_t* d_out, void* stream);
 
+/* One pass of fic.codec.decode_iterates (codec.py:534-598): d_dst[h*w] =
+ * the next float64 iterate computed from d_src[h*w]; d_out (optional, h*w
+ * uint8) receives rint(d_dst), the snapshot decode_iterates yields.
+ * Isometry bytes > 7 keep the identity as in the reference; records are not
+ * re-validated here (fic_decode_v1 / the Python layer do that first), an
+ * out-of-geometry domain index reads domain 0 instead of faulting. */
+int fic_decode_step_v1(const uint8_t* d_records, int32_t height, int32_t width,
+                       int32_t range_size, int32_t domain_size, int32_t stride,
+                       const double* d_src, double* d_dst, uint8_t* d_out, void* stream);
+
 const char* fic_last_error(void);
 int fic_abi_version(void);
 /* Releases cached device workspaces of the calling thread's current device. */

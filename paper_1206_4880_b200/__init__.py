@@ -1,8 +1,9 @@
 """B200-native fractal-image encoder hot path (arXiv 1206.4880), see DESIGN.md.
 
 Public names mirror the reference package ``fic`` for the rebuilt path:
-``encode``, ``decode``, ``serialize``, ``deserialize``, ``FractalCode``,
-``EncodeStats``, ``FormatError``, ``RECORD_DTYPE``, ``dbc_grid``.
+``encode``, ``decode``, ``decode_iterates``, ``serialize``, ``deserialize``,
+``FractalCode``, ``EncodeStats``, ``FormatError``, ``RECORD_DTYPE``,
+``dbc_grid``, ``fit_transform``, ``quantize_so``, ``dequantize_so``.
 """
 
 from .codec import (  # noqa: F401
@@ -14,10 +15,14 @@ from .codec import (  # noqa: F401
     FractalCode,
     dbc_grid,
     decode,
+    decode_iterates,
+    dequantize_so,
     deserialize,
     encode,
     encode_device,
+    fit_transform,
     plan,
+    quantize_so,
     serialize,
 )
 

@@ -318,7 +318,9 @@ def encode(image, strategy: str = "dynamic_fd", *, range_size: int = 8,
             img_dev = image
         else:
             # host image -> pinned staging -> device (one async copy)
-            stage.h_img.copy_(torch.from_numpy(image))  # (faster than a numpy assignment)
+            # (a torch copy is faster than a numpy assignment; negative-stride
+            # views such as np.flipud(img) are made contiguous first)
+            stage.h_img.copy_(torch.from_numpy(np.ascontiguousarray(image)))
             stage.d_img.copy_(stage.h_img, non_blocking=True)
             img_dev = stage.d_img
         # (no clearing: a full encode writes every range's outputs)
@@ -386,8 +388,9 @@ def deserialize(data: bytes) -> FractalCode:
 # decode (codec.py:516-598) on the GPU
 # ---------------------------------------------------------------------------
 
-def decode(code: FractalCode, iterations: int = 10, initial=None) -> np.ndarray:
-    """Iterate the stored transforms from a gray level (128) or an image."""
+def _decode_setup(code: FractalCode, iterations: int, initial):
+    """decode_iterates' validation (codec.py:541-556, reference texts and
+    order) and the device buffers: records, the float64 work image."""
     if iterations < 1:
         raise ValueError("iterations must be >= 1")
     torch = _torch()
@@ -397,25 +400,105 @@ def decode(code: FractalCode, iterations: int = 10, initial=None) -> np.ndarray:
         raise FormatError("record-count mismatch: records vs geometry")
     if code.records["domain"].size and int(code.records["domain"].max()) >= n_dom:
         raise ValueError("record references a domain outside the current image geometry")
-    init_dev = None
-    level = 128.0
-    if initial is not None:
-        if np.ndim(initial) == 0:
-            level = float(initial)
-        else:
-            arr = np.asarray(initial)
-            if arr.shape != (h, w):
-                raise ValueError("initial image does not match the encoded geometry")
-            init_dev = torch.from_numpy(np.ascontiguousarray(arr.astype(np.uint8))).cuda()
-    rec = torch.from_numpy(np.ascontiguousarray(code.records).view(np.uint8).copy()).cuda()
-    out = torch.empty((h, w), dtype=torch.uint8, device=rec.device)
-    lib = _lib.load()
-    rc = lib.fic_decode_v1(ctypes.c_void_p(rec.data_ptr()), h, w, code.range_size,
-                           code.domain_size, code.stride, iterations, level,
-                           ctypes.c_void_p(init_dev.data_ptr() if init_dev is not None else 0),
-                           ctypes.c_void_p(out.data_ptr()), _stream(torch, rec.device))
+    dev = torch.device("cuda", torch.cuda.current_device())
+    if initial is None:
+        work = torch.full((h, w), 128.0, dtype=torch.float64, device=dev)
+    elif np.ndim(initial) == 0:
+        work = torch.full((h, w), float(initial), dtype=torch.float64, device=dev)
+    else:
+        arr = np.asarray(initial)
+        if arr.shape != (h, w):
+            raise ValueError("initial image does not match the encoded geometry")
+        # initial.astype(np.float64) as the reference (codec.py:572)
+        work = torch.from_numpy(np.ascontiguousarray(arr.astype(np.float64))).to(dev)
+    rec = torch.from_numpy(np.ascontiguousarray(code.records).view(np.uint8).copy()).to(dev)
+    return torch, rec, work
+
+
+def _decode_step(torch, code, rec, src, dst, out):
+    rc = _lib.load().fic_decode_step_v1(
+        ctypes.c_void_p(rec.data_ptr()), code.height, code.width, code.range_size,
+        code.domain_size, code.stride, ctypes.c_void_p(src.data_ptr()),
+        ctypes.c_void_p(dst.data_ptr()), ctypes.c_void_p(out.data_ptr() if out is not None else 0),
+        _stream(torch, rec.device))
     _lib.check(rc)
+
+
+def decode_iterates(code: FractalCode, iterations: int = 10, initial=None):
+    """Drop-in for ``fic.codec.decode_iterates`` (codec.py:534-598): yield the
+    decoded uint8 image after each pass.  The float64 work image stays on the
+    GPU; one kernel per pass writes the next iterate and its rint snapshot."""
+    torch, rec, work = _decode_setup(code, iterations, initial)
+    nxt = torch.empty_like(work)
+    out = torch.empty(work.shape, dtype=torch.uint8, device=work.device)
+    for _ in range(iterations):
+        _decode_step(torch, code, rec, work, nxt, out)
+        work, nxt = nxt, work
+        yield out.cpu().numpy()
+
+
+def decode(code: FractalCode, iterations: int = 10, initial=None) -> np.ndarray:
+    """Drop-in for ``fic.codec.decode`` (codec.py:516-531): the last iterate."""
+    torch, rec, work = _decode_setup(code, iterations, initial)
+    nxt = torch.empty_like(work)
+    out = torch.empty(work.shape, dtype=torch.uint8, device=work.device)
+    for i in range(iterations):
+        _decode_step(torch, code, rec, work, nxt, out if i == iterations - 1 else None)
+        work, nxt = nxt, work
     return out.cpu().numpy()
+
+
+# ---------------------------------------------------------------------------
+# scalar fit / quantiser API (codec.py:90-130) -- host helpers on single
+# blocks, as in the reference (the encoder's batched fp64 sequence is
+# eval_candidate in csrc/common.cuh)
+# ---------------------------------------------------------------------------
+_S_STEPS = 31.0   # codec.py:28
+_O_STEPS = 127.0  # codec.py:29
+
+
+def fit_transform(range_pixels, domain_pixels) -> tuple[float, float, float]:
+    """Least-squares (s, o) minimizing sum((s*d + o - r)^2), s clamped to
+    [-1, 1]; returns (s, o, rms) with o and rms after the clamp
+    (codec.py:90-110, same op order: true division, not the encoder's
+    reciprocal)."""
+    r = np.asarray(range_pixels, dtype=np.float64).ravel()
+    d = np.asarray(domain_pixels, dtype=np.float64).ravel()
+    if r.shape != d.shape or r.size == 0:
+        raise ValueError("range and domain pixel counts must match and be >= 1")
+    n = float(r.size)
+    sum_d = d.sum()
+    sum_r = r.sum()
+    sum_dd = float(np.einsum("i,i->", d, d))
+    sum_dr = float(np.einsum("i,i->", d, r))
+    den = n * sum_dd - sum_d * sum_d
+    s = 0.0 if den == 0.0 else (n * sum_dr - sum_d * sum_r) / den
+    s = min(1.0, max(-1.0, s))
+    o = (sum_r - s * sum_d) / n
+    resid = s * d + o - r
+    rms = math.sqrt(float(np.einsum("i,i->", resid, resid)) / n)
+    return s, o, rms
+
+
+def quantize_so(s: float, o: float) -> tuple[int, int]:
+    """5-bit contrast over [-1, 1], 7-bit brightness over [-255, 255],
+    round-half-even (codec.py:113-122)."""
+    if not -1.0 <= s <= 1.0:
+        raise ValueError(f"s {s} outside [-1, 1]")
+    if not -255.0 <= o <= 255.0:
+        raise ValueError(f"o {o} outside [-255, 255]")
+    s_q = int(np.rint((s + 1.0) * (_S_STEPS / 2.0)))
+    o_q = int(np.rint((o + 255.0) * (_O_STEPS / 510.0)))
+    return s_q, o_q
+
+
+def dequantize_so(s_q: int, o_q: int) -> tuple[float, float]:
+    """codec.py:125-130."""
+    if not 0 <= s_q <= int(_S_STEPS):
+        raise ValueError(f"s_q {s_q} outside [0, 31]")
+    if not 0 <= o_q <= int(_O_STEPS):
+        raise ValueError(f"o_q {o_q} outside [0, 127]")
+    return s_q * (2.0 / _S_STEPS) - 1.0, o_q * (510.0 / _O_STEPS) - 255.0
 
 
 # ---------------------------------------------------------------------------

@@ -35,6 +35,14 @@ extern thread_local int g_launches;  // kernels launched by the current call
 
 inline void invalid(const std::string& msg) { throw Error{FIC_EINVAL, msg}; }
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) applies per device: set it
+// once per (current device, kernel, size), thread-safe (fic_api.cu).
+void smem_optin(const void* func, int bytes);
+template <class F>
+inline void smem_optin_k(F* func, int bytes) {
+  smem_optin(reinterpret_cast<const void*>(func), bytes);
+}
+
 // ---------------------------------------------------------------------------
 // geometry of one encode call (blocks.py / codec.py)
 // ---------------------------------------------------------------------------

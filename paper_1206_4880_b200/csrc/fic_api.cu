@@ -10,6 +10,7 @@
 #include <cstring>
 #include <map>
 #include <mutex>
+#include <set>
 #include <tuple>
 #include <vector>
 
@@ -23,6 +24,17 @@ thread_local int g_launches = 0;
 void set_error(const std::string& m) { g_err = m; }
 const char* last_error() { return g_err.c_str(); }
 
+void smem_optin(const void* func, int bytes) {
+  static std::mutex mu;
+  static std::set<std::tuple<int, const void*, int>> done;
+  int dev = 0;
+  FIC_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.count({dev, func, bytes})) return;
+  FIC_CUDA(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  done.insert({dev, func, bytes});
+}
+
 // ---------------------------------------------------------------------------
 // stream-ordered scratch: every buffer of a call comes from the device's
 // default memory pool (kept cached across calls) and is freed on the stream.
@@ -30,16 +42,19 @@ const char* last_error() { return g_err.c_str(); }
 class Scratch {
  public:
   explicit Scratch(cudaStream_t s) : s_(s) {
-    static bool pool_set = false;
-    if (!pool_set) {
-      int dev = 0;
-      cudaGetDevice(&dev);
+    // keep freed blocks cached in the device's default pool (once per device)
+    static std::mutex mu;
+    static std::set<int> done;
+    int dev = 0;
+    FIC_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lock(mu);
+    if (!done.count(dev)) {
       cudaMemPool_t pool;
       if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
         uint64_t thr = UINT64_MAX;
         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
       }
-      pool_set = true;
+      done.insert(dev);
     }
   }
   ~Scratch() {
@@ -139,18 +154,13 @@ static Geo validate(int H, int W, const fic_params_t& p) {
   return g;
 }
 
+// fdim.py:48-56: the DBC estimator needs at least two scales (scale_set)
 static void check_dbc_side(int side) {
-  uint16_t q[7 * 256];
-  int smax = 0, need = 0;
   int J = 0;
-  std::vector<int> scales;
   for (int s = 2; s <= side / 2; s *= 2)
     if (side % s == 0) ++J;
   if (J < 2)
     invalid("block side " + std::to_string(side) + " too small: need at least two DBC scales");
-  (void)q;
-  (void)smax;
-  (void)need;
 }
 
 // Device-resident DBC tables for one block side.
@@ -293,15 +303,6 @@ __global__ void k_classify(ClassifyArgs a) {
   }
 }
 
-__global__ void k_cost(const unsigned long long* key, int R, int n_iso, unsigned long long* cost) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= R) return;
-  unsigned long long k = key[i];
-  unsigned long long pool = (uint32_t)k - (uint32_t)((k >> 32) & 0x7fffffffu);
-  // an exact-path candidate costs ~32x a screened one
-  cost[i] = pool * n_iso * ((k >> 63) ? 32ull : 1ull) + 1ull;
-}
-
 __global__ void k_shard(const unsigned long long* key, const unsigned long long* cum, int R,
                         int shard, int nshard, PlanCounts* out) {
   if (threadIdx.x || blockIdx.x) return;
@@ -396,6 +397,87 @@ __global__ void __launch_bounds__(1024) k_range_scatter(const uint32_t* bin, con
       key_s[pos] = key[r];
       rid_s[pos] = (uint32_t)r;
     }
+  }
+}
+
+// Stable, deterministic variant of the counting sort (sharded calls: every
+// rank must cut the same order, so ties inside a bin keep raster order).
+// Ranges are cut into chunks of kStableChunk; k_chunk_hist counts the bins of
+// each chunk into a bin-major [nb][nchunk] matrix, whose exclusive scan
+// (k_bin_scan) is each (bin, chunk)'s first output position; one warp per
+// chunk then places its ranges in order (__match_any_sync ranks equal bins
+// within a round of 32, a shared counter per bin carries across rounds).
+constexpr int kStableChunk = 2048;
+
+__global__ void __launch_bounds__(1024) k_chunk_hist(const uint32_t* bin, int R, int nb,
+                                                     int nchunk, uint32_t* mat) {
+  extern __shared__ uint32_t cnt[];  // [nb]
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) cnt[b] = 0;
+  __syncthreads();
+  const int r0 = blockIdx.x * kStableChunk;
+  for (int i = threadIdx.x; i < kStableChunk; i += blockDim.x)
+    if (r0 + i < R) atomicAdd(cnt + bin[r0 + i], 1u);
+  __syncthreads();
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) mat[(int64_t)b * nchunk + blockIdx.x] = cnt[b];
+}
+
+__global__ void __launch_bounds__(32) k_range_scatter_stable(const uint32_t* bin,
+                                                             const unsigned long long* key, int R,
+                                                             int nb, int nchunk,
+                                                             const uint32_t* start,
+                                                             unsigned long long* key_s,
+                                                             uint32_t* rid_s) {
+  extern __shared__ uint32_t cur[];  // [nb] next position of each bin in this chunk
+  const int lane = threadIdx.x;
+  for (int b = lane; b < nb; b += 32) cur[b] = start[(int64_t)b * nchunk + blockIdx.x];
+  __syncwarp();
+  const int r0 = blockIdx.x * kStableChunk, r1 = min(R, r0 + kStableChunk);
+  for (int base = r0; base < r1; base += 32) {
+    const int r = base + lane;
+    const bool ok = r < r1;
+    const uint32_t b = ok ? bin[r] : 0xffffffffu;
+    const uint32_t peers = __match_any_sync(0xffffffffu, b);
+    const uint32_t rank = __popc(peers & ((1u << lane) - 1u));
+    uint32_t pos = 0;
+    if (ok) pos = cur[b] + rank;
+    __syncwarp();
+    if (ok && rank == 0) cur[b] += __popc(peers);
+    __syncwarp();
+    if (ok) {
+      key_s[pos] = key[r];
+      rid_s[pos] = (uint32_t)r;
+    }
+  }
+}
+
+// Inclusive scan of the per-position shard costs (one block; k_cost's rule).
+__global__ void __launch_bounds__(1024) k_cost_scan(const unsigned long long* key, int R,
+                                                    int n_iso, unsigned long long* cum) {
+  using Scan = cub::BlockScan<unsigned long long, 1024>;
+  __shared__ typename Scan::TempStorage tmp;
+  unsigned long long carry = 0;
+  for (int base = 0; base < R; base += 1024 * 4) {
+    unsigned long long v[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int k = base + threadIdx.x * 4 + i;
+      v[i] = 0;
+      if (k < R) {
+        const unsigned long long kk = key[k];
+        const unsigned long long pool = (uint32_t)kk - (uint32_t)((kk >> 32) & 0x7fffffffu);
+        // an exact-path candidate costs ~32x a screened one (as k_cost)
+        v[i] = pool * n_iso * ((kk >> 63) ? 32ull : 1ull) + 1ull;
+      }
+    }
+    unsigned long long t = 0;
+    Scan(tmp).InclusiveSum(v, v, t);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int k = base + threadIdx.x * 4 + i;
+      if (k < R) cum[k] = carry + v[i];
+    }
+    carry += t;
+    __syncthreads();
   }
 }
 
@@ -1009,9 +1091,11 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
   const int nb = pb.rank_start ? 2 * (pb.n_rank + 1) : 0;
   // (the shard partition is a cut of this order: every rank must compute the
   // same one, so shards keep the deterministic stable radix sort)
-  const bool bin_sort = pb.lo_rank && nb <= kMaxRangeBins && nshard == 1 && !getenv("FIC_RANGE_RADIX");
+  const bool bin_ok = pb.lo_rank && nb <= kMaxRangeBins && !getenv("FIC_RANGE_RADIX");
+  const bool bin_sort = bin_ok && nshard == 1 && !getenv("FIC_RANGE_STABLE");
+  const bool stable_sort = bin_ok && !bin_sort;
   uint32_t* bin_hist = nullptr;
-  if (bin_sort) {
+  if (bin_ok) {
     ca.lo_rank = pb.lo_rank;
     ca.n_rank = pb.n_rank;
     ca.bin = sc.get<uint32_t>(g.R);
@@ -1026,14 +1110,23 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
     uint32_t* cursor = sc.get<uint32_t>(nb);
     k_bin_scan<<<1, 1024, 0, s>>>(bin_hist, nb, cursor, pb.n_rank + 1, g.R, d_pc);
     FIC_CHECK_LAUNCH();
-    static bool attr = false;
-    if (!attr) {
-      FIC_CUDA(cudaFuncSetAttribute(k_range_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    kMaxRangeBins * (int)sizeof(uint32_t)));
-      attr = true;
-    }
+    smem_optin_k(k_range_scatter, kMaxRangeBins * (int)sizeof(uint32_t));
     k_range_scatter<<<(unsigned)cdiv(g.R, 4096), 1024, nb * sizeof(uint32_t), s>>>(
         ca.bin, key, g.R, nb, cursor, key_s, rid_s);
+    FIC_CHECK_LAUNCH();
+  } else if (stable_sort) {
+    // deterministic order (raster order inside a bin): every shard cuts the same list
+    const int nchunk = (int)cdiv(g.R, kStableChunk);
+    uint32_t* mat = sc.get<uint32_t>((size_t)nb * nchunk);
+    uint32_t* start = sc.get<uint32_t>((size_t)nb * nchunk);
+    smem_optin_k(k_chunk_hist, kMaxRangeBins * (int)sizeof(uint32_t));
+    smem_optin_k(k_range_scatter_stable, kMaxRangeBins * (int)sizeof(uint32_t));
+    k_chunk_hist<<<nchunk, 1024, nb * sizeof(uint32_t), s>>>(ca.bin, g.R, nb, nchunk, mat);
+    FIC_CHECK_LAUNCH();
+    k_bin_scan<<<1, 1024, 0, s>>>(mat, nb * nchunk, start, (pb.n_rank + 1) * nchunk, g.R, d_pc);
+    FIC_CHECK_LAUNCH();
+    k_range_scatter_stable<<<nchunk, 32, nb * sizeof(uint32_t), s>>>(ca.bin, key, g.R, nb, nchunk,
+                                                                   start, key_s, rid_s);
     FIC_CHECK_LAUNCH();
   } else {
     // order by (class, lo) only (bits 32..63; stable, so ties keep raster order):
@@ -1043,13 +1136,9 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
     });
   }
   if (!bin_sort) {
-    unsigned long long* cost = sc.get<unsigned long long>(g.R);
     unsigned long long* cum = sc.get<unsigned long long>(g.R);
-    k_cost<<<(unsigned)cdiv(g.R, 256), 256, 0, s>>>(key_s, g.R, g.n_iso, cost);
+    k_cost_scan<<<1, 1024, 0, s>>>(key_s, g.R, g.n_iso, cum);
     FIC_CHECK_LAUNCH();
-    cub_call(sc, [&](void* t, size_t& b) {
-      return cub::DeviceScan::InclusiveSum(t, b, cost, cum, g.R, s);
-    });
     k_shard<<<1, 32, 0, s>>>(key_s, cum, g.R, shard, nshard, d_pc);
     FIC_CHECK_LAUNCH();
   }
@@ -1285,14 +1374,16 @@ static void plan_impl(const uint8_t* img, int H, int W, const fic_params_t& p, d
 
 // ---------------------------------------------------------------------------
 // decode (codec.py:534-598): gather 2x2 means, isometry, s*x + o, clip,
-// scatter; the work image stays float64, rint -> uint8 at the end.
+// scatter; the work image stays float64, rint -> uint8 when yielded.
 // ---------------------------------------------------------------------------
 struct DecArgs {
   const uint8_t* rec;
   int W, rs, st, ndx, nrx, R;
+  uint32_t n_dom;
   const int* perm;  // [8][K]
-  double* src;
+  const double* src;
   double* dst;
+  uint8_t* out;     // optional: rint(dst) as uint8 (one decode_iterates snapshot)
 };
 
 __global__ void k_decode(DecArgs a) {
@@ -1302,10 +1393,13 @@ __global__ void k_decode(DecArgs a) {
   int r = (int)(t / K), k = (int)(t - (int64_t)r * K);
   const uint8_t* rc = a.rec + (int64_t)r * 7;
   uint32_t dom = rc[0] | (rc[1] << 8) | (rc[2] << 16) | ((uint32_t)rc[3] << 24);
+  if (dom >= a.n_dom) dom = 0;  // memory safety only: callers validate first
   int iso = rc[4];
   double s_hat = __dsub_rn(__dmul_rn((double)rc[5], 2.0 / 31.0), 1.0);
   double o_hat = __dsub_rn(__dmul_rn((double)rc[6], 510.0 / 127.0), 255.0);
-  int m = a.perm[iso * K + k];  // domains[rows][:, perms[iso]]
+  // domains[rows][:, perms[iso]] for iso 0..7; other bytes keep the identity
+  // (codec.py:580-592 permutes only the rows of isometries 0..7)
+  int m = iso < 8 ? a.perm[iso * K + k] : k;
   int u = m / a.rs, v = m - u * a.rs;
   int64_t y = (int64_t)(dom / a.ndx) * a.st + 2 * u;
   int64_t x = (int64_t)(dom % a.ndx) * a.st + 2 * v;
@@ -1318,6 +1412,7 @@ __global__ void k_decode(DecArgs a) {
   int ry = r / a.nrx, rx = r - ry * a.nrx;
   int64_t oy = (int64_t)ry * a.rs + k / a.rs, ox = (int64_t)rx * a.rs + k % a.rs;
   a.dst[oy * a.W + ox] = val;
+  if (a.out) a.out[oy * a.W + ox] = (uint8_t)rint(val);
 }
 
 __global__ void k_fill(double* w, int64_t n, double v, const uint8_t* init) {
@@ -1325,13 +1420,16 @@ __global__ void k_fill(double* w, int64_t n, double v, const uint8_t* init) {
   if (i < n) w[i] = init ? (double)init[i] : v;
 }
 
-__global__ void k_round(const double* w, uint8_t* out, int64_t n) {
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) out[i] = (uint8_t)rint(w[i]);
+__global__ void k_max_domain(const uint8_t* rec, int R, unsigned int* mx) {
+  int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= R) return;
+  const uint8_t* rc = rec + (int64_t)r * 7;
+  atomicMax(mx, rc[0] | (rc[1] << 8) | (rc[2] << 16) | ((uint32_t)rc[3] << 24));
 }
 
-static void decode_impl(const uint8_t* rec, int H, int W, int rs, int ds, int st, int iters,
-                        double initial, const uint8_t* init_img, uint8_t* out, cudaStream_t s) {
+// Validation of decode_iterates (codec.py:541-556), reference texts.
+static DecArgs decode_geometry(const uint8_t* rec, int H, int W, int rs, int ds, int st,
+                               int iters) {
   if (iters < 1) invalid("iterations must be >= 1");
   if (rs <= 0 || H % rs || W % rs)
     invalid("image " + std::to_string(W) + "x" + std::to_string(H) +
@@ -1340,26 +1438,83 @@ static void decode_impl(const uint8_t* rec, int H, int W, int rs, int ds, int st
   if (ds > std::min(W, H))
     invalid("domain size " + std::to_string(ds) + " exceeds image " + std::to_string(W) + "x" +
             std::to_string(H));
-  int K = rs * rs;
-  Scratch sc(s);
+  DecArgs a{};
+  a.rec = rec;
+  a.W = W;
+  a.rs = rs;
+  a.st = st;
+  a.ndx = (W - ds) / st + 1;
+  a.nrx = W / rs;
+  a.R = (W / rs) * (H / rs);
+  const int ndy = (H - ds) / st + 1;
+  a.n_dom = (uint32_t)((int64_t)a.ndx * ndy);
+  // the 2x2 gathers of the last domain must stay inside the image (numpy
+  // raises IndexError there, codec.py:575-582)
+  if ((int64_t)(a.ndx - 1) * st + 2 * rs > W || (int64_t)(ndy - 1) * st + 2 * rs > H)
+    invalid("index out of bounds: domain_size too small for range_size in this geometry");
+  return a;
+}
+
+// isometry permutation tables on the device, once per (device, range size)
+static const int* iso_perm_table(int rs) {
+  static std::mutex mu;
+  static std::map<std::pair<int, int>, int*> cache;
+  int dev = 0;
+  FIC_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find({dev, rs});
+  if (it != cache.end()) return it->second;
+  const int K = rs * rs;
   std::vector<int> perm(8 * K), inv(8 * K);
   iso_tables(rs, perm.data(), inv.data());
-  int* d_perm = sc.get<int>(8 * K);
-  FIC_CUDA(cudaMemcpyAsync(d_perm, perm.data(), 8 * K * sizeof(int), cudaMemcpyHostToDevice, s));
+  int* d = nullptr;
+  FIC_CUDA(cudaMalloc(&d, 8 * K * sizeof(int)));
+  FIC_CUDA(cudaMemcpy(d, perm.data(), 8 * K * sizeof(int), cudaMemcpyHostToDevice));
+  cache.emplace(std::make_pair(dev, rs), d);
+  return d;
+}
+
+static void decode_impl(const uint8_t* rec, int H, int W, int rs, int ds, int st, int iters,
+                        double initial, const uint8_t* init_img, uint8_t* out, cudaStream_t s) {
+  DecArgs a = decode_geometry(rec, H, W, rs, ds, st, iters);
+  Scratch sc(s);
+  // records referencing a domain outside the geometry (codec.py:551-555)
+  unsigned int* d_mx = sc.get<unsigned int>(1);
+  FIC_CUDA(cudaMemsetAsync(d_mx, 0, sizeof(unsigned int), s));
+  k_max_domain<<<(unsigned)cdiv(a.R, 256), 256, 0, s>>>(rec, a.R, d_mx);
+  FIC_CHECK_LAUNCH();
+  unsigned int mx = 0;
+  FIC_CUDA(cudaMemcpyAsync(&mx, d_mx, sizeof(mx), cudaMemcpyDeviceToHost, s));
+  FIC_CUDA(cudaStreamSynchronize(s));
+  if (a.R && mx >= a.n_dom) invalid("record references a domain outside the current image geometry");
+  a.perm = iso_perm_table(rs);
   int64_t n = (int64_t)H * W;
   double* w0 = sc.get<double>(n);
   double* w1 = sc.get<double>(n);
   k_fill<<<(unsigned)cdiv(n, 256), 256, 0, s>>>(w0, n, initial, init_img);
   FIC_CHECK_LAUNCH();
-  DecArgs a{rec, W, rs, st, (W - ds) / st + 1, W / rs, (W / rs) * (H / rs), d_perm, w0, w1};
   for (int i = 0; i < iters; ++i) {
+    a.src = w0;
+    a.dst = w1;
+    a.out = (i == iters - 1) ? out : nullptr;
     k_decode<<<(unsigned)cdiv(n, 256), 256, 0, s>>>(a);
     FIC_CHECK_LAUNCH();
-    std::swap(a.src, a.dst);
+    std::swap(w0, w1);
   }
-  k_round<<<(unsigned)cdiv(n, 256), 256, 0, s>>>(a.src, out, n);
-  FIC_CHECK_LAUNCH();
   FIC_CUDA(cudaStreamSynchronize(s));
+}
+
+static void decode_step_impl(const uint8_t* rec, int H, int W, int rs, int ds, int st,
+                             const double* src, double* dst, uint8_t* out, cudaStream_t s) {
+  DecArgs a = decode_geometry(rec, H, W, rs, ds, st, 1);
+  if (!src || !dst) invalid("work images must not be NULL");
+  a.perm = iso_perm_table(rs);
+  a.src = src;
+  a.dst = dst;
+  a.out = out;
+  const int64_t n = (int64_t)H * W;
+  k_decode<<<(unsigned)cdiv(n, 256), 256, 0, s>>>(a);
+  FIC_CHECK_LAUNCH();
 }
 
 }  // namespace fic
@@ -1423,6 +1578,16 @@ extern "C" int fic_decode_v1(const uint8_t* d_records, int32_t height, int32_t w
   return guarded([&] {
     decode_impl(d_records, height, width, range_size, domain_size, stride, iterations, initial,
                 d_initial, d_out, as_stream(stream));
+  });
+}
+
+extern "C" int fic_decode_step_v1(const uint8_t* d_records, int32_t height, int32_t width,
+                                  int32_t range_size, int32_t domain_size, int32_t stride,
+                                  const double* d_src, double* d_dst, uint8_t* d_out,
+                                  void* stream) {
+  return guarded([&] {
+    decode_step_impl(d_records, height, width, range_size, domain_size, stride, d_src, d_dst,
+                     d_out, as_stream(stream));
   });
 }
 

@@ -379,14 +379,12 @@ void launch_fd(const FdArgs& a, cudaStream_t s) {
     const int64_t nby = a.n / a.nbx;
     const int nr = a.rank_hist ? a.n_rank : 0;
     const bool pow2 = a.qshift[0] >= 0 && a.qshift[1] >= 0 && a.qshift[2] >= 0;
-    static bool attr = false;
-    if (!attr) {
+    {
       const int mx = (int)fd16_tile_smem(16, 4, kCountSortMaxRanks);
-      FIC_CUDA(cudaFuncSetAttribute(k_fd16_tile<16, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
-      FIC_CUDA(cudaFuncSetAttribute(k_fd16_tile<32, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
-      FIC_CUDA(cudaFuncSetAttribute(k_fd16_tile<16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
-      FIC_CUDA(cudaFuncSetAttribute(k_fd16_tile<32, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
-      attr = true;
+      smem_optin_k(k_fd16_tile<16, false>, mx);
+      smem_optin_k(k_fd16_tile<32, false>, mx);
+      smem_optin_k(k_fd16_tile<16, true>, mx);
+      smem_optin_k(k_fd16_tile<32, true>, mx);
     }
     if (a.bst == 1) {
       constexpr int T = 32;
@@ -628,12 +626,7 @@ void launch_count_sort(const uint32_t* rank, int64_t D, int n_rank, const uint32
                        const ScalArgs& sa, cudaStream_t s) {
   k_rank_scan<<<1, 1024, 0, s>>>(hist, n_rank, D, start, cursor, sa);
   FIC_CHECK_LAUNCH();
-  static bool attr = false;
-  if (!attr) {
-    FIC_CUDA(cudaFuncSetAttribute(k_rank_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  kCountSortMaxRanks * (int)sizeof(uint32_t)));
-    attr = true;
-  }
+  smem_optin_k(k_rank_scatter, kCountSortMaxRanks * (int)sizeof(uint32_t));
   k_rank_scatter<<<(unsigned)cdiv(D, 4096), 1024, n_rank * sizeof(uint32_t), s>>>(
       rank, D, n_rank, minid, start, cursor, order);
   FIC_CHECK_LAUNCH();
@@ -711,12 +704,7 @@ void launch_slabs(const SlabArgs& a, cudaStream_t s) {
   }
   const bool rank_form = (a.strategy == FIC_STATIC2 || a.strategy == FIC_DYNAMIC_FD) && !a.keys;
   const size_t smem = rank_form ? (size_t)a.n_rank * sizeof(double) : 0;
-  static bool attr = false;
-  if (!attr) {
-    FIC_CUDA(cudaFuncSetAttribute(k_slabs, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  kCountSortMaxRanks * (int)sizeof(double)));
-    attr = true;
-  }
+  smem_optin_k(k_slabs, kCountSortMaxRanks * (int)sizeof(double));
   k_slabs<<<(unsigned)cdiv(a.R, 128), 128, smem, s>>>(a);
   FIC_CHECK_LAUNCH();
 }
@@ -968,11 +956,7 @@ void launch_pool(const PoolArgs& a, cudaStream_t s) {
   if (a.rs == 8 && a.trows) {
     const int pw = (DR_COLS - 1) * a.st + 16;
     const size_t smem = (size_t)(DR_ROWS + 1) * (((pw + 3) & ~3) + 4) + 16;
-    static bool attr = false;
-    if (!attr) {
-      FIC_CUDA(cudaFuncSetAttribute(k_domrows, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-      attr = true;
-    }
+    smem_optin_k(k_domrows, 200 * 1024);
     if (smem > 200 * 1024) invalid("domain stride too large for the row-segment pool builder");
     dim3 grid((unsigned)cdiv(a.ndx, DR_COLS), (unsigned)cdiv(2 * a.mh, DR_ROWS));
     k_domrows<<<grid, 256, smem, s>>>(a.img, a.H, a.W, a.st, a.ndx, a.mh, a.trows);

@@ -1042,14 +1042,8 @@ static void launch_tc_k(const PoolView& P, const RangeView& Rv, const TcArgs& a,
                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (cr != CUDA_SUCCESS) throw Error{FIC_ECUDA, "cuTensorMapEncodeTiled failed"};
-  static bool attr_set = false;
-  if (!attr_set) {
-    FIC_CUDA(cudaFuncSetAttribute(k_match_tc<K, CG, false>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-    FIC_CUDA(cudaFuncSetAttribute(k_match_tc<K, CG, true>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-    attr_set = true;
-  }
+  smem_optin_k(k_match_tc<K, CG, false>, C::SMEM);
+  smem_optin_k(k_match_tc<K, CG, true>, C::SMEM);
   int dev = 0, sms = 148;
   FIC_CUDA(cudaGetDevice(&dev));
   FIC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));

@@ -36,3 +36,8 @@ def golden_delta():
 @pytest.fixture(scope="session")
 def golden_fd():
     return load_golden("fd_cases.npz")
+
+
+@pytest.fixture(scope="session")
+def golden_decode():
+    return load_golden("decode_cases.npz")

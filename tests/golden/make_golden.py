@@ -45,10 +45,12 @@ def sha(img: np.ndarray) -> str:
     return hashlib.sha256(np.ascontiguousarray(img).tobytes()).hexdigest()
 
 
-def harness_encode(image, strategy, *, range_size=8, domain_size=16, stride=1,
-                   isometries=False, fd_source="original", delta=None,
-                   range_ids=None):
-    """codec.encode setup with ``delta`` in place of D_f; reference matcher."""
+def harness_setup(image, strategy, *, range_size=8, domain_size=16, stride=1,
+                  isometries=False, fd_source="original", delta=None):
+    """codec.encode's setup (codec.py:324-376) with ``delta`` in place of D_f.
+
+    Returns (ctx, r_matrix, extra): the reference's own ``_SearchContext``
+    with its slabs set, the range matrix, and the FD arrays / K1 inputs."""
     image = np.asarray(image)
     r_stack = rbl.range_stack(image, range_size)
     n_ranges = r_stack.shape[0]
@@ -61,7 +63,7 @@ def harness_encode(image, strategy, *, range_size=8, domain_size=16, stride=1,
     inv_perms = [np.argsort(perms[i]) for i in range(rbl.ISOMETRY_COUNT)]
     iso_list = list(range(rbl.ISOMETRY_COUNT)) if isometries else [0]
     ctx = rcodec._SearchContext(d_matrix, iso_list, inv_perms)
-    extra = {}
+    extra = {"d_down": d_down}
     if strategy == "exhaustive":
         ctx.slab_lo = np.zeros(n_ranges, dtype=np.int64)
         ctx.slab_hi = np.full(n_ranges, n_domains, dtype=np.int64)
@@ -93,21 +95,46 @@ def harness_encode(image, strategy, *, range_size=8, domain_size=16, stride=1,
             pos = rcodec._nearest_fd_positions(keys, ids, fd_rng[empty])
             ctx.slab_lo[empty] = pos
             ctx.slab_hi[empty] = pos + 1
-        extra = dict(fd_dom=fd_dom, fd_rng=fd_rng, keys=keys, ids=ids)
+        extra.update(fd_dom=fd_dom, fd_rng=fd_rng, keys=keys, ids=ids)
+    del d_stack
+    return ctx, r_matrix, extra
+
+
+def harness_run(ctx, r_matrix, range_ids):
+    """The reference's own matcher ``codec._search_chunk`` on ``range_ids``."""
+    n_ranges = r_matrix.shape[0]
     out = {k: np.zeros(n_ranges, dtype=np.int64) for k in ("domain", "isometry", "s_q", "o_q")}
     out["pre_rms"] = np.zeros(n_ranges)
     out["post_rms"] = np.zeros(n_ranges)
-    if range_ids is None:
-        range_ids = np.arange(n_ranges)
     rcodec._search_chunk(ctx, r_matrix, np.asarray(range_ids), out)
+    return out
+
+
+def harness_result(ctx, r_matrix, extra, out):
+    n_ranges = r_matrix.shape[0]
     pools = (ctx.slab_hi - ctx.slab_lo).astype(np.int64)
     rec = np.zeros(n_ranges, dtype=rcodec.RECORD_DTYPE)
     for k in ("domain", "isometry", "s_q", "o_q"):
         rec[k] = out[k]
+    extra = {k: v for k, v in extra.items() if k != "d_down"}
     return dict(records=rec, pre_rms=out["pre_rms"], post_rms=out["post_rms"],
                 pool_sizes=pools, slab_lo=ctx.slab_lo.astype(np.int64),
                 slab_hi=ctx.slab_hi.astype(np.int64),
-                comparisons=int(pools.sum()) * len(iso_list), **extra)
+                comparisons=int(pools.sum()) * len(ctx.iso_list), **extra)
+
+
+def harness_encode(image, strategy, *, range_size=8, domain_size=16, stride=1,
+                   isometries=False, fd_source="original", delta=None,
+                   range_ids=None):
+    """codec.encode setup with ``delta`` in place of D_f; reference matcher."""
+    ctx, r_matrix, extra = harness_setup(image, strategy, range_size=range_size,
+                                         domain_size=domain_size, stride=stride,
+                                         isometries=isometries, fd_source=fd_source,
+                                         delta=delta)
+    if range_ids is None:
+        range_ids = np.arange(r_matrix.shape[0])
+    out = harness_run(ctx, r_matrix, range_ids)
+    return harness_result(ctx, r_matrix, extra, out)
 
 
 def rand(shape, seed):
@@ -295,6 +322,56 @@ def bench_cases():
     print(f"wrote {path} ({os.path.getsize(path)} bytes)")
 
 
+def decode_cases():
+    """decode_iterates snapshots, float initial images and isometry bytes > 7
+    through the reference's own decoder (codec.py:516-598), plus the scalar
+    fit / quantiser API (codec.py:90-130)."""
+    out = {}
+    rng = np.random.default_rng(31)
+    for name, img, strat, stride in (("rand64_dyn_s2", rand((64, 64), 41), "dynamic_fd", 2),
+                                     ("rand48x80_ex_s4", rand((48, 80), 42), "exhaustive", 4)):
+        code, _ = rcodec.encode(img, strat, stride=stride, isometries=True)
+        out[f"{name}.image"] = img
+        out[f"{name}.params"] = np.array([stride, 1, rcodec.STRATEGY_IDS[strat], 8, 16])
+        out[f"{name}.records"] = code.records.view(np.uint8).reshape(-1, 7)
+        out[f"{name}.iterates"] = np.stack(list(rcodec.decode_iterates(code, 6)))
+        init = rng.uniform(-20.0, 280.0, img.shape)      # float, out of byte range
+        out[f"{name}.init_float"] = init
+        out[f"{name}.decoded_float_init"] = rcodec.decode(code, 4, initial=init)
+        out[f"{name}.decoded_level"] = rcodec.decode(code, 3, initial=37.25)
+        bad = code.records.copy()
+        sel = rng.choice(len(bad), len(bad) // 3, replace=False)
+        bad["isometry"][sel] = rng.integers(8, 256, len(sel))
+        code_bad = rcodec.FractalCode(code.width, code.height, 8, 16, stride, code.strategy_id,
+                                      True, bad)
+        out[f"{name}.records_iso_gt7"] = bad.view(np.uint8).reshape(-1, 7)
+        out[f"{name}.decoded_iso_gt7"] = rcodec.decode(code_bad, 5)
+    # fit_transform on random pairs of several lengths, incl. clamps and flat domains
+    fits_in, fits_out = [], []
+    for n in (1, 4, 16, 64):
+        for k in range(40):
+            r = rng.integers(0, 256, n).astype(np.float64)
+            d = rng.integers(0, 256, n).astype(np.float64)
+            if k % 10 == 0:
+                d[:] = d[0]
+            if k % 10 == 1:
+                r = 3.0 * d - 100.0
+            row = np.full((2, 64), np.nan)
+            row[0, :n], row[1, :n] = r, d
+            fits_in.append(row)
+            fits_out.append(rcodec.fit_transform(r, d))
+    out["fit.inputs"] = np.stack(fits_in)
+    out["fit.outputs"] = np.array(fits_out)
+    so = np.column_stack([rng.uniform(-1.0, 1.0, 500), rng.uniform(-255.0, 255.0, 500)])
+    so[:4] = [[-1.0, -255.0], [1.0, 255.0], [0.0, 0.0], [1.0 / 31.0, 255.0 / 127.0]]
+    out["quant.inputs"] = so
+    out["quant.outputs"] = np.array([rcodec.quantize_so(a, b) for a, b in so])
+    grid = np.array([(a, b) for a in range(32) for b in range(128)])
+    out["dequant.inputs"] = grid
+    out["dequant.outputs"] = np.array([rcodec.dequantize_so(int(a), int(b)) for a, b in grid])
+    save("decode_cases.npz", **out)
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 1:
         for fn in sys.argv[1:]:
@@ -304,3 +381,4 @@ if __name__ == "__main__":
         encode_cases()
         delta_cases()
         bench_cases()
+        decode_cases()

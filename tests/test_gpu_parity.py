@@ -376,3 +376,75 @@ def test_run_single_rows_match_reference_bench_rows():
         for i in timing:
             row[i] = ""
         assert row == run["row"], run["name"] + "/" + run["strategy"]
+
+
+DEC = load_golden("decode_cases.npz")
+DEC_CASES = sorted({k.split(".")[0] for k in DEC if k.endswith(".iterates")})
+
+
+def _dec_code(name, recs_key="records"):
+    img = DEC[f"{name}.image"]
+    stride, iso, sid, rs, ds = (int(v) for v in DEC[f"{name}.params"])
+    return codec.FractalCode(img.shape[1], img.shape[0], rs, ds, stride, sid, bool(iso),
+                             _recs(DEC[f"{name}.{recs_key}"]).copy())
+
+
+@pytest.mark.parametrize("name", DEC_CASES)
+def test_decode_iterates_match_reference_snapshots(name):
+    code = _dec_code(name)
+    its = list(codec.decode_iterates(code, 6))
+    assert len(its) == 6
+    for got, want in zip(its, DEC[f"{name}.iterates"]):
+        assert got.dtype == np.uint8 and np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("name", DEC_CASES)
+def test_decode_float_initial_and_level(name):
+    code = _dec_code(name)
+    out = codec.decode(code, 4, initial=DEC[f"{name}.init_float"])
+    assert np.array_equal(out, DEC[f"{name}.decoded_float_init"])
+    assert np.array_equal(codec.decode(code, 3, initial=37.25), DEC[f"{name}.decoded_level"])
+
+
+@pytest.mark.parametrize("name", DEC_CASES)
+def test_decode_isometry_bytes_above_7_keep_identity(name):
+    code = _dec_code(name, "records_iso_gt7")
+    assert int(code.records["isometry"].max()) > 7
+    assert np.array_equal(codec.decode(code, 5), DEC[f"{name}.decoded_iso_gt7"])
+
+
+def test_decode_rejects_out_of_geometry_domain_via_c_abi():
+    import ctypes
+
+    import torch
+    name = DEC_CASES[0]
+    code = _dec_code(name)
+    rec = code.records.copy()
+    rec["domain"][3] = 10 ** 6
+    d_rec = torch.from_numpy(rec.view(np.uint8).copy()).cuda()
+    out = torch.empty((code.height, code.width), dtype=torch.uint8, device="cuda")
+    lib = codec._lib.load()
+    rc = lib.fic_decode_v1(ctypes.c_void_p(d_rec.data_ptr()), code.height, code.width, 8, 16,
+                           code.stride, 2, 128.0, None, ctypes.c_void_p(out.data_ptr()), None)
+    assert rc == codec._lib.FIC_EINVAL
+    assert "outside the current image geometry" in lib.fic_last_error().decode()
+
+
+def test_encode_accepts_negative_stride_views():
+    img = np.random.default_rng(12).integers(0, 256, (64, 64), dtype=np.uint8)
+    flipped = np.flipud(img)
+    a, _ = codec.encode(flipped, "dynamic_fd", stride=4, isometries=True)
+    b, _ = codec.encode(np.ascontiguousarray(flipped), "dynamic_fd", stride=4, isometries=True)
+    assert a == b
+
+
+def test_encode_on_a_second_device_after_the_first():
+    """Per-device shared-memory opt-ins: an encode on cuda:1 after cuda:0 (one
+    process, two devices) must launch; skipped on a one-GPU box."""
+    import torch
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs two GPUs")
+    img = synth.CONFIGS["cfg1"].make()
+    a, _ = codec.encode(img, "dynamic_fd", stride=8, isometries=True, device=0)
+    b, _ = codec.encode(img, "dynamic_fd", stride=8, isometries=True, device=1)
+    assert a == b

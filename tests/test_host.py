@@ -216,3 +216,56 @@ def test_params_are_cached_per_argument_tuple():
     p3 = codec.make_params("dynamic_fd", 8, 16, 2, True, "original", 0.05, "auto", (0, 1))
     assert p1 is p2 and p1 is not p3
     assert p3.stride == 2 and p1.stride == 1
+
+
+def test_scalar_fit_and_quantiser_match_reference(golden_decode):
+    g = golden_decode
+    for row, want in zip(g["fit.inputs"], g["fit.outputs"]):
+        n = int(np.count_nonzero(~np.isnan(row[0])))
+        got = codec.fit_transform(row[0, :n], row[1, :n])
+        assert got == tuple(want)          # bit-identical fp64
+    for (s, o), want in zip(g["quant.inputs"], g["quant.outputs"]):
+        assert codec.quantize_so(s, o) == tuple(int(v) for v in want)
+    for (sq, oq), want in zip(g["dequant.inputs"], g["dequant.outputs"]):
+        assert codec.dequantize_so(int(sq), int(oq)) == tuple(want)
+
+
+@pytest.mark.parametrize("call,msg", [
+    (lambda: codec.fit_transform([1, 2, 3], [1, 2]), "match"),
+    (lambda: codec.fit_transform([], []), "match"),
+    (lambda: codec.quantize_so(1.5, 0.0), "outside"),
+    (lambda: codec.quantize_so(0.0, 300.0), "outside"),
+    (lambda: codec.dequantize_so(32, 0), "outside"),
+    (lambda: codec.dequantize_so(0, 128), "outside"),
+])
+def test_scalar_api_errors_match_reference(call, msg):
+    with pytest.raises(ValueError, match=msg):
+        call()
+
+
+def test_scalar_api_known_answers():
+    # test_codec.py:21-99 of the reference
+    s, o, rms = codec.fit_transform([1, 3, 5, 7], [0, 1, 2, 3])
+    assert s == 1.0 and o == pytest.approx(2.5) and rms == pytest.approx(1.25 ** 0.5)
+    s, o, rms = codec.fit_transform([10, 20, 30, 40], [7, 7, 7, 7])
+    assert s == 0.0 and o == pytest.approx(25.0)
+    assert codec.quantize_so(-1.0, -255.0) == (0, 0)
+    assert codec.quantize_so(1.0, 255.0) == (31, 127)
+    assert codec.dequantize_so(codec.quantize_so(0.0, 0.0)[0], 0)[0] == pytest.approx(1 / 31)
+
+
+def test_oracle_decode_matches_reference_snapshots(golden_decode):
+    g = golden_decode
+    for name in sorted({k.split(".")[0] for k in g if k.endswith(".iterates")}):
+        img = g[f"{name}.image"]
+        stride = int(g[f"{name}.params"][0])
+        rec = np.ascontiguousarray(g[f"{name}.records"]).view(orc.RECORD_DTYPE).ravel()
+        for k, want in enumerate(g[f"{name}.iterates"], start=1):
+            got = orc.decode(rec, img.shape[1], img.shape[0], 8, 16, stride, iterations=k)
+            assert np.array_equal(got, want)
+        bad = np.ascontiguousarray(g[f"{name}.records_iso_gt7"]).view(orc.RECORD_DTYPE).ravel()
+        got = orc.decode(bad, img.shape[1], img.shape[0], 8, 16, stride, iterations=5)
+        assert np.array_equal(got, g[f"{name}.decoded_iso_gt7"])
+        got = orc.decode(rec, img.shape[1], img.shape[0], 8, 16, stride, iterations=4,
+                         initial=g[f"{name}.init_float"])
+        assert np.array_equal(got, g[f"{name}.decoded_float_init"])
