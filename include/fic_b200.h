@@ -131,6 +131,18 @@ int fic_plan_v1(const uint8_t* d_image, int32_t height, int32_t width,
                 int64_t* d_order, int64_t* d_slab_lo, int64_t* d_slab_hi,
                 fic_stats_t* h_stats, void* stream);
 
+/* The pool builder alone (K1) -- fic.blocks.downsample2(domain_stack)
+ * (blocks.py:75-82, 158-164) and the _SearchContext sums (codec.py:136-157),
+ * in the pool order of `params` (FD order for dynamic_fd / static2, raster
+ * otherwise; codec.py:159-164 use_order).  Device outputs, any may be NULL:
+ * d_order[D] raster domain id per pool position, d_decimated[D*K] uint8,
+ * d_sums[2*D] uint32 (sum_d, sum_dd) pairs, d_inv_den[D] (1/den, 0 where
+ * den == 0), d_b_rows[D*K] fp16 bits of the tensor path's centred unit-norm
+ * rows (K = 16 or 64 only).  Synchronises `stream`. */
+int fic_pool_v1(const uint8_t* d_image, int32_t height, int32_t width,
+                const fic_params_t* params, int64_t* d_order, uint8_t* d_decimated,
+                uint32_t* d_sums, double* d_inv_den, uint16_t* d_b_rows, void* stream);
+
 /* Replaces fic.fdim.dbc_grid (fdim.py:44-80) for an (n, side, side) uint8
  * stack in device memory; d_fd[n] receives the dimension (clamped to [2,3]
  * when clamp != 0). */

@@ -93,7 +93,10 @@ def dbc_scales(side: int) -> list[int]:
 
 def dbc_weights(side: int) -> np.ndarray:
     """Slope weights exactly as the reference's numpy computes them."""
-    xs = np.log([side / s for s in dbc_scales(side)])
+    scales = dbc_scales(side)
+    if len(scales) < 2:  # no slope (the FD paths raise before using it)
+        return np.zeros(len(scales), dtype=np.float64)
+    xs = np.log([side / s for s in scales])
     dx = xs - xs.mean()
     return np.ascontiguousarray(dx / np.dot(dx, dx), dtype=np.float64)
 
@@ -553,6 +556,40 @@ def plan(image, strategy="dynamic_fd", *, range_size=8, domain_size=16, stride=1
     if strategy in ("static2", "dynamic_fd"):
         out["fd_dom"] = fd_dom.cpu().numpy()
         out["fd_rng"] = fd_rng.cpu().numpy()
+    return out
+
+
+def pool(image, strategy="dynamic_fd", *, range_size=8, domain_size=16, stride=1,
+         fd_source="original", delta=None, b_rows=False) -> dict:
+    """The pool builder's outputs in pool order (fic_pool_v1): ``order``
+    (raster id per position), ``decimated`` (D, K) uint8 = downsample2 of
+    the domains (blocks.py:75-82), ``sum_d``/``sum_dd`` (uint32),
+    ``inv_den`` (float64) as ``_SearchContext`` (codec.py:136-157), and with
+    ``b_rows`` the tensor path's fp16 rows."""
+    torch = _torch()
+    image, h, w = validate(image, strategy, range_size, domain_size, stride, fd_source)
+    img = image if hasattr(image, "is_cuda") else torch.from_numpy(np.ascontiguousarray(image)).cuda()
+    n_d = ((h - domain_size) // stride + 1) * ((w - domain_size) // stride + 1)
+    k = range_size * range_size
+    dev = img.device
+    order = torch.empty(n_d, dtype=torch.int64, device=dev)
+    dec = torch.empty((n_d, k), dtype=torch.uint8, device=dev)
+    sums = torch.empty((n_d, 2), dtype=torch.int32, device=dev)
+    inv = torch.empty(n_d, dtype=torch.float64, device=dev)
+    bh = torch.empty((n_d, k), dtype=torch.float16, device=dev) if b_rows else None
+    prm = make_params(strategy, range_size, domain_size, stride, False, fd_source, delta,
+                      "auto", (0, 1))
+    rc = _lib.load().fic_pool_v1(
+        ctypes.c_void_p(img.data_ptr()), h, w, ctypes.byref(prm),
+        ctypes.c_void_p(order.data_ptr()), ctypes.c_void_p(dec.data_ptr()),
+        ctypes.c_void_p(sums.data_ptr()), ctypes.c_void_p(inv.data_ptr()),
+        ctypes.c_void_p(bh.data_ptr() if bh is not None else 0), _stream(torch, dev))
+    _lib.check(rc)
+    s = sums.cpu().numpy().view(np.uint32)
+    out = dict(order=order.cpu().numpy(), decimated=dec.cpu().numpy(), sum_d=s[:, 0].copy(),
+               sum_dd=s[:, 1].copy(), inv_den=inv.cpu().numpy())
+    if bh is not None:
+        out["b_rows"] = bh.cpu().numpy()
     return out
 
 

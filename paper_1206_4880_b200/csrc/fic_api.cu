@@ -955,6 +955,59 @@ static const int* iso_inverse_table(int dev, int rs) {
   return d;
 }
 
+// K1 buffers: what the matchers read per pool position (fp16 B rows on the
+// tensor path, sums, 1/den) plus the source of the decimated pixels -- the
+// row segments or box-floor planes the builder stages anyway (8x8 / 4x4
+// ranges), or a zero-padded raw copy for other range sizes.
+static PoolArgs pool_args(Scratch& sc, const Geo& g, const uint8_t* img, const uint32_t* order,
+                          bool tensor_ok) {
+  PoolArgs pa{};
+  pa.img = img;
+  pa.H = g.H;
+  pa.W = g.W;
+  pa.rs = g.rs;
+  pa.plane_rows = g.H - 1;
+  pa.pitch = (int)align_up((size_t)(g.W / 2 + 16), 16);
+  pa.mh = g.H / 2;
+  pa.KP = (int)align_up((size_t)g.npx, 4);
+  // 8x8 ranges: per-domain-column row segments when they fit well inside L2
+  // (cfg3: 8.3 MB), else the box-floor planes (cfg5: T would be 268 MB)
+  const size_t t_bytes = (size_t)g.ndx * 2 * pa.mh * 8;
+  if (g.rs == 8 && g.st <= 16 && t_bytes <= ((size_t)48 << 20) && !getenv("FIC_POOL_PLANES"))
+    pa.trows = sc.get<unsigned long long>(t_bytes / 8);
+  else if (g.rs == 8 || g.rs == 4)
+    pa.planes = sc.get<uint8_t>((size_t)2 * pa.plane_rows * pa.pitch + 16);
+  else
+    pa.raw = sc.get<uint8_t>((size_t)g.D * pa.KP);
+  pa.st = g.st;
+  pa.ndx = g.ndx;
+  pa.D = g.D;
+  pa.order = order;
+  pa.bh = tensor_ok ? sc.get<uint16_t>((size_t)g.D * g.npx) : nullptr;
+  pa.inv_den = sc.get<double>(g.D);
+  pa.sums = sc.get<uint2>(g.D);
+  return pa;
+}
+
+static PoolView pool_view(const PoolArgs& pa) {
+  PoolView P{};
+  P.bh = pa.bh;
+  P.inv_den = pa.inv_den;
+  P.sums = pa.sums;
+  P.order = pa.order;
+  P.D = pa.D;
+  P.src.trows = pa.trows;
+  P.src.planes = pa.planes;
+  P.src.raw = pa.raw;
+  P.src.ndx = pa.ndx;
+  P.src.st = pa.st;
+  P.src.mh = pa.mh;
+  P.src.plane_rows = pa.plane_rows;
+  P.src.pitch = pa.pitch;
+  P.src.KP = pa.KP;
+  return P;
+}
+
 static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p, uint8_t* records,
                         double* pre_rms, double* post_rms, int64_t* pool_sizes,
                         fic_stats_t* st, cudaStream_t s) {
@@ -963,7 +1016,6 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
     check_dbc_side(p.fd_source == FIC_FD_ORIGINAL ? g.ds : g.rs);
     check_dbc_side(g.rs);
   }
-  if (g.npx % 4) invalid("range_size must be even on the GPU path");
   const int K = g.npx;
   const int nshard = std::max(1, p.shard_count);
   const int shard = std::min(std::max(0, p.shard_index), nshard - 1);
@@ -1031,7 +1083,8 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
   ra.n_iso = g.n_iso;
   ra.inv_perm = d_inv;
   ra.info = sc.get<RangeInfo>(g.R);
-  ra.rows = sc.get<uint8_t>((size_t)g.R * g.n_iso * K);
+  ra.KP = (int)align_up((size_t)K, 4);
+  ra.rows = sc.get<uint8_t>((size_t)g.R * g.n_iso * ra.KP);
   FIC_CUDA(cudaEventRecord(side.ev[0], s));
   FIC_CUDA(cudaStreamWaitEvent(side.s2, side.ev[0], 0));
   launch_ranges(ra, side.s2);
@@ -1040,30 +1093,7 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
   tm.mark();  // 1
 
   // K1 pool builder (side stream: needs the FD order, overlaps the planning)
-  PoolArgs pa{};
-  pa.img = img;
-  pa.H = g.H;
-  pa.W = g.W;
-  pa.rs = g.rs;
-  pa.plane_rows = g.H - 1;
-  pa.pitch = (int)align_up((size_t)(g.W / 2 + 16), 16);
-  pa.mh = g.H / 2;
-  // 8x8 ranges: per-domain-column row segments when they fit well inside L2
-  // (cfg3: 8.3 MB), else the box-floor planes (cfg5: T would be 268 MB)
-  const size_t t_bytes = (size_t)g.ndx * 2 * pa.mh * 8;
-  if (g.rs == 8 && g.st <= 16 && t_bytes <= ((size_t)48 << 20) && !getenv("FIC_POOL_PLANES"))
-    pa.trows = sc.get<unsigned long long>(t_bytes / 8);
-  else
-    pa.planes = sc.get<uint8_t>((size_t)2 * pa.plane_rows * pa.pitch);
-  pa.st = g.st;
-  pa.ndx = g.ndx;
-  pa.D = g.D;
-  pa.order = pb.order;
-  pa.raw = sc.get<uint8_t>((size_t)g.D * K);
-  pa.bh = tensor_ok ? sc.get<uint16_t>((size_t)g.D * K) : nullptr;
-  pa.inv_den = sc.get<double>(g.D);
-  pa.sums = sc.get<uint2>(g.D);
-  pa.ids = sc.get<uint32_t>(g.D);
+  PoolArgs pa = pool_args(sc, g, img, pb.order, tensor_ok);
   // FIC_POOL_SERIAL: the pool builder on the caller's stream (a measurement
   // of K1 without the planning kernels running beside it)
   const bool pool_serial = getenv("FIC_POOL_SERIAL") != nullptr;
@@ -1202,8 +1232,8 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
 
   pmark();  // 14
   FIC_CUDA(cudaStreamWaitEvent(s, side.ev[2], 0));  // join: pool + ranges
-  PoolView P{pa.raw, pa.bh, pa.inv_den, pa.sums, pa.ids, g.D};
-  RangeView Rv{ra.info, ra.rows, pb.lo, pb.hi, g.n_iso, K};
+  PoolView P = pool_view(pa);
+  RangeView Rv{ra.info, ra.rows, pb.lo, pb.hi, g.n_iso, K, ra.KP};
   tm.mark();  // 3
   if (n_tt_max && titems_n) {
     unsigned long long* thr_g = sc.get<unsigned long long>(g.R);
@@ -1330,6 +1360,70 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
       fprintf(stderr, "tc cycles: producer-empty %.3g  mma-tempty %.3g  mma-full %.3g  epi-tfull %.3g  epi-slow %.3g  epi-total %.3g  mma-loop %.3g  setup %.3g  teardown(tma warp) %.3g  items %.0f\n",
               (double)hc[4], (double)hc[5], (double)hc[6], (double)hc[7], (double)hc[8], (double)hc[9], (double)hc[10], (double)hc[11], (double)hc[12], (double)hc[13]);
   }
+}
+
+// K1 outputs in pool order, for the parity tests (fic_pool_v1): the
+// decimated pixels come through the same DomSrc gather the matchers use.
+template <int K>
+__global__ void k_dom_gather(PoolView P, uint8_t* dec) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= P.D) return;
+  uint32_t w[K / 4];
+  dom_words<K>(P, p, pool_id(P, p), w);
+  uint32_t* o = reinterpret_cast<uint32_t*>(dec + (size_t)p * K);
+#pragma unroll
+  for (int i = 0; i < K / 4; ++i) o[i] = w[i];
+}
+
+__global__ void k_raw_gather(PoolView P, int K, uint8_t* dec) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= P.D) return;
+  for (int k = 0; k < K; ++k) dec[(size_t)p * K + k] = P.src.raw[(size_t)p * P.src.KP + k];
+}
+
+static void pool_impl(const uint8_t* img, int H, int W, const fic_params_t& p, int64_t* order,
+                      uint8_t* dec, uint32_t* sums, double* inv_den, uint16_t* b_rows,
+                      cudaStream_t s) {
+  Geo g = validate(H, W, p);
+  if (p.strategy == FIC_STATIC2 || p.strategy == FIC_DYNAMIC_FD) {
+    check_dbc_side(p.fd_source == FIC_FD_ORIGINAL ? g.ds : g.rs);
+    check_dbc_side(g.rs);
+  }
+  const int K = g.npx;
+  const bool tensor_ok = tc_supported(K);
+  if (b_rows && !tensor_ok) invalid("fp16 B rows exist for 4x4 and 8x8 ranges only");
+  Scratch sc(s);
+  PlanBufs pb = make_plan(sc, s, img, g, p, false, true);
+  PoolArgs pa = pool_args(sc, g, img, pb.order, tensor_ok);
+  launch_pool(pa, s);
+  const PoolView P = pool_view(pa);
+  const unsigned blocks = (unsigned)cdiv(g.D, 256);
+  if (order) {
+    if (pb.order) {
+      k_u32_to_i64<<<blocks, 256, 0, s>>>(pb.order, order, g.D);
+    } else {
+      uint32_t* io = sc.get<uint32_t>(g.D);
+      k_iota<<<blocks, 256, 0, s>>>(io, g.D);
+      k_u32_to_i64<<<blocks, 256, 0, s>>>(io, order, g.D);
+    }
+    FIC_CHECK_LAUNCH();
+  }
+  if (dec) {
+    if (K == 64)
+      k_dom_gather<64><<<blocks, 256, 0, s>>>(P, dec);
+    else if (K == 16)
+      k_dom_gather<16><<<blocks, 256, 0, s>>>(P, dec);
+    else
+      k_raw_gather<<<blocks, 256, 0, s>>>(P, K, dec);
+    FIC_CHECK_LAUNCH();
+  }
+  if (sums)
+    FIC_CUDA(cudaMemcpyAsync(sums, pa.sums, g.D * sizeof(uint2), cudaMemcpyDeviceToDevice, s));
+  if (inv_den)
+    FIC_CUDA(cudaMemcpyAsync(inv_den, pa.inv_den, g.D * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  if (b_rows)
+    FIC_CUDA(cudaMemcpyAsync(b_rows, pa.bh, (size_t)g.D * K * 2, cudaMemcpyDeviceToDevice, s));
+  FIC_CUDA(cudaStreamSynchronize(s));
 }
 
 static void plan_impl(const uint8_t* img, int H, int W, const fic_params_t& p, double* fd_dom,
@@ -1543,6 +1637,17 @@ extern "C" int fic_plan_v1(const uint8_t* d_image, int32_t height, int32_t width
     if (!params) invalid("params must not be NULL");
     plan_impl(d_image, height, width, *params, d_fd_dom, d_fd_rng, d_order, d_slab_lo, d_slab_hi,
               h_stats, as_stream(stream));
+  });
+}
+
+extern "C" int fic_pool_v1(const uint8_t* d_image, int32_t height, int32_t width,
+                           const fic_params_t* params, int64_t* d_order, uint8_t* d_decimated,
+                           uint32_t* d_sums, double* d_inv_den, uint16_t* d_b_rows,
+                           void* stream) {
+  return guarded([&] {
+    if (!params) invalid("params must not be NULL");
+    pool_impl(d_image, height, width, *params, d_order, d_decimated, d_sums, d_inv_den, d_b_rows,
+              as_stream(stream));
   });
 }
 

@@ -68,7 +68,7 @@ __global__ void __launch_bounds__(256) k_exact(PoolView P, RangeView Rv, ExactAr
   int64_t c1 = min(hi, c0 + a.seg_len);
   const int n_iso = Rv.n_iso;
   const uint32_t* rw = reinterpret_cast<const uint32_t*>(Rv.rows + (int64_t)r * n_iso * K);
-  for (int i = threadIdx.x; i < n_iso * KW; i += blockDim.x) srow[i / KW][i % KW] = rw[i];
+  for (int i = threadIdx.x; i < n_iso * KW; i += blockDim.x) srow[i / KW][i % KW] = rw[i];  // KP == K
   __syncthreads();
   const RangeInfo inf = Rv.info[r];
   const double n = (double)K;
@@ -76,19 +76,11 @@ __global__ void __launch_bounds__(256) k_exact(PoolView P, RangeView Rv, ExactAr
   best_init(b);
   unsigned long long evals = 0;
   for (int64_t p = c0 + threadIdx.x; p < c1; p += blockDim.x) {
+    const uint32_t dom = pool_id(P, p);
     uint32_t dw[KW];
-    const uint4* src = reinterpret_cast<const uint4*>(P.raw + p * K);
-#pragma unroll
-    for (int q = 0; q < KW / 4; ++q) {
-      uint4 v = __ldg(src + q);
-      dw[4 * q] = v.x;
-      dw[4 * q + 1] = v.y;
-      dw[4 * q + 2] = v.z;
-      dw[4 * q + 3] = v.w;
-    }
+    dom_words<K>(P, p, dom, dw);
     uint2 sm = P.sums[p];
     double sd = (double)sm.x, sdd = (double)sm.y, inv = P.inv_den[p];
-    uint32_t dom = P.ids[p];
     for (int i = 0; i < n_iso; ++i) {
       uint32_t acc = 0;
 #pragma unroll
@@ -129,11 +121,12 @@ __global__ void __launch_bounds__(256) k_exact(PoolView P, RangeView Rv, ExactAr
   }
 }
 
-// Generic K (any range size whose K is a multiple of 4, K <= 1024).
+// Generic K (any range size): rows zero-padded to KP = K rounded up to a
+// multiple of 4 on both sides, so whole-word dp4a products are exact.
 __global__ void __launch_bounds__(256) k_exact_generic(PoolView P, RangeView Rv, ExactArgs a) {
   extern __shared__ uint32_t dyn[];
   __shared__ Best sbest[8];
-  const int K = Rv.K, KW = K / 4;
+  const int K = Rv.K, KP = Rv.KP, KW = KP / 4;
   int64_t n_items = a.n_items;
   const uint32_t* elist = a.elist;
   if (a.plan) {  // device-side work count (n_items is then a bound)
@@ -147,7 +140,7 @@ __global__ void __launch_bounds__(256) k_exact_generic(PoolView P, RangeView Rv,
   int64_t c0 = lo + (int64_t)item.y * a.seg_len;
   int64_t c1 = min(hi, c0 + a.seg_len);
   const int n_iso = Rv.n_iso;
-  const uint32_t* rw = reinterpret_cast<const uint32_t*>(Rv.rows + (int64_t)r * n_iso * K);
+  const uint32_t* rw = reinterpret_cast<const uint32_t*>(Rv.rows + (int64_t)r * n_iso * KP);
   for (int i = threadIdx.x; i < n_iso * KW; i += blockDim.x) dyn[i] = rw[i];
   __syncthreads();
   const RangeInfo inf = Rv.info[r];
@@ -156,10 +149,10 @@ __global__ void __launch_bounds__(256) k_exact_generic(PoolView P, RangeView Rv,
   best_init(b);
   unsigned long long evals = 0;
   for (int64_t p = c0 + threadIdx.x; p < c1; p += blockDim.x) {
-    const uint32_t* dw = reinterpret_cast<const uint32_t*>(P.raw + p * K);
+    const uint32_t* dw = reinterpret_cast<const uint32_t*>(P.src.raw + p * KP);
     uint2 sm = P.sums[p];
     double sd = (double)sm.x, sdd = (double)sm.y, inv = P.inv_den[p];
-    uint32_t dom = P.ids[p];
+    const uint32_t dom = pool_id(P, p);
     for (int i = 0; i < n_iso; ++i) {
       uint32_t acc = 0;
       for (int q = 0; q < KW; ++q) acc = __dp4a(__ldg(dw + q), dyn[i * KW + q], acc);
@@ -200,7 +193,6 @@ __global__ void __launch_bounds__(256) k_exact_generic(PoolView P, RangeView Rv,
 
 void launch_exact(const PoolView& P, const RangeView& Rv, const ExactArgs& a, cudaStream_t s) {
   if (a.n_items == 0) return;
-  if (Rv.K % 4) invalid("range_size * range_size must be a multiple of 4 on the GPU path");
   // one block per item; with a device-side count, a grid-stride loop over
   // at most 4 blocks per SM
   unsigned grid = (unsigned)(a.plan ? std::min<int64_t>(a.n_items, 148 * 4) : a.n_items);
@@ -209,7 +201,7 @@ void launch_exact(const PoolView& P, const RangeView& Rv, const ExactArgs& a, cu
   else if (Rv.K == 16)
     k_exact<16><<<grid, 256, 0, s>>>(P, Rv, a);
   else
-    k_exact_generic<<<grid, 256, (size_t)Rv.n_iso * Rv.K, s>>>(P, Rv, a);
+    k_exact_generic<<<grid, 256, (size_t)Rv.n_iso * Rv.KP, s>>>(P, Rv, a);
   FIC_CHECK_LAUNCH();
 }
 

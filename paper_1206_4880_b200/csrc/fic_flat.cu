@@ -80,7 +80,7 @@ __global__ void __launch_bounds__(256) k_flat_best(PoolView P, FlatArgs a) {
       const double sd = (double)sm.x;
       const Cand q = eval_candidate(__dmul_rn(cd, sd), sd, (double)sm.y, __ldg(P.inv_den + p), sr,
                                     srr, n);
-      const FlatArgs::Best x{q.err, __ldg(P.ids + p), q.sq, q.oq, 0};
+      const FlatArgs::Best x{q.err, pool_id(P, p), q.sq, q.oq, 0};
       if (flat_better(x, b)) b = x;
     }
     red[threadIdx.x] = b;

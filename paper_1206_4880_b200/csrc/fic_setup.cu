@@ -721,14 +721,46 @@ void launch_slabs(const SlabArgs& a, cudaStream_t s) {
 // I[y+1][x+1]) >> 2 with x = 2k + par.  A decimated domain row (blocks.py:
 // 75-82) is then RS consecutive bytes of one plane row, so a domain is RS
 // short row reads from a 2 x (H-1) x W/2 byte array that stays in L2.
-__global__ void k_boxplanes(const uint8_t* img, int H, int W, int pitch, uint8_t* planes) {
-  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  int64_t n = (int64_t)(H - 1) * (W - 1);
-  if (t >= n) return;
-  int y = (int)(t / (W - 1)), x = (int)(t - (int64_t)y * (W - 1));
-  const uint8_t* q = img + (int64_t)y * W + x;
-  uint8_t v = (uint8_t)((q[0] + q[1] + q[W] + q[W + 1]) >> 2);
-  planes[((int64_t)(x & 1) * (H - 1) + y) * pitch + (x >> 1)] = v;
+__global__ void __launch_bounds__(256) k_boxplanes(const uint8_t* img, int H, int W, int pitch,
+                                                   uint8_t* planes) {
+  // one thread: 16 consecutive x of one row y (x0 = 16 t): rows y and y + 1
+  // as five 4-byte loads each (W % 4 == 0 for 4x4 / 8x8 ranges, so x0 + 16 <
+  // W implies x0 + 20 <= W), 8 outputs to each parity plane (8-byte stores)
+  const int tx = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y;
+  const int x0 = 16 * tx;
+  if (x0 >= W - 1 || y >= H - 1) return;
+  const uint8_t* r0 = img + (int64_t)y * W + x0;
+  const uint8_t* r1 = r0 + W;
+  uint32_t a[5], b[5];
+  const bool more = x0 + 16 < W;
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+    const bool ok = k < 4 || more;
+    a[k] = ok ? __ldg(reinterpret_cast<const uint32_t*>(r0) + k) : 0u;
+    b[k] = ok ? __ldg(reinterpret_cast<const uint32_t*>(r1) + k) : 0u;
+  }
+  // vertical pair sums of bytes i, i+1 in 16-bit lanes, then the 2x2 sums
+  uint32_t ev[4], od[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    // bytes 4k .. 4k+4 of both rows
+    const uint32_t lo_a = __byte_perm(a[k], 0, 0x4240), hi_a = __byte_perm(a[k], 0, 0x4341);
+    const uint32_t lo_b = __byte_perm(b[k], 0, 0x4240), hi_b = __byte_perm(b[k], 0, 0x4341);
+    const uint32_t nx_a = __byte_perm(a[k], a[k + 1], 0x4442), nx_b = __byte_perm(b[k], b[k + 1], 0x4442);
+    const uint32_t v_e = lo_a + lo_b;   // v[4k], v[4k+2]
+    const uint32_t v_o = hi_a + hi_b;   // v[4k+1], v[4k+3]
+    const uint32_t v_n = __byte_perm(nx_a, 0, 0x4240) + __byte_perm(nx_b, 0, 0x4240);  // v[4k+2], v[4k+4]
+    ev[k] = ((v_e + v_o) >> 2) & 0x00ff00ffu;  // x = 4k, 4k+2
+    od[k] = ((v_o + v_n) >> 2) & 0x00ff00ffu;  // x = 4k+1, 4k+3
+  }
+  const unsigned long long e = (unsigned long long)__byte_perm(ev[0], ev[1], 0x6420) |
+                               ((unsigned long long)__byte_perm(ev[2], ev[3], 0x6420) << 32);
+  const unsigned long long o = (unsigned long long)__byte_perm(od[0], od[1], 0x6420) |
+                               ((unsigned long long)__byte_perm(od[2], od[3], 0x6420) << 32);
+  uint8_t* p0 = planes + (int64_t)y * pitch + (x0 >> 1);
+  uint8_t* p1 = planes + ((int64_t)(H - 1) + y) * pitch + (x0 >> 1);
+  *reinterpret_cast<unsigned long long*>(p0) = e;
+  *reinterpret_cast<unsigned long long*>(p1) = o;
 }
 
 // 8 bytes starting at byte offset k of an 8-byte aligned, padded row
@@ -891,12 +923,7 @@ __global__ void __launch_bounds__(256, 8) k_pool(PoolArgs a) {
       my_sd = t_sd;
       my_sdd = t_sdd;
     }
-    if (!ok) continue;
-    if (RS == 8)
-      reinterpret_cast<uint2*>(a.raw + (size_t)p * K)[i] = make_uint2(w0, w1);
-    else
-      reinterpret_cast<uint32_t*>(a.raw + (size_t)p * K)[i] = w0;
-    if (!a.bh) continue;
+    if (!ok || !a.bh) continue;
     // B row: fp16(fp32(K x - sum_d) * rsqrt(K den)); x from the byte via
     // 0x4B0000xx - 2^23 (exact), K x - sum_d by an exact FMA (|.| < 2^24),
     // packed fp32 pairs.  rsqrtf's ~2 ulp are far inside the screen's slack.
@@ -924,7 +951,6 @@ __global__ void __launch_bounds__(256, 8) k_pool(PoolArgs a) {
     const int64_t den = (int64_t)K * my_sdd - (int64_t)my_sd * my_sd;
     a.inv_den[pm] = den != 0 ? __ddiv_rn(1.0, (double)den) : 0.0;
     a.sums[pm] = make_uint2(my_sd, my_sdd);
-    a.ids[pm] = my_id;
   }
 }
 
@@ -936,18 +962,19 @@ __global__ void k_pool_generic(PoolArgs a, int rs) {
   int dy = (int)(id / (uint32_t)a.ndx), dx = (int)(id - (uint32_t)dy * a.ndx);
   const uint8_t* base = a.img + (int64_t)dy * a.st * a.W + (int64_t)dx * a.st;
   uint32_t sd = 0, sdd = 0;
+  uint8_t* out = a.raw + (size_t)p * a.KP;
   for (int i = 0; i < rs; ++i)
     for (int j = 0; j < rs; ++j) {
       const uint8_t* q = base + (int64_t)(2 * i) * a.W + 2 * j;
       uint32_t x = (q[0] + q[1] + q[a.W] + q[a.W + 1]) >> 2;
-      a.raw[p * K + i * rs + j] = (uint8_t)x;
+      out[i * rs + j] = (uint8_t)x;
       sd += x;
       sdd += x * x;
     }
+  for (int k = K; k < a.KP; ++k) out[k] = 0;  // zero padding: dp4a over whole words
   int64_t den = (int64_t)K * sdd - (int64_t)sd * sd;
   a.inv_den[p] = den != 0 ? __ddiv_rn(1.0, (double)den) : 0.0;
   a.sums[p] = make_uint2(sd, sdd);
-  a.ids[p] = id;
 }
 
 void launch_pool(const PoolArgs& a, cudaStream_t s) {
@@ -964,8 +991,8 @@ void launch_pool(const PoolArgs& a, cudaStream_t s) {
     if (a.ev_main) FIC_CUDA(cudaEventRecord(a.ev_main, s));
     k_pool<8><<<blocks, 256, 0, s>>>(a);
   } else if ((a.rs == 8 || a.rs == 4) && a.planes) {
-    const int64_t n = (int64_t)(a.H - 1) * (a.W - 1);
-    k_boxplanes<<<(unsigned)cdiv(n, 256), 256, 0, s>>>(a.img, a.H, a.W, a.pitch, a.planes);
+    dim3 grid((unsigned)cdiv(cdiv(a.W - 1, 16), 256), (unsigned)(a.H - 1));
+    k_boxplanes<<<grid, 256, 0, s>>>(a.img, a.H, a.W, a.pitch, a.planes);
     FIC_CHECK_LAUNCH();
     if (a.ev_main) FIC_CUDA(cudaEventRecord(a.ev_main, s));
     if (a.rs == 8)
@@ -1004,12 +1031,14 @@ __global__ void k_ranges(RangeArgs a) {
   inf.rho = (int32_t)((2 * sr + K) / (2 * K));
   inf.pad = 0;
   a.info[r] = inf;
-  uint8_t* out = a.rows + (int64_t)r * a.n_iso * K;
-  for (int i = 0; i < a.n_iso; ++i)
+  uint8_t* out = a.rows + (int64_t)r * a.n_iso * a.KP;
+  for (int i = 0; i < a.n_iso; ++i) {
     for (int k = 0; k < K; ++k) {
       int src = a.inv_perm[i * K + k];
-      out[i * K + k] = base[(int64_t)(src / rs) * a.W + (src % rs)];
+      out[i * a.KP + k] = base[(int64_t)(src / rs) * a.W + (src % rs)];
     }
+    for (int k = K; k < a.KP; ++k) out[i * a.KP + k] = 0;
+  }
 }
 
 // RS = 8 fast path: one thread per (range, isometry); rows are aligned 8-byte

@@ -387,19 +387,21 @@ __global__ void __maxnreg__(MAXREG)
   unsigned long long gt_start = 0;  // debug & 8192: per-CTA start / end (globaltimer, ns)
   if (DBG && (debug & 8192) && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt_start));
 
-  // exact rescoring of pool position p (codec.py:218-258 via eval_candidate)
-  auto exact = [&](int64_t p, int erow, double esr, double esrr) -> Cand {
+  // exact rescoring of pool position p, raster id `id` (codec.py:218-258
+  // via eval_candidate); the domain's pixels come from the pool builder's
+  // L2-resident row segments / planes (DomSrc)
+  auto exact = [&](int64_t p, uint32_t id, int erow, double esr, double esrr) -> Cand {
+    uint32_t dw[C::KW];
+    dom_words<K>(P, p, id, dw);
     uint32_t acc32 = 0;
-    const uint4* src = reinterpret_cast<const uint4*>(P.raw + p * K);
     const uint4* rrow = reinterpret_cast<const uint4*>(sRows + erow * K);
 #pragma unroll
     for (int w4 = 0; w4 < C::KW / 4; ++w4) {
-      const uint4 dv = __ldg(src + w4);
       const uint4 rv = rrow[w4];
-      acc32 = __dp4a(dv.x, rv.x, acc32);
-      acc32 = __dp4a(dv.y, rv.y, acc32);
-      acc32 = __dp4a(dv.z, rv.z, acc32);
-      acc32 = __dp4a(dv.w, rv.w, acc32);
+      acc32 = __dp4a(dw[4 * w4], rv.x, acc32);
+      acc32 = __dp4a(dw[4 * w4 + 1], rv.y, acc32);
+      acc32 = __dp4a(dw[4 * w4 + 2], rv.z, acc32);
+      acc32 = __dp4a(dw[4 * w4 + 3], rv.w, acc32);
     }
     const uint2 sm = __ldg(P.sums + p);
     return eval_candidate((double)acc32, (double)sm.x, (double)sm.y, __ldg(P.inv_den + p), esr,
@@ -700,7 +702,8 @@ __global__ void __maxnreg__(MAXREG)
               for (int q = 0; q < CH; ++q) eq |= (fabsf(v[q]) == bv) ? (1ull << q) : 0ull;
               const int e = __ffsll((long long)(eq & wmask)) - 1;
               wmask &= ~(1ull << e);
-              tnew = fmax(exact(c0 + rel + e, row, sr, srr).err, 0.0);
+              const int64_t pe = c0 + rel + e;
+              tnew = fmax(exact(pe, pool_id(P, pe), row, sr, srr).err, 0.0);
               ++evals;
               push((uint32_t)(rel + e));  // the rescorer records it
             }
@@ -881,8 +884,8 @@ __global__ void __maxnreg__(MAXREG)
           for (int e = 0; e < NE; ++e) {
             rr[e] = got[e] >= 0 ? t + RSTRIDE * got[e] : t + RSTRIDE * got[0];
             const int64_t p = c0 + (got[e] >= 0 ? rel[e] : rel[0]);
-            cd[e] = exact(p, rr[e], rstate[rr[e]].sr, rstate[rr[e]].srr);
-            did[e] = __ldg(P.ids + p);
+            did[e] = pool_id(P, p);
+            cd[e] = exact(p, did[e], rr[e], rstate[rr[e]].sr, rstate[rr[e]].srr);
           }
 #pragma unroll
           for (int e = 0; e < NE; ++e)

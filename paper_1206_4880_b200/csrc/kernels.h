@@ -88,11 +88,11 @@ struct PoolArgs {
   int mh;                     // domain's 8 rows are 64 contiguous bytes (scratch)
   int64_t D;
   const uint32_t* order;   // raster id per pool position (nullptr = identity)
-  uint8_t* raw;            // [D][K] decimated pixels, pool order
+  uint8_t* raw;            // generic sizes only: [D][KP] decimated pixels, pool order, zero-padded
+  int KP;                  // raw row pitch
   uint16_t* bh;            // [D][K] fp16 centred unit-norm rows (nullptr = skip)
   double* inv_den;         // [D]
   uint2* sums;             // [D] (sum_d, sum_dd)
-  uint32_t* ids;           // [D] raster id per pool position (copy of order)
   cudaEvent_t ev_main;     // optional: recorded just before the main kernel (k_pool)
 };
 void launch_pool(const PoolArgs& a, cudaStream_t s);
@@ -103,7 +103,8 @@ struct RangeArgs {
   int W, rs, nrx, R, n_iso;
   const int* inv_perm;     // [8][K] device
   RangeInfo* info;         // [R]
-  uint8_t* rows;           // [R][n_iso][K] permuted range pixels
+  uint8_t* rows;           // [R][n_iso][KP] permuted range pixels (zero-padded rows)
+  int KP;
 };
 void launch_ranges(const RangeArgs& a, cudaStream_t s);
 

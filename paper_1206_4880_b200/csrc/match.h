@@ -4,23 +4,90 @@
 
 namespace fic {
 
+// Where the matchers read a domain's decimated pixels (blocks.py:75-82).
+// The pool builder does not write a per-pool-position copy of them: the
+// rescorers and the exact matcher gather a domain by raster id from the
+// pool builder's own L2-resident intermediates.
+struct DomSrc {
+  const unsigned long long* trows;  // RS 8: [ndx][2][mh] row segments; domain (Y, X) =
+                                    // 8 consecutive words at (dx * 2 + (Y & 1)) * mh + (Y >> 1)
+  const uint8_t* planes;            // RS 4/8: [2][plane_rows][pitch] box-floor planes
+  const uint8_t* raw;               // other sizes: [D][KP] pool order, rows zero-padded to KP
+  int ndx, st, mh, plane_rows, pitch;
+  int KP;                           // raw row pitch (K rounded up to a multiple of 4)
+};
+
 // Column (domain) data in pool order, produced by the pool builder (K1).
 struct PoolView {
-  const uint8_t* raw;      // [D][K]
   const uint16_t* bh;      // [D][K] fp16 bits (tensor path)
   const double* inv_den;   // [D]
   const uint2* sums;       // [D] (sum_d, sum_dd)
-  const uint32_t* ids;     // [D] raster domain index
+  const uint32_t* order;   // [D] raster domain index per pool position (nullptr = identity)
+  DomSrc src;
   int64_t D;
 };
+
+__device__ __forceinline__ uint32_t pool_id(const PoolView& P, int64_t p) {
+  return P.order ? __ldg(P.order + p) : (uint32_t)p;
+}
+
+// 4 bytes starting at byte address q (4-byte aligned loads + funnel shift)
+__device__ __forceinline__ uint32_t bytes4_at(const uint8_t* q) {
+  const uintptr_t u = reinterpret_cast<uintptr_t>(q);
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(u & ~(uintptr_t)3);
+  return __funnelshift_r(__ldg(w), __ldg(w + 1), (uint32_t)(u & 3) * 8);
+}
+
+// The K/4 little-endian words of the decimated domain at pool position p
+// (raster id `id`), K = 64 or 16 (RS 8 / 4).
+template <int K>
+__device__ __forceinline__ void dom_words(const PoolView& P, int64_t p, uint32_t id,
+                                          uint32_t (&w)[K / 4]) {
+  constexpr int RS = K == 64 ? 8 : 4;
+  const DomSrc& d = P.src;
+  const uint32_t dy = id / (uint32_t)d.ndx, dx = id - dy * (uint32_t)d.ndx;
+  const uint32_t Y = dy * d.st, X = dx * d.st;
+  if (RS == 8 && d.trows) {
+    const unsigned long long* t = d.trows + ((size_t)dx * 2 + (Y & 1)) * d.mh + (Y >> 1);
+#pragma unroll
+    for (int i = 0; i < RS; ++i) {
+      const unsigned long long v = __ldg(t + i);
+      w[2 * i] = (uint32_t)v;
+      w[2 * i + 1] = (uint32_t)(v >> 32);
+    }
+  } else if (d.planes) {
+    const uint8_t* b = d.planes + (size_t)(X & 1) * d.plane_rows * d.pitch + (size_t)Y * d.pitch +
+                       (X >> 1);
+#pragma unroll
+    for (int i = 0; i < RS; ++i) {
+      if (RS == 8) {
+        const uint8_t* q = b + (size_t)(2 * i) * d.pitch;
+        w[2 * i] = bytes4_at(q);
+        w[2 * i + 1] = bytes4_at(q + 4);
+      } else {
+        w[i] = bytes4_at(b + (size_t)(2 * i) * d.pitch);
+      }
+    }
+  } else {
+    const uint4* q = reinterpret_cast<const uint4*>(d.raw + (size_t)p * K);
+#pragma unroll
+    for (int i = 0; i < K / 16; ++i) {
+      const uint4 v = __ldg(q + i);
+      w[4 * i] = v.x;
+      w[4 * i + 1] = v.y;
+      w[4 * i + 2] = v.z;
+      w[4 * i + 3] = v.w;
+    }
+  }
+}
 
 // Range data (raster index).
 struct RangeView {
   const RangeInfo* info;   // [R]
-  const uint8_t* rows;     // [R][n_iso][K] permuted pixels
+  const uint8_t* rows;     // [R][n_iso][KP] permuted pixels (rows zero-padded to KP)
   const int32_t* lo;       // [R] slab start (pool order)
   const int32_t* hi;       // [R] slab end
-  int n_iso, K;
+  int n_iso, K, KP;        // KP: row pitch, K rounded up to a multiple of 4
 };
 
 // Work counts of one encode, computed on the device by the planner

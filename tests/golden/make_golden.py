@@ -322,6 +322,49 @@ def bench_cases():
     print(f"wrote {path} ({os.path.getsize(path)} bytes)")
 
 
+def odd_cases():
+    """Range sizes other than 4 and 8 (odd and non-power-of-two sides) through
+    the reference's own encode / decode, and dbc_grid on side-12/24 stacks
+    (fdim.py:26-34,73-76: h = s*256/M is not an integer there)."""
+    out = {}
+    cases = [
+        ("rand60_ex_r5_s3_iso", rand((60, 60), 61), "exhaustive", 5, 3, True),
+        ("rand60_ns_r5_s2_iso", rand((60, 60), 62), "nosearch", 5, 2, True),
+        ("rand48_ex_r6_s4_iso", rand((48, 48), 63), "exhaustive", 6, 4, True),
+        ("rand36_ex_r3_s1", rand((36, 36), 64), "exhaustive", 3, 1, False),
+        ("rand72_dyn_r12_s4_iso", rand((72, 72), 65), "dynamic_fd", 12, 4, True),
+        ("rand96_st2_r12_s6_iso", rand((96, 96), 66), "static2", 12, 6, True),
+        ("rand40_ex_r2_s1_iso", rand((40, 40), 67), "exhaustive", 2, 1, True),
+    ]
+    for name, img, strat, rs, stride, iso in cases:
+        code, st = rcodec.encode(img, strat, range_size=rs, domain_size=2 * rs, stride=stride,
+                                 isometries=iso)
+        out[f"{name}.image"] = img
+        out[f"{name}.params"] = np.array([stride, int(iso), rcodec.STRATEGY_IDS[strat], rs, 2 * rs])
+        out[f"{name}.records"] = code.records.view(np.uint8).reshape(-1, 7)
+        out[f"{name}.pre_rms"] = st.pre_rms
+        out[f"{name}.post_rms"] = st.post_rms
+        out[f"{name}.pool_sizes"] = st.pool_sizes
+        out[f"{name}.stats"] = np.array([st.comparisons, st.mean_pool_size])
+        out[f"{name}.decoded"] = rcodec.decode(code, iterations=10)
+        if strat in ("dynamic_fd", "static2"):
+            h = harness_encode(img, strat, range_size=rs, domain_size=2 * rs, stride=stride,
+                               isometries=iso)
+            assert np.array_equal(h["records"], code.records), name
+            out[f"{name}.fd_dom"] = h["fd_dom"]
+            out[f"{name}.fd_rng"] = h["fd_rng"]
+            out[f"{name}.slab_lo"] = h["slab_lo"]
+            out[f"{name}.slab_hi"] = h["slab_hi"]
+    for side in (12, 24, 20, 48):
+        stk = rand((50, side, side), 100 + side)
+        stk[0] = 0
+        stk[1] = 255
+        out[f"dbc{side}.blocks"] = stk
+        out[f"dbc{side}.fd"] = rfdim.dbc_grid(stk)
+        out[f"dbc{side}.raw"] = rfdim.dbc_grid(stk, clamp=False)
+    save("odd_cases.npz", **out)
+
+
 def decode_cases():
     """decode_iterates snapshots, float initial images and isometry bytes > 7
     through the reference's own decoder (codec.py:516-598), plus the scalar
@@ -382,3 +425,4 @@ if __name__ == "__main__":
         delta_cases()
         bench_cases()
         decode_cases()
+        odd_cases()

@@ -14,7 +14,7 @@ Outputs ``tests/golden/scale_<cfg>.npz``:
 * cfg2: all 4,096 ranges (dynamic_fd, delta 0.1) and all 4,096 exhaustive;
 * cfg3: all 16,384 ranges (dynamic_fd, delta 0.05);
 * cfg4: all 65,536 ranges (exhaustive, 4x4 ranges);
-* cfg5: 64 ranges (the empty-window ranges first, then seeded random ones)
+* cfg5: 1,024 ranges (16 empty-window ranges, then seeded random ones)
   plus the full pool sizes and SHA-256 checksums of the slabs, range FDs and
   FD order (the reference's cfg5 setup peaks near 41 GB of host RAM);
 * k1: the pool builder's inputs to the matcher (blocks.py:75-82,
@@ -126,7 +126,7 @@ def case_cfg4(workers):
     save("scale_cfg4.npz", **full_case("cfg4", "exhaustive", None, workers, "cfg4_ex"))
 
 
-def case_cfg5(workers, n_pick=64):
+def case_cfg5(workers, n_pick=1024):
     cfg = synth.CONFIGS["cfg5"]
     img = cfg.make()
     t0 = time.perf_counter()

@@ -448,3 +448,34 @@ def test_encode_on_a_second_device_after_the_first():
     a, _ = codec.encode(img, "dynamic_fd", stride=8, isometries=True, device=0)
     b, _ = codec.encode(img, "dynamic_fd", stride=8, isometries=True, device=1)
     assert a == b
+
+
+ODD = load_golden("odd_cases.npz")
+ODD_CASES = cases(ODD)
+
+
+@pytest.mark.parametrize("matcher", ["auto", "exact"])
+@pytest.mark.parametrize("name", ODD_CASES)
+def test_odd_and_non_pow2_range_sizes_match_reference(name, matcher):
+    kw, strat = _params(ODD, name)
+    code, st = codec.encode(ODD[f"{name}.image"], strat, matcher=matcher, **kw)
+    assert np.array_equal(code.records, _recs(ODD[f"{name}.records"]))
+    assert np.array_equal(st.pre_rms, ODD[f"{name}.pre_rms"])
+    assert np.array_equal(st.post_rms, ODD[f"{name}.post_rms"])
+    assert np.array_equal(st.pool_sizes, ODD[f"{name}.pool_sizes"])
+    assert st.comparisons == int(ODD[f"{name}.stats"][0])
+    if f"{name}.slab_lo" in ODD:
+        p = codec.plan(ODD[f"{name}.image"], strat, range_size=kw["range_size"],
+                       domain_size=kw["domain_size"], stride=kw["stride"])
+        assert np.array_equal(p["fd_dom"], ODD[f"{name}.fd_dom"])
+        assert np.array_equal(p["fd_rng"], ODD[f"{name}.fd_rng"])
+        assert np.array_equal(p["slab_lo"], ODD[f"{name}.slab_lo"])
+        assert np.array_equal(p["slab_hi"], ODD[f"{name}.slab_hi"])
+    assert np.array_equal(codec.decode(code, 10), ODD[f"{name}.decoded"])
+
+
+@pytest.mark.parametrize("side", [12, 20, 24, 48])
+def test_dbc_grid_non_pow2_sides_match_reference(side):
+    blocks = ODD[f"dbc{side}.blocks"]
+    assert np.array_equal(codec.dbc_grid(blocks), ODD[f"dbc{side}.fd"])
+    assert np.array_equal(codec.dbc_grid(blocks, clamp=False), ODD[f"dbc{side}.raw"])

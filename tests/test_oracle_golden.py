@@ -125,3 +125,24 @@ def test_oracle_validation_messages():
         orc.encode(img, "dynamic_fd", range_size=4, domain_size=8)
     with pytest.raises(ValueError, match="not divisible"):
         orc.encode(np.zeros((60, 64), np.uint8), "exhaustive")
+
+
+ODD = load_golden("odd_cases.npz")
+
+
+@pytest.mark.parametrize("name", cases(ODD))
+def test_oracle_odd_range_sizes_match_reference(name):
+    stride, iso, sid, rs, ds = (int(v) for v in ODD[f"{name}.params"])
+    res = orc.encode(ODD[f"{name}.image"], orc.STRATEGIES[sid], range_size=rs, domain_size=ds,
+                     stride=stride, isometries=bool(iso))
+    want = np.ascontiguousarray(ODD[f"{name}.records"]).view(orc.RECORD_DTYPE).ravel()
+    assert np.array_equal(res.records, want)
+    assert np.array_equal(res.pre_rms, ODD[f"{name}.pre_rms"])
+    assert np.array_equal(res.post_rms, ODD[f"{name}.post_rms"])
+
+
+@pytest.mark.parametrize("side", [12, 20, 24, 48])
+def test_oracle_dbc_non_pow2_sides(side):
+    blocks = ODD[f"dbc{side}.blocks"]
+    assert np.array_equal(orc.dbc(blocks), ODD[f"dbc{side}.fd"])
+    assert np.array_equal(orc.dbc(blocks, clamp=False), ODD[f"dbc{side}.raw"])

@@ -125,3 +125,35 @@ def test_cfg5_ranges_pools_and_slabs_match_reference():
     assert _sha(p["order"]) == str(g["cfg5.ids_sha"])
     fd = p["fd_dom"]
     assert [fd.sum(), fd.min(), fd.max()] == list(g["cfg5.fd_dom_sum"])
+
+
+@pytest.mark.parametrize("cname", ["cfg2", "cfg3"])
+@pytest.mark.parametrize("strategy,planes", [("exhaustive", False), ("dynamic_fd", False),
+                                             ("dynamic_fd", True)])
+def test_pool_builder_outputs_match_reference(cname, strategy, planes, monkeypatch):
+    """K1 directly: decimated domains, sum_d, sum_dd and inv_den bitwise equal
+    to the reference's downsample2(domain_stack) and _SearchContext (raster
+    order, SHA-256 of the whole arrays + 4,096 sampled rows), through the
+    row-segment and the box-plane sources."""
+    g = _golden("scale_k1.npz")
+    img = synth.CONFIGS[cname].make()
+    if _sha(img) != str(g[f"{cname}.sha"]):
+        pytest.skip("synthetic generator output differs on this host")
+    if planes:
+        monkeypatch.setenv("FIC_POOL_PLANES", "1")
+    st = int(g[f"{cname}.stride"][0])
+    out = codec.pool(img, strategy, range_size=8, domain_size=16, stride=st, delta=0.05)
+    inv = np.argsort(out["order"])          # raster id -> pool position
+    dec = out["decimated"][inv]
+    sum_d = out["sum_d"][inv].astype(np.float64)
+    sum_dd = out["sum_dd"][inv].astype(np.float64)
+    inv_den = out["inv_den"][inv]
+    pick = g[f"{cname}.pick"]
+    assert np.array_equal(dec[pick], g[f"{cname}.dec_pick"])
+    assert np.array_equal(sum_d[pick], g[f"{cname}.sum_d_pick"])
+    assert np.array_equal(sum_dd[pick], g[f"{cname}.sum_dd_pick"])
+    assert np.array_equal(inv_den[pick], g[f"{cname}.inv_den_pick"])
+    assert _sha(dec) == str(g[f"{cname}.dec_sha"])
+    assert _sha(sum_d) == str(g[f"{cname}.sum_d_sha"])
+    assert _sha(sum_dd) == str(g[f"{cname}.sum_dd_sha"])
+    assert _sha(inv_den) == str(g[f"{cname}.inv_den_sha"])
