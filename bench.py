@@ -305,29 +305,65 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
-def _pool_roofline(stats, peak_gbs, src, serial_stats=None):
-    """HBM roofline of the pool builder's main kernel k_pool (DESIGN.md
-    section 4): algorithmic bytes per domain = 4 B order entry read + 3K + 20 B
-    written (raw K u8, fp16 B row 2K, inv_den 8, sums 8, ids 4), over its
-    device time in the timed steps (CUDA events on the side stream it runs on,
-    next to the planning kernels).  `isolated` repeats the measurement with
-    the pool builder alone on the main stream (FIC_POOL_SERIAL, untimed
-    encodes); `k1_ms` is the whole pool builder (row segments + k_pool) in
-    the timed steps."""
-    D, K = 1009 * 1009, 64
-    nbytes = D * (4 + 3 * K + 20)
+def _k1_traffic():
+    """ncu dram bytes (read + write) per launch of k_pool / k_domrows at
+    cfg3, from the committed profile summary (profiles/k1_traffic.json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "k1_traffic.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+def _pool_roofline(stats, peak_gbs, src, serial_stats=None, H=1024, W=1024, D=1009 * 1009, K=64):
+    """HBM roofline of the pool builder K1 on SURVEY §8(d)'s algorithmic
+    bytes: H*W image bytes read + D*(2K + 16) written (fp16 B row, sum_d and
+    sum_dd u32, inv_den f64) = 147.6 MB at cfg3.  Reported for the main
+    kernel k_pool alone and for the whole K1 stage (row segments k_domrows +
+    k_pool), each over its device time in the timed steps (CUDA events on the
+    side stream K1 runs on, beside the planning kernels) and `isolated`
+    (FIC_POOL_SERIAL: K1 alone on the main stream, untimed encodes)."""
+    nbytes = H * W + D * (2 * K + 16)
     ms = float(np.mean([s["ms_pool_main"] for s in stats]))
+    ms_k1 = float(np.mean([s["ms_pool"] for s in stats]))
     gbs = nbytes / (ms / 1e3) / 1e9 if ms > 0 else 0.0
+    g_k1 = nbytes / (ms_k1 / 1e3) / 1e9 if ms_k1 > 0 else 0.0
+    tr = _k1_traffic()
     out = {"bound": "hbm", "kernel": "k_pool (pool builder K1 main kernel)", "achieved": gbs,
            "peak": peak_gbs, "unit": "GB/s", "frac": gbs / peak_gbs,
-           "peak_source": f"{src} copy bandwidth", "algorithmic_bytes_per_launch": nbytes,
-           "ms_per_launch": ms, "k1_ms": float(np.mean([s["ms_pool"] for s in stats])),
-           "traffic": None}
+           "peak_source": f"{src} copy bandwidth",
+           "algorithmic_bytes_per_launch": nbytes,
+           "bytes_rule": "SURVEY 8(d): H*W + D*(2K+16)", "ms_per_launch": ms,
+           "traffic": tr.get("k_pool"),
+           "k1_stage": {"kernels": "k_domrows + k_pool", "ms": ms_k1, "achieved": g_k1,
+                        "frac": g_k1 / peak_gbs,
+                        "traffic": (tr["k_pool"] + tr["k_domrows"]) if "k_domrows" in tr else None}}
     if serial_stats:
         ms_s = float(np.median([s["ms_pool_main"] for s in serial_stats]))
+        ms_s1 = float(np.median([s["ms_pool"] for s in serial_stats]))
         g_s = nbytes / (ms_s / 1e3) / 1e9 if ms_s > 0 else 0.0
-        out["isolated"] = {"ms_per_launch": ms_s, "achieved": g_s, "frac": g_s / peak_gbs}
+        g_s1 = nbytes / (ms_s1 / 1e3) / 1e9 if ms_s1 > 0 else 0.0
+        out["isolated"] = {"ms_per_launch": ms_s, "achieved": g_s, "frac": g_s / peak_gbs,
+                           "k1_stage_ms": ms_s1, "k1_stage_frac": g_s1 / peak_gbs}
     return out
+
+
+def _parity_vs_reference(records, pre, post):
+    """Records of the timed encode against the reference's own cfg3 outputs
+    (tests/golden/scale_cfg3.npz, every range): mismatches and near-ties
+    (|E - E_ref| <= 1e-6 E_ref)."""
+    path = os.path.join(ROOT, "tests", "golden", "scale_cfg3.npz")
+    try:
+        with np.load(path) as z:
+            want, wpre, wpost = z["cfg3.records"], z["cfg3.pre_rms"], z["cfg3.post_rms"]
+    except Exception as e:  # pragma: no cover
+        return {"error": str(e)}
+    bad = np.flatnonzero((records != want).any(axis=1))
+    e_got, e_ref = post[bad] ** 2, wpost[bad] ** 2
+    near = int(np.count_nonzero(np.abs(e_got - e_ref) <= 1e-6 * e_ref))
+    return {"ranges": int(len(want)), "record_mismatches": int(len(bad)), "near_ties": near,
+            "rms_bit_exact": bool(np.array_equal(pre, wpre) and np.array_equal(post, wpost)),
+            "against": "reference fic.codec._search_chunk on every cfg3 range"}
 
 
 def run_ours(args):
@@ -387,6 +423,12 @@ def run_ours(args):
     serial_stats = [step() for _ in range(3)] if world == 1 else None
     os.environ.pop("FIC_POOL_SERIAL", None)
 
+    # the timed encode's records against the reference's own (rank 0, 1 GPU)
+    parity = None
+    if world == 1:
+        r = codec.encode_device(d_img, "dynamic_fd", **CFG)
+        parity = _parity_vs_reference(r.records.cpu().numpy(), r.pre_rms.cpu().numpy(),
+                                      r.post_rms.cpu().numpy())
     # e2e through the public API: host image in, host records/RMS out
     e2e_times = []
     for i in range(max(1, args.steps // 2) + 1):
@@ -431,10 +473,12 @@ def run_ours(args):
                 "h2d_bytes_per_step": int(img.nbytes),
                 "d2h_bytes_per_step": n_r * (7 + 8 + 8 + 8)},
         "gpu_launches": int(stats[-1]["kernel_launches"]) * args.steps,
+        "parity": parity,
         "clocks": clk.summary(),
         "device_stats": {k: stats[-1][k] for k in ("ms_fd", "ms_pool", "ms_match", "ms_tensor",
                                                   "ms_exact", "exact_evals", "tensor_candidates",
-                                                  "tensor_tiles", "exact_tiles", "work_items")},
+                                                  "tensor_tiles", "exact_tiles", "work_items",
+                                                  "bulk_ranges", "ms_bulk")},
     }
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(img)

@@ -109,6 +109,8 @@ typedef struct fic_stats {
   int32_t tensor_tiles, exact_tiles, work_items;
   int32_t kernel_launches;   /* kernels this call launched (library-internal CUB passes excluded) */
   double ms_pool_main;       /* device time of the pool builder's main kernel (k_pool) alone */
+  int64_t bulk_ranges;       /* ranges the tensor screen handed to the CUDA-core bulk pass */
+  double ms_bulk;            /* device time of the bulk pass */
 } fic_stats_t;
 
 /* Replaces fic.codec.encode (codec.py:290-427) for one image already in

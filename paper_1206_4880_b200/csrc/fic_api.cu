@@ -1037,7 +1037,7 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
   const bool ptime = getenv("FIC_PLAN_TIMING") != nullptr;
   int pn = 8;
   auto pmark = [&]() {
-    if (ptime && pn < 23) FIC_CUDA(cudaEventRecord(tm.ev[pn++], s));
+    if (ptime && pn < 21) FIC_CUDA(cudaEventRecord(tm.ev[pn++], s));
   };
   tm.mark();  // 0
   SideStream& side = SideStream::get();
@@ -1053,6 +1053,7 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
     double scal[4];
     DevPlan plan;
     unsigned long long flat[2];  // [0] flat count, [1] low word: canonical flat range
+    uint32_t n_bulk[2];          // [0] ranges handed to the bulk pass
   };
   Readback* d_rb = sc.get<Readback>(1);
   FIC_CUDA(cudaMemsetAsync(d_rb, 0, sizeof(Readback), s));
@@ -1235,6 +1236,8 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
   PoolView P = pool_view(pa);
   RangeView Rv{ra.info, ra.rows, pb.lo, pb.hi, g.n_iso, K, ra.KP};
   tm.mark();  // 3
+  BulkArgs bulk{};                 // ranges the screen hands over (k_bulk)
+  const uint32_t* bulk_idx = nullptr;
   if (n_tt_max && titems_n) {
     unsigned long long* thr_g = sc.get<unsigned long long>(g.R);
     k_fill_u64<<<(unsigned)cdiv(g.R, 256), 256, 0, s>>>(thr_g, 0x7ff0000000000000ull, g.R);
@@ -1247,6 +1250,23 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
     if (flat_path) {
       ta.flat_c = fl.flat_c;
       ta.flat_canon = fl.canon;
+    }
+    if (!getenv("FIC_NO_BULK")) {
+      ta.surv_g = sc.get<uint32_t>(g.R);
+      ta.bulk_idx = sc.get<uint32_t>(g.R);
+      FIC_CUDA(cudaMemsetAsync(ta.surv_g, 0, g.R * sizeof(uint32_t), s));
+      FIC_CUDA(cudaMemsetAsync(ta.bulk_idx, 0, g.R * sizeof(uint32_t), s));
+      ta.bulk_cap = (int)std::min<int64_t>(g.R, 4096);
+      ta.bulk_list = sc.get<uint32_t>(ta.bulk_cap);
+      ta.n_bulk = d_rb->n_bulk;
+      ta.bulk_min = getenv("FIC_BULK_MIN") ? std::max(1, atoi(getenv("FIC_BULK_MIN"))) : 2048;
+      ta.bulk_shift = getenv("FIC_BULK_SHIFT") ? std::min(31, std::max(0, atoi(getenv("FIC_BULK_SHIFT")))) : 6;
+      bulk.list = ta.bulk_list;
+      bulk.n_bulk = ta.n_bulk;
+      bulk.cap = ta.bulk_cap;
+      bulk.partials = sc.get<Partial>((size_t)ta.bulk_cap * kBulkPieces);
+      bulk.counters = counters;
+      bulk_idx = ta.bulk_idx;
     }
     const char* dbg_env = getenv("FIC_TC_DEBUG");
     if (dbg_env && (atoi(dbg_env) & (32 | 8192))) {
@@ -1288,13 +1308,17 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
       }
     }
   }
+  FIC_CUDA(cudaEventRecord(tm.ev[21], s));
+  launch_bulk(P, Rv, bulk, s);
+  FIC_CUDA(cudaEventRecord(tm.ev[22], s));
   tm.mark();  // 4
   if (eitems_n) {
     ExactArgs ea{eitems, eitems_n, rid_s, seg_e, sbase, partials, counters, d_plan};
     launch_exact(P, Rv, ea, s);
   }
   tm.mark();  // 5
-  MergeArgs ma{g.R, sbase, nslots, partials, records, pre_rms, post_rms, (double)K};
+  MergeArgs ma{g.R, sbase, nslots, partials, records, pre_rms, post_rms, (double)K, bulk_idx,
+               bulk.partials};
   launch_merge(ma, s);
   tm.mark();  // 6
 
@@ -1346,7 +1370,9 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
       st->ms_pool_main = t;
     }
     st->ms_match = tm.ms(3, 6);
-    st->ms_tensor = tm.ms(3, 4);
+    st->ms_tensor = tm.ms(3, 21);
+    st->ms_bulk = tm.ms(21, 22);
+    st->bulk_ranges = std::min<int64_t>(hrb.n_bulk[0], bulk.cap);
     st->ms_exact = tm.ms(4, 5);
     st->ms_total = n_flat ? tm.ms(0, 23) : tm.ms(0, 7);
     st->exact_evals = (int64_t)hc[0];

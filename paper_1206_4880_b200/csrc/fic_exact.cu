@@ -49,29 +49,19 @@ __device__ __forceinline__ Best shfl_best(const Best& b, int lane_mask) {
   return o;
 }
 
+// Every candidate of range r against pool columns [c0, c1), one thread per
+// column (all isometries), block-wide lexicographic best.  The block has
+// staged the range's n_iso permuted rows in srow.  Returns the block's best
+// in thread 0 and adds the evaluations to counters[0].
 template <int K>
-__global__ void __launch_bounds__(256) k_exact(PoolView P, RangeView Rv, ExactArgs a) {
-  constexpr int KW = K / 4;  // 32-bit words per row
-  __shared__ uint32_t srow[8][KW];
-  __shared__ Best sbest[8];
-  int64_t n_items = a.n_items;
-  const uint32_t* elist = a.elist;
-  if (a.plan) {  // device-side work count (n_items is then a bound)
-    n_items = a.plan->n_eitems;
-    elist = a.elist + a.plan->eb;
-  }
-  for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
-  int2 item = a.items[it];
-  uint32_t r = elist[item.x];
-  int64_t lo = Rv.lo[r], hi = Rv.hi[r];
-  int64_t c0 = lo + (int64_t)item.y * a.seg_len;
-  int64_t c1 = min(hi, c0 + a.seg_len);
-  const int n_iso = Rv.n_iso;
-  const uint32_t* rw = reinterpret_cast<const uint32_t*>(Rv.rows + (int64_t)r * n_iso * K);
-  for (int i = threadIdx.x; i < n_iso * KW; i += blockDim.x) srow[i / KW][i % KW] = rw[i];  // KP == K
-  __syncthreads();
+__device__ __forceinline__ Best scan_columns(const PoolView& P, const RangeView& Rv, uint32_t r,
+                                             int64_t c0, int64_t c1,
+                                             const uint32_t (*srow)[K / 4], Best* sbest,
+                                             unsigned long long* counters) {
+  constexpr int KW = K / 4;
   const RangeInfo inf = Rv.info[r];
   const double n = (double)K;
+  const int n_iso = Rv.n_iso;
   Best b;
   best_init(b);
   unsigned long long evals = 0;
@@ -102,23 +92,86 @@ __global__ void __launch_bounds__(256) k_exact(PoolView P, RangeView Rv, ExactAr
   int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (lane == 0) sbest[warp] = b;
   for (int m = 16; m >= 1; m >>= 1) evals += __shfl_xor_sync(0xffffffffu, evals, m);
-  if (lane == 0 && evals) atomicAdd(a.counters, evals);
+  if (lane == 0 && evals) atomicAdd(counters, evals);
   __syncthreads();
-  if (threadIdx.x == 0) {
-    Best t = sbest[0];
+  Best t = sbest[0];
+  if (threadIdx.x == 0)
     for (int w = 1; w < (int)(blockDim.x >> 5); ++w) best_merge(t, sbest[w]);
-    Partial out;
-    out.err = t.err;
-    out.pre = t.pre;
-    out.dom = t.dom;
-    out.iso = (uint8_t)t.iso;
-    out.sq = (uint8_t)t.sq;
-    out.oq = (uint8_t)t.oq;
-    out.valid = (c1 > c0) ? 1 : 0;
-    a.partials[a.slot_base[r] + item.y] = out;
+  return t;
+}
+
+__device__ __forceinline__ Partial to_partial(const Best& t, bool valid) {
+  Partial out;
+  out.err = t.err;
+  out.pre = t.pre;
+  out.dom = t.dom;
+  out.iso = (uint8_t)t.iso;
+  out.sq = (uint8_t)t.sq;
+  out.oq = (uint8_t)t.oq;
+  out.valid = valid ? 1 : 0;
+  return out;
+}
+
+template <int K>
+__global__ void __launch_bounds__(256) k_exact(PoolView P, RangeView Rv, ExactArgs a) {
+  constexpr int KW = K / 4;  // 32-bit words per row
+  __shared__ uint32_t srow[8][KW];
+  __shared__ Best sbest[8];
+  int64_t n_items = a.n_items;
+  const uint32_t* elist = a.elist;
+  if (a.plan) {  // device-side work count (n_items is then a bound)
+    n_items = a.plan->n_eitems;
+    elist = a.elist + a.plan->eb;
   }
-  __syncthreads();  // shared rows / bests are reused by the next item
+  for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
+    int2 item = a.items[it];
+    uint32_t r = elist[item.x];
+    int64_t lo = Rv.lo[r], hi = Rv.hi[r];
+    int64_t c0 = lo + (int64_t)item.y * a.seg_len;
+    int64_t c1 = min(hi, c0 + a.seg_len);
+    const uint32_t* rw = reinterpret_cast<const uint32_t*>(Rv.rows + (int64_t)r * Rv.n_iso * K);
+    for (int i = threadIdx.x; i < Rv.n_iso * KW; i += blockDim.x) srow[i / KW][i % KW] = rw[i];  // KP == K
+    __syncthreads();
+    const Best t = scan_columns<K>(P, Rv, r, c0, c1, srow, sbest, a.counters);
+    if (threadIdx.x == 0) a.partials[a.slot_base[r] + item.y] = to_partial(t, c1 > c0);
+    __syncthreads();  // shared rows / bests are reused by the next item
   }
+}
+
+// Bulk pass for the ranges the tensor matcher handed over (TcArgs::bulk_*):
+// every candidate of each listed range, its slab cut into kBulkPieces equal
+// column pieces, one block per (range, piece); partial f * kBulkPieces + piece.
+template <int K>
+__global__ void __launch_bounds__(256) k_bulk(PoolView P, RangeView Rv, BulkArgs a) {
+  constexpr int KW = K / 4;
+  __shared__ uint32_t srow[8][KW];
+  __shared__ Best sbest[8];
+  const int64_t n_items = (int64_t)min(*a.n_bulk, (uint32_t)a.cap) * kBulkPieces;
+  for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
+    const int f = (int)(it / kBulkPieces), piece = (int)(it - (int64_t)f * kBulkPieces);
+    const uint32_t r = a.list[f];
+    const int64_t lo = Rv.lo[r], hi = Rv.hi[r];
+    const int64_t len = cdiv(hi - lo, (int64_t)kBulkPieces);
+    const int64_t c0 = min(hi, lo + piece * len), c1 = min(hi, c0 + len);
+    const uint32_t* rw = reinterpret_cast<const uint32_t*>(Rv.rows + (int64_t)r * Rv.n_iso * K);
+    for (int i = threadIdx.x; i < Rv.n_iso * KW; i += blockDim.x) srow[i / KW][i % KW] = rw[i];
+    __syncthreads();
+    const Best t = scan_columns<K>(P, Rv, r, c0, c1, srow, sbest, a.counters);
+    if (threadIdx.x == 0) a.partials[it] = to_partial(t, c1 > c0);
+    __syncthreads();
+  }
+}
+
+void launch_bulk(const PoolView& P, const RangeView& Rv, const BulkArgs& a, cudaStream_t s) {
+  if (a.cap == 0) return;
+  const unsigned grid = 148 * 8;  // grid-stride over the device-side item count
+  if (Rv.K == 64)
+    k_bulk<64><<<grid, 256, 0, s>>>(P, Rv, a);
+  else if (Rv.K == 16)
+    k_bulk<16><<<grid, 256, 0, s>>>(P, Rv, a);
+  else
+    invalid("bulk pass supports range_size 4 and 8");
+  FIC_CHECK_LAUNCH();
 }
 
 // Generic K (any range size): rows zero-padded to KP = K rounded up to a
@@ -212,11 +265,14 @@ __global__ void k_merge(MergeArgs a) {
   int ns = a.nslots[r];
   if (ns == 0) return;
   const Partial* p = a.partials + a.slot_base[r];
+  // a range the bulk pass took over also has its kBulkPieces partials there
+  const uint32_t bi = a.bulk_idx ? a.bulk_idx[r] : 0u;
+  const Partial* pb = bi ? a.bulk_part + (int64_t)(bi - 1) * kBulkPieces : nullptr;
   double err = INFINITY, pre = INFINITY;
   uint32_t dom = 0xffffffffu;
   int iso = 0, sq = 0, oq = 0;
-  for (int i = 0; i < ns; ++i) {
-    Partial q = p[i];
+  for (int i = 0; i < ns + (pb ? kBulkPieces : 0); ++i) {
+    Partial q = i < ns ? p[i] : pb[i - ns];
     if (!q.valid) continue;
     pre = fmin(pre, q.pre);
     if (better(q.err, q.dom, q.iso, err, dom, iso)) {

@@ -185,16 +185,33 @@ def test_write_csv_and_pgm(tmp_path):
 
 
 def test_bench_pool_roofline_arithmetic():
-    """bench.py's HBM roofline of k_pool: algorithmic bytes per domain
-    (4 B read + 3K + 20 B written) over the mean device time of the steps."""
+    """bench.py's HBM roofline of K1 on SURVEY §8(d)'s bytes (H*W + D*(2K+16),
+    147.6 MB at cfg3) over the mean device time of k_pool and of the K1 stage."""
     import bench
     stats = [{"ms_pool_main": 0.05, "ms_pool": 0.06}, {"ms_pool_main": 0.05, "ms_pool": 0.06}]
-    r = bench._pool_roofline(stats, 6552.3, "measured", serial_stats=[{"ms_pool_main": 0.04}])
+    r = bench._pool_roofline(stats, 6552.3, "measured",
+                             serial_stats=[{"ms_pool_main": 0.04, "ms_pool": 0.045}])
     d = 1009 * 1009
-    assert r["algorithmic_bytes_per_launch"] == d * (4 + 3 * 64 + 20)
+    assert r["algorithmic_bytes_per_launch"] == 1024 * 1024 + d * (2 * 64 + 16)
+    assert abs(r["algorithmic_bytes_per_launch"] - 147.6e6) < 0.1e6
     assert abs(r["achieved"] - r["algorithmic_bytes_per_launch"] / 0.05e-3 / 1e9) < 1e-6
     assert abs(r["frac"] - r["achieved"] / 6552.3) < 1e-12
+    assert abs(r["k1_stage"]["achieved"] - r["algorithmic_bytes_per_launch"] / 0.06e-3 / 1e9) < 1e-6
     assert r["bound"] == "hbm" and r["isolated"]["ms_per_launch"] == 0.04
+    assert r["isolated"]["k1_stage_ms"] == 0.045
+
+
+def test_bench_parity_counts_mismatches_and_near_ties():
+    import bench
+    with np.load(os.path.join(ROOT, "tests", "golden", "scale_cfg3.npz")) as z:
+        rec, pre, post = z["cfg3.records"].copy(), z["cfg3.pre_rms"], z["cfg3.post_rms"].copy()
+    p = bench._parity_vs_reference(rec, pre, post)
+    assert p["record_mismatches"] == 0 and p["rms_bit_exact"] and p["ranges"] == 16384
+    rec[5, 4] ^= 1                        # another isometry, same error: a near-tie
+    rec[9, 0] ^= 1
+    post[9] *= 1.01                       # a real mismatch
+    p = bench._parity_vs_reference(rec, pre, post)
+    assert p["record_mismatches"] == 2 and p["near_ties"] == 1 and not p["rms_bit_exact"]
 
 
 def test_bench_clock_summary_from_nvidia_smi_lines():

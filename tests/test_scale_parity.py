@@ -3,7 +3,7 @@
 The fixtures (tests/golden/make_scale_golden.py) hold what the reference
 package itself computed -- its setup and its ``_search_chunk`` -- for EVERY
 range of cfg2 (dynamic and exhaustive), cfg3 and cfg4 (exhaustive, 4x4),
-and for 64 ranges of cfg5 plus cfg5's full pool sizes and checksums of its
+and for 1,024 ranges of cfg5 (16 of them empty-window fallbacks) plus cfg5's full pool sizes and checksums of its
 slabs, range FDs and FD order.  Records and both RMS columns must be
 bit-identical; near-ties (SURVEY §8c protocol: the reference's and our
 candidate within 1e-6 relative) are counted and must be zero.
@@ -157,3 +157,18 @@ def test_pool_builder_outputs_match_reference(cname, strategy, planes, monkeypat
     assert _sha(sum_d) == str(g[f"{cname}.sum_d_sha"])
     assert _sha(sum_dd) == str(g[f"{cname}.sum_dd_sha"])
     assert _sha(inv_den) == str(g[f"{cname}.inv_den_sha"])
+
+
+@pytest.mark.parametrize("env", [{"FIC_BULK_MIN": "1", "FIC_BULK_SHIFT": "31"},
+                                 {"FIC_NO_BULK": "1"}])
+@pytest.mark.parametrize("prefix", ["cfg2", "cfg2_ex"])
+def test_bulk_handover_extremes_match_reference(prefix, env, monkeypatch):
+    """Hand every range with one survivor to the bulk pass, or none: the
+    records must not change (both paths evaluate exactly)."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    _, res = _check_full("scale_cfg2.npz", prefix)
+    if "FIC_NO_BULK" in env:
+        assert res.stats["bulk_ranges"] == 0
+    else:
+        assert res.stats["bulk_ranges"] > 0
