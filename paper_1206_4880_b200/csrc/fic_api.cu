@@ -1238,6 +1238,7 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
   tm.mark();  // 3
   BulkArgs bulk{};                 // ranges the screen hands over (k_bulk)
   const uint32_t* bulk_idx = nullptr;
+  const uint32_t* surv_g = nullptr;
   if (n_tt_max && titems_n) {
     unsigned long long* thr_g = sc.get<unsigned long long>(g.R);
     k_fill_u64<<<(unsigned)cdiv(g.R, 256), 256, 0, s>>>(thr_g, 0x7ff0000000000000ull, g.R);
@@ -1267,6 +1268,7 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
       bulk.partials = sc.get<Partial>((size_t)ta.bulk_cap * kBulkPieces);
       bulk.counters = counters;
       bulk_idx = ta.bulk_idx;
+      surv_g = ta.surv_g;
     }
     const char* dbg_env = getenv("FIC_TC_DEBUG");
     if (dbg_env && (atoi(dbg_env) & (32 | 8192))) {
@@ -1309,6 +1311,16 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
     }
   }
   FIC_CUDA(cudaEventRecord(tm.ev[21], s));
+  if (getenv("FIC_SURV_DUMP") && surv_g) {  // per-range survivors / hand-overs (analysis only)
+    std::vector<uint32_t> h(2 * (size_t)g.R);
+    FIC_CUDA(cudaMemcpyAsync(h.data(), surv_g, g.R * 4, cudaMemcpyDeviceToHost, s));
+    FIC_CUDA(cudaMemcpyAsync(h.data() + g.R, bulk_idx, g.R * 4, cudaMemcpyDeviceToHost, s));
+    FIC_CUDA(cudaStreamSynchronize(s));
+    if (FILE* f = fopen(getenv("FIC_SURV_DUMP"), "wb")) {
+      fwrite(h.data(), 4, h.size(), f);
+      fclose(f);
+    }
+  }
   launch_bulk(P, Rv, bulk, s);
   FIC_CUDA(cudaEventRecord(tm.ev[22], s));
   tm.mark();  // 4

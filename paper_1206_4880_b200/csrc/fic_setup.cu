@@ -324,6 +324,183 @@ __global__ void __launch_bounds__(256) k_fd16_tile(FdArgs a) {
   }
 }
 
+// K2 for 16x16 domain blocks at an EVEN stride (st = 2 hs): every domain
+// origin and every DBC cell corner is an even pixel position, so the cell
+// maps are needed on the even sub-lattice only -- a half-resolution grid
+// (y', x') = (y / 2, x / 2).  Scale-2 cells are the disjoint 2x2 blocks of
+// that grid, a scale-4 cell is 2x2 neighbouring scale-2 cells, a scale-8
+// cell is 2x2 scale-4 cells two half-grid steps apart (fdim.py:63-72); the
+// per-block counts are the same strided sums as k_fd16_tile, on a 4x smaller
+// map.  Same integer counts, hence the same FD bits.
+template <int T, bool POW2>
+__global__ void __launch_bounds__(256) k_fd16_half(FdArgs a) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  __shared__ uint16_t quot[3][256];
+  for (int i = threadIdx.x; i < 3 * 256; i += blockDim.x) quot[i >> 8][i & 255] = a.quot[i];
+  const int hs = a.bst >> 1;          // half-grid step between domain origins
+  const int HP = (T - 1) * hs + 8;    // half-grid patch side
+  const int PW = 2 * HP;              // image patch side (pixels)
+  const int PWP = (PW + 3) & ~3;      // patch row pitch (whole words)
+  const int HH = HP * HP;
+  uint8_t* P = sm;                    // [PW][PWP]
+  uint8_t* X2 = P + PW * PWP;         // half-grid maps [HP][HP]
+  uint8_t* N2 = X2 + HH;
+  uint8_t* C2 = N2 + HH;
+  uint8_t* X4 = C2 + HH;
+  uint8_t* N4 = X4 + HH;
+  uint8_t* C4 = N4 + HH;
+  uint8_t* C8 = C4 + HH;
+  uint16_t* H2 = reinterpret_cast<uint16_t*>(sm + ((PW * PWP + 7 * HH + 15) & ~15));
+  uint16_t* H4 = H2 + HP * T;
+  uint16_t* H8 = H4 + HP * T;
+  uint32_t* hist = reinterpret_cast<uint32_t*>(H8 + HP * T + (HP * T & 1));
+  uint32_t* minid = hist + a.n_rank;
+  if (a.rank_hist)
+    for (int r = threadIdx.x; r < a.n_rank; r += blockDim.x) {
+      hist[r] = 0;
+      minid[r] = 0xffffffffu;
+    }
+  const int64_t nby = a.n / a.nbx;
+  const int kx0 = blockIdx.x * T, ky0 = blockIdx.y * T;
+  const int x0 = kx0 * a.bst, y0 = ky0 * a.bst;
+  const int Himg = (int)((nby - 1) * a.bst + 16), Wimg = a.W;
+  const int wp = threadIdx.x >> 5, ln = threadIdx.x & 31;
+  auto for_xy = [&](int ny, int nx, auto&& f) {
+    for (int y = wp; y < ny; y += 8)
+      for (int x = ln; x < nx; x += 32) f(y, x);
+  };
+  const int sh0 = a.qshift[0], sh1 = a.qshift[1], sh2 = a.qshift[2];
+  auto qd = [&](int j, int mx, int mn) -> int {
+    if (POW2) {
+      const int sh = j == 0 ? sh0 : (j == 1 ? sh1 : sh2);
+      return (mx >> sh) - (mn >> sh);
+    }
+    return quot[j][mx] - quot[j][mn];
+  };
+  // image patch as 4-byte words (x0 = 64 hs bx: a multiple of 4; W % 4 == 0,
+  // so a word starting inside the image lies inside it)
+  {
+    const int pw4 = PWP >> 2, nw = PW * pw4;
+    for (int i = threadIdx.x; i < nw; i += blockDim.x) {
+      const int y = i / pw4, xw = i - y * pw4;
+      const int gy = y0 + y, gx = x0 + 4 * xw;
+      const uint32_t v = (gy < Himg && gx < Wimg)
+                             ? __ldg(reinterpret_cast<const uint32_t*>(a.src + (int64_t)gy * Wimg + gx))
+                             : 0u;
+      *reinterpret_cast<uint32_t*>(P + y * PWP + 4 * xw) = v;
+    }
+  }
+  __syncthreads();
+  // scale 2: the disjoint 2x2 pixel blocks
+  for_xy(HP, HP, [&](int y, int x) {
+    const uint8_t* q = P + 2 * y * PWP + 2 * x;
+    const int p0 = q[0], p1 = q[1], p2 = q[PWP], p3 = q[PWP + 1];
+    const int mx = max(max(p0, p1), max(p2, p3)), mn = min(min(p0, p1), min(p2, p3));
+    const int i = y * HP + x;
+    X2[i] = (uint8_t)mx;
+    N2[i] = (uint8_t)mn;
+    C2[i] = (uint8_t)qd(0, mx, mn);
+  });
+  __syncthreads();
+  // scale 4: 2x2 neighbouring scale-2 cells
+  for_xy(HP - 1, HP - 1, [&](int y, int x) {
+    const int i = y * HP + x;
+    const int mx = max(max(X2[i], X2[i + 1]), max(X2[i + HP], X2[i + HP + 1]));
+    const int mn = min(min(N2[i], N2[i + 1]), min(N2[i + HP], N2[i + HP + 1]));
+    X4[i] = (uint8_t)mx;
+    N4[i] = (uint8_t)mn;
+    C4[i] = (uint8_t)qd(1, mx, mn);
+  });
+  __syncthreads();
+  // scale 8: 2x2 scale-4 cells two half-grid steps apart
+  for_xy(HP - 3, HP - 3, [&](int y, int x) {
+    const int i = y * HP + x;
+    const int mx = max(max(X4[i], X4[i + 2]), max(X4[i + 2 * HP], X4[i + 2 * HP + 2]));
+    const int mn = min(min(N4[i], N4[i + 2]), min(N4[i + 2 * HP], N4[i + 2 * HP + 2]));
+    C8[i] = (uint8_t)qd(2, mx, mn);
+  });
+  __syncthreads();
+  // row sums per domain column: 8 scale-2, 4 scale-4, 2 scale-8 cells
+  for (int i = threadIdx.x; i < HP * T; i += blockDim.x) {
+    const int y = i / T, lx = i - y * T;
+    const int xo = lx * hs;
+    const uint8_t* r2 = C2 + y * HP + xo;
+    int h2 = 0, h4 = 0, h8 = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) h2 += r2[j];
+    if (y < HP - 1) {
+      const uint8_t* r4 = C4 + y * HP + xo;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) h4 += r4[2 * j];
+    }
+    if (y < HP - 3) {
+      const uint8_t* r8 = C8 + y * HP + xo;
+      h8 = r8[0] + r8[4];
+    }
+    H2[i] = (uint16_t)h2;
+    H4[i] = (uint16_t)h4;
+    H8[i] = (uint16_t)h8;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < T * T; i += blockDim.x) {
+    const int ly = i / T, lx = i - ly * T;
+    const int ky = ky0 + ly, kx = kx0 + lx;
+    if (ky >= nby || kx >= a.nbx) continue;
+    const int Y = ly * hs;
+    int cnt[3] = {0, 0, 0};
+#pragma unroll
+    for (int r = 0; r < 8; ++r) cnt[0] += H2[(Y + r) * T + lx];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) cnt[1] += H4[(Y + 2 * r) * T + lx];
+    cnt[2] = H8[Y * T + lx] + H8[(Y + 4) * T + lx];
+    double f = 0.0;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      const int k = 16 >> (j + 1);
+      const int c = min(cnt[j] + k * k, a.ln_len - 1);
+      const double t = __dmul_rn(__ldg(a.ln + c), __ldg(a.w + j));
+      f = (j == 0) ? t : __dadd_rn(f, t);
+    }
+    if (a.clamp) f = fmin(fmax(f, 2.0), 3.0);
+    const int64_t b = (int64_t)ky * a.nbx + kx;
+    if (a.fd) a.fd[b] = f;
+    if (a.key) a.key[b] = (unsigned long long)__double_as_longlong(f);
+    if (a.combo || a.rank) {
+      uint32_t c = 0;
+#pragma unroll
+      for (int j = 0; j < 3; ++j) c += (uint32_t)cnt[j] * (uint32_t)a.cstride[j];
+      if (a.rank_of_combo) {
+        const uint32_t r = __ldg(a.rank_of_combo + c);
+        a.rank[b] = r;
+        if (a.rank_hist) {
+          const unsigned grp = __match_any_sync(__activemask(), r);
+          if ((int)(threadIdx.x & 31) == __ffs(grp) - 1) {
+            atomicAdd(hist + r, (uint32_t)__popc(grp));
+            atomicMin(minid + r, (uint32_t)b);
+          }
+        }
+      } else {
+        a.combo[b] = c;
+      }
+    }
+    if (a.iota) a.iota[b] = (uint32_t)b;
+  }
+  if (a.rank_hist) {
+    __syncthreads();
+    for (int r = threadIdx.x; r < a.n_rank; r += blockDim.x)
+      if (hist[r]) {
+        atomicAdd(a.rank_hist + r, hist[r]);
+        atomicMin(a.rank_minid + r, minid[r]);
+      }
+  }
+}
+
+static size_t fd16_half_smem(int T, int st, int n_rank) {
+  const int HP = (T - 1) * (st >> 1) + 8, PW = 2 * HP, HH = HP * HP, PWP = (PW + 3) & ~3;
+  return (size_t)((PW * PWP + 7 * HH + 15) & ~15) +
+         (size_t)(3 * HP * T + (HP * T & 1)) * sizeof(uint16_t) + (size_t)2 * n_rank * sizeof(uint32_t);
+}
+
 static size_t fd16_tile_smem(int T, int st, int n_rank) {
   const int PW = (T - 1) * st + 16, PP = PW * PW;
   return (size_t)((8 * PP + 15) & ~15) + (size_t)(3 * PW * T + (PW * T & 1)) * sizeof(uint16_t) +
@@ -393,6 +570,17 @@ void launch_fd(const FdArgs& a, cudaStream_t s) {
         k_fd16_tile<T, true><<<grid, 256, fd16_tile_smem(T, 1, nr), s>>>(a);
       else
         k_fd16_tile<T, false><<<grid, 256, fd16_tile_smem(T, 1, nr), s>>>(a);
+    } else if ((a.bst & 1) == 0 && !getenv("FIC_FD_FULLGRID")) {
+      // even stride: the half-resolution lattice (k_fd16_half)
+      constexpr int T = 32;
+      const size_t smem = fd16_half_smem(T, a.bst, nr);
+      smem_optin_k(k_fd16_half<T, true>, (int)fd16_half_smem(T, 4, kCountSortMaxRanks));
+      smem_optin_k(k_fd16_half<T, false>, (int)fd16_half_smem(T, 4, kCountSortMaxRanks));
+      dim3 grid((unsigned)cdiv(a.nbx, T), (unsigned)cdiv(nby, T));
+      if (pow2)
+        k_fd16_half<T, true><<<grid, 256, smem, s>>>(a);
+      else
+        k_fd16_half<T, false><<<grid, 256, smem, s>>>(a);
     } else {
       constexpr int T = 16;
       dim3 grid((unsigned)cdiv(a.nbx, T), (unsigned)cdiv(nby, T));

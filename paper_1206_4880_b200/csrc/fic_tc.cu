@@ -684,13 +684,9 @@ __global__ void __maxnreg__(MAXREG)
             hit_lanes += hit ? 1 : 0;
           }
           const long long ts0 = TCLK();
-          // a range handed over to the bulk pass: nothing more to screen
-          if (hit && a.bulk_idx &&
-              (reinterpret_cast<volatile uint32_t*>(flag_s)[rk] ||
-               *reinterpret_cast<volatile uint32_t*>(a.bulk_idx + rid))) {
-            flag_s[rk] = 1;
-            hit = false;
-          }
+          // a range handed over to the bulk pass (by this CTA, or by another
+          // one before this item started): nothing more to screen
+          if (hit && a.bulk_idx && reinterpret_cast<volatile uint32_t*>(flag_s)[rk]) hit = false;
           const int32_t wl = max(e_lo, 0), wh = min(e_hi, CH);
           uint64_t wmask = 0;
           if (hit) wmask = ((wh >= 64) ? ~0ull : ((1ull << wh) - 1ull)) & ~((1ull << wl) - 1ull);

@@ -120,6 +120,20 @@ def test_plan_tiled_fd_equals_direct_at_cfg3(monkeypatch):
         assert np.array_equal(a[k], b[k]), k
 
 
+@pytest.mark.parametrize("cname", ["cfg2", "cfg5"])
+def test_plan_half_lattice_fd_equals_full_grid(cname, monkeypatch):
+    """Full-size property at the even-stride configs: the half-lattice DBC
+    kernel (k_fd16_half) and the full-grid tiled kernel agree bit for bit on
+    every domain (16.7 M at cfg5), and so do the order and slabs."""
+    c = synth.CONFIGS[cname]
+    img = c.make()
+    a = codec.plan(img, "dynamic_fd", stride=c.stride, delta=c.delta)
+    monkeypatch.setenv("FIC_FD_FULLGRID", "1")
+    b = codec.plan(img, "dynamic_fd", stride=c.stride, delta=c.delta)
+    for k in ("fd_dom", "fd_rng", "order", "slab_lo", "slab_hi"):
+        assert np.array_equal(a[k], b[k]), k
+
+
 @pytest.mark.parametrize("delta", [1e-4, 0.02])
 def test_encode_count_sorted_pools_match_oracle(delta):
     """encode() orders equal-FD domains by a counting sort (unspecified order
