@@ -66,6 +66,7 @@ class FicStats(ctypes.Structure):
         ("ms_pool_main", ctypes.c_double),
         ("bulk_ranges", ctypes.c_int64),
         ("ms_bulk", ctypes.c_double),
+        ("sl_entries", ctypes.c_int64),
     ]
 
     def as_dict(self) -> dict:

@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <cstring>
 #include <string>
 
 #include "../../include/fic_b200.h"
@@ -71,6 +72,20 @@ struct Partial {
   uint32_t dom;     // raster domain index (0xffffffff = none)
   uint8_t iso, sq, oq, valid;
 };
+
+// order-preserving bits of a double (unsigned order == numeric order,
+// negatives included) and back, for atomicMin / CAS on fp64 values
+__host__ __device__ __forceinline__ unsigned long long ord_bits(double x) {
+  unsigned long long b;
+  memcpy(&b, &x, 8);
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__host__ __device__ __forceinline__ double unord_bits(unsigned long long k) {
+  const unsigned long long b = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+  double x;
+  memcpy(&x, &b, 8);
+  return x;
+}
 
 // lexicographic (err, dom, iso): codec.py:243-258
 __host__ __device__ __forceinline__ bool better(double e1, uint32_t d1, int i1,

@@ -709,6 +709,14 @@ static RankTable make_rank_table(const DbcTables& td, const FdCombo& fc, int cla
   return rt;
 }
 
+__global__ void k_sl_init(unsigned long long* best, unsigned long long* pre, int64_t n) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  best[2 * i] = ~0ull;
+  best[2 * i + 1] = ord_bits(INFINITY);
+  pre[i] = ord_bits(INFINITY);
+}
+
 __global__ void k_fill_u64(unsigned long long* a, unsigned long long v, int64_t n) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) a[i] = v;
@@ -1053,7 +1061,7 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
     double scal[4];
     DevPlan plan;
     unsigned long long flat[2];  // [0] flat count, [1] low word: canonical flat range
-    uint32_t n_bulk[2];          // [0] ranges handed to the bulk pass
+    uint32_t n_bulk[2];          // [0] ranges handed to the bulk pass, [1] survivor-list entries
   };
   Readback* d_rb = sc.get<Readback>(1);
   FIC_CUDA(cudaMemsetAsync(d_rb, 0, sizeof(Readback), s));
@@ -1236,6 +1244,7 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
   PoolView P = pool_view(pa);
   RangeView Rv{ra.info, ra.rows, pb.lo, pb.hi, g.n_iso, K, ra.KP};
   tm.mark();  // 3
+  SlArgs sla{};                    // survivor list (k_sl_rescore)
   BulkArgs bulk{};                 // ranges the screen hands over (k_bulk)
   const uint32_t* bulk_idx = nullptr;
   const uint32_t* surv_g = nullptr;
@@ -1252,7 +1261,22 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
       ta.flat_c = fl.flat_c;
       ta.flat_canon = fl.canon;
     }
-    if (!getenv("FIC_NO_BULK")) {
+    if (!getenv("FIC_NO_SL")) {
+      // survivor list (TcArgs::sl): capacity min(16 M, max(1 M, 128 R)) entries
+      ta.sl_cap = (uint32_t)std::min<int64_t>(16 << 20, std::max<int64_t>(1 << 20, 128 * (int64_t)g.R));
+      if (getenv("FIC_SL_CAP")) ta.sl_cap = (uint32_t)std::max(1, atoi(getenv("FIC_SL_CAP")));
+      ta.sl = sc.get<uint4>(ta.sl_cap);
+      ta.sl_count = d_rb->n_bulk + 1;
+      sla.sl = ta.sl;
+      sla.sl_count = ta.sl_count;
+      sla.sl_cap = ta.sl_cap;
+      sla.best = sc.get<unsigned long long>(2 * (size_t)g.R);
+      sla.pre = sc.get<unsigned long long>(g.R);
+      sla.counters = counters;
+      k_sl_init<<<(unsigned)cdiv(g.R, 256), 256, 0, s>>>(sla.best, sla.pre, g.R);
+      FIC_CHECK_LAUNCH();
+    }
+    if (getenv("FIC_BULK")) {
       ta.surv_g = sc.get<uint32_t>(g.R);
       ta.bulk_idx = sc.get<uint32_t>(g.R);
       FIC_CUDA(cudaMemsetAsync(ta.surv_g, 0, g.R * sizeof(uint32_t), s));
@@ -1321,6 +1345,7 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
       fclose(f);
     }
   }
+  launch_sl_rescore(P, Rv, sla, s);
   launch_bulk(P, Rv, bulk, s);
   FIC_CUDA(cudaEventRecord(tm.ev[22], s));
   tm.mark();  // 4
@@ -1330,7 +1355,7 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
   }
   tm.mark();  // 5
   MergeArgs ma{g.R, sbase, nslots, partials, records, pre_rms, post_rms, (double)K, bulk_idx,
-               bulk.partials};
+               bulk.partials, sla.best, sla.pre};
   launch_merge(ma, s);
   tm.mark();  // 6
 
@@ -1385,6 +1410,7 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
     st->ms_tensor = tm.ms(3, 21);
     st->ms_bulk = tm.ms(21, 22);
     st->bulk_ranges = std::min<int64_t>(hrb.n_bulk[0], bulk.cap);
+    st->sl_entries = std::min<int64_t>(hrb.n_bulk[1], sla.sl_cap);
     st->ms_exact = tm.ms(4, 5);
     st->ms_total = n_flat ? tm.ms(0, 23) : tm.ms(0, 7);
     st->exact_evals = (int64_t)hc[0];

@@ -162,6 +162,113 @@ __global__ void __launch_bounds__(256) k_bulk(PoolView P, RangeView Rv, BulkArgs
   }
 }
 
+__device__ __forceinline__ void cas128(unsigned long long* addr, unsigned long long cmp_lo,
+                                       unsigned long long cmp_hi, unsigned long long new_lo,
+                                       unsigned long long new_hi, unsigned long long& old_lo,
+                                       unsigned long long& old_hi) {
+  asm volatile(
+      "{\n .reg .b128 d, b, c;\n mov.b128 b, {%2, %3};\n mov.b128 c, {%4, %5};\n"
+      " atom.global.cas.b128 d, [%6], b, c;\n mov.b128 {%0, %1}, d;\n}\n"
+      : "=l"(old_lo), "=l"(old_hi)
+      : "l"(cmp_lo), "l"(cmp_hi), "l"(new_lo), "l"(new_hi), "l"(addr)
+      : "memory");
+}
+
+// Survivor-list rescoring (SlArgs).  A warp takes 32 entries, stages them
+// and the prefix sums of their popcounts in shared memory, and deals their
+// candidates (set mask bits) round-robin to its lanes, so every lane
+// evaluates whatever the masks' sizes.  Each candidate goes through
+// eval_candidate (the reference's fp64 sequence); improvements of the
+// range's best are published with a 128-bit CAS on (ord(err), dom | iso |
+// s_q | o_q), whose unsigned order is the lexicographic (err, dom, iso)
+// order, and the pre-quantisation error with a 64-bit atomicMin on ord(pre).
+template <int K>
+__global__ void __launch_bounds__(256) k_sl_rescore(PoolView P, RangeView Rv, SlArgs a) {
+  constexpr int KW = K / 4;
+  __shared__ uint4 s_ent[8][32];
+  __shared__ uint32_t s_incl[8][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t n = (int64_t)min(*a.sl_count, a.sl_cap);
+  const int64_t warp0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int n_iso = Rv.n_iso;
+  const double nK = (double)K;
+  unsigned long long evals = 0;
+  for (int64_t base = warp0 * 32; base < n; base += nwarps * 32) {
+    uint4 e = make_uint4(0, 0, 0, 0);
+    if (base + lane < n) e = a.sl[base + lane];
+    const unsigned long long mask = ((unsigned long long)e.w << 32) | e.z;
+    uint32_t incl = (uint32_t)__popcll(mask);
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t v = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= d) incl += v;
+    }
+    s_ent[w][lane] = e;
+    s_incl[w][lane] = incl;
+    __syncwarp();
+    const uint32_t total = s_incl[w][31];
+    for (uint32_t t = lane; t < total; t += 32) {
+      int j = 0;  // first entry whose inclusive count exceeds t
+#pragma unroll
+      for (int step = 16; step >= 1; step >>= 1)
+        if (s_incl[w][j + step - 1] <= t) j += step;
+      const uint4 ej = s_ent[w][j];
+      const uint32_t k = t - (j ? s_incl[w][j - 1] : 0u);
+      const uint32_t plo = (uint32_t)__popc(ej.z);
+      const int bit = k < plo ? (int)__fns(ej.z, 0, (int)k + 1) : 32 + (int)__fns(ej.w, 0, (int)(k - plo) + 1);
+      const int64_t p = (int64_t)ej.y + bit;
+      const uint32_t rid = ej.x >> 3, iso = ej.x & 7u;
+      const uint32_t dom = pool_id(P, p);
+      uint32_t dw[KW];
+      dom_words<K>(P, p, dom, dw);
+      const uint4* rrow = reinterpret_cast<const uint4*>(Rv.rows + ((int64_t)rid * n_iso + iso) * K);
+      uint32_t acc = 0;
+#pragma unroll
+      for (int q = 0; q < KW / 4; ++q) {
+        const uint4 rv = __ldg(rrow + q);
+        acc = __dp4a(dw[4 * q], rv.x, acc);
+        acc = __dp4a(dw[4 * q + 1], rv.y, acc);
+        acc = __dp4a(dw[4 * q + 2], rv.z, acc);
+        acc = __dp4a(dw[4 * q + 3], rv.w, acc);
+      }
+      const uint2 sm = __ldg(P.sums + p);
+      const RangeInfo inf = Rv.info[rid];
+      const Cand c = eval_candidate((double)acc, (double)sm.x, (double)sm.y, __ldg(P.inv_den + p),
+                                    inf.sr, inf.srr, nK);
+      ++evals;
+      atomicMin(a.pre + rid, ord_bits(c.pre));
+      const unsigned long long khi = ord_bits(c.err);
+      const unsigned long long klo = ((unsigned long long)dom << 32) | (iso << 24) |
+                                     ((uint32_t)c.sq << 16) | ((uint32_t)c.oq << 8);
+      unsigned long long* slot = a.best + 2 * (int64_t)rid;
+      unsigned long long clo = __ldcg(slot), chi = __ldcg(slot + 1);
+      while (khi < chi || (khi == chi && klo < clo)) {
+        unsigned long long olo, ohi;
+        cas128(slot, clo, chi, klo, khi, olo, ohi);
+        if (olo == clo && ohi == chi) break;
+        clo = olo;
+        chi = ohi;
+      }
+    }
+    __syncwarp();
+  }
+  for (int m = 16; m >= 1; m >>= 1) evals += __shfl_xor_sync(0xffffffffu, evals, m);
+  if (lane == 0 && evals) atomicAdd(a.counters, evals);
+}
+
+void launch_sl_rescore(const PoolView& P, const RangeView& Rv, const SlArgs& a, cudaStream_t s) {
+  if (!a.sl) return;
+  const unsigned grid = 148 * 8;  // grid-stride over the device-side entry count
+  if (Rv.K == 64)
+    k_sl_rescore<64><<<grid, 256, 0, s>>>(P, Rv, a);
+  else if (Rv.K == 16)
+    k_sl_rescore<16><<<grid, 256, 0, s>>>(P, Rv, a);
+  else
+    invalid("survivor list supports range_size 4 and 8");
+  FIC_CHECK_LAUNCH();
+}
+
 void launch_bulk(const PoolView& P, const RangeView& Rv, const BulkArgs& a, cudaStream_t s) {
   if (a.cap == 0) return;
   const unsigned grid = 148 * 8;  // grid-stride over the device-side item count
@@ -271,6 +378,17 @@ __global__ void k_merge(MergeArgs a) {
   double err = INFINITY, pre = INFINITY;
   uint32_t dom = 0xffffffffu;
   int iso = 0, sq = 0, oq = 0;
+  if (a.sl_best) {  // the survivor list's best for this range (k_sl_rescore)
+    const unsigned long long hi = a.sl_best[2 * (int64_t)r + 1], lo = a.sl_best[2 * (int64_t)r];
+    if (hi != ord_bits(INFINITY)) {
+      err = unord_bits(hi);
+      dom = (uint32_t)(lo >> 32);
+      iso = (int)((lo >> 24) & 255u);
+      sq = (int)((lo >> 16) & 255u);
+      oq = (int)((lo >> 8) & 255u);
+    }
+    pre = unord_bits(a.sl_pre[r]);
+  }
   for (int i = 0; i < ns + (pb ? kBulkPieces : 0); ++i) {
     Partial q = i < ns ? p[i] : pb[i - ns];
     if (!q.valid) continue;

@@ -1061,37 +1061,47 @@ __global__ void __launch_bounds__(256) k_domrows(const uint8_t* img, int H, int 
   }
 }
 
-template <int RS>
-__global__ void __launch_bounds__(256, 8) k_pool(PoolArgs a) {
+// One warp builds 32 consecutive pool positions p0 .. p0 + 31.  Lane j
+// locates domain p0 + j (raster id from the FD order, byte offset of its
+// first decimated row in the row segments / box planes).  Per instruction
+// the warp then covers DPI = 32 / RS domains, RS lanes per domain, one
+// decimated row per lane: row sums by dp4a, reduced across the RS lanes,
+// and the fp16 B row written as whole contiguous rows.  Lane j keeps its
+// domain's sums and writes the per-domain scalars coalesced (1/den as
+// codec.py:141-145: __drcp_rn(den) is the correctly rounded 1.0 / den).
+//   B_k = fp16(fp32(K d_k - sum_d) * rsqrt(K den))
+// fp32 rounding before the fp16 rounding is far inside the screen's error
+// budget (fic_tc.cu: eps has 2^-12 + 2^-13 of slack beyond fp16's 2^-11).
+template <int RS, bool TROWS, bool FULL>
+__device__ __forceinline__ void pool_warp(const PoolArgs& a, int64_t p0, int lane) {
   constexpr int K = RS * RS;
   constexpr int DPI = 32 / RS;  // domains per instruction
-  constexpr int NIT = RS;       // instructions per 32 domains
-  const int lane = threadIdx.x & 31;
-  const int64_t p0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32;
-  if (p0 >= a.D) return;
   const int g = lane / RS, i = lane % RS;
   const uint32_t D = (uint32_t)a.D;
-  // lane j locates domain p0 + j once: byte offset of its first decimated row
-  // in the box-floor planes; the RS lanes of each row read it by shuffle
   const uint32_t pm = (uint32_t)p0 + lane;
-  const uint32_t my_id = pm < D ? (a.order ? __ldg(a.order + pm) : pm) : 0u;
+  const bool mine = FULL || pm < D;
+  const uint32_t my_id = mine ? (a.order ? __ldg(a.order + pm) : pm) : 0u;
   uint32_t my_off;
   {
     const uint32_t dy = my_id / (uint32_t)a.ndx, dx = my_id - dy * (uint32_t)a.ndx;
     const uint32_t Y = dy * a.st, X = dx * a.st;
-    my_off = a.trows ? ((dx * 2u + (Y & 1u)) * (uint32_t)a.mh + (Y >> 1))
-                     : (X & 1) * (uint32_t)a.plane_rows * (uint32_t)a.pitch + Y * (uint32_t)a.pitch + (X >> 1);
+    my_off = TROWS ? ((dx * 2u + (Y & 1u)) * (uint32_t)a.mh + (Y >> 1))
+                   : (X & 1) * (uint32_t)a.plane_rows * (uint32_t)a.pitch + Y * (uint32_t)a.pitch + (X >> 1);
   }
   const uint32_t ip = (uint32_t)(2 * i) * (uint32_t)a.pitch;
+  const unsigned long long* trow = TROWS ? a.trows + i : nullptr;
+  const uint8_t* prow = TROWS ? nullptr : a.planes + ip;
+  // this lane's fp16 row in the first domain it writes; +DPI domains per step
+  uint16_t* bq = a.bh ? a.bh + (size_t)(p0 + g) * K + i * RS : nullptr;
   uint32_t my_sd = 0, my_sdd = 0;
   const float2 kk = make_float2((float)K, (float)K);
 #pragma unroll
-  for (int k = 0; k < NIT; ++k) {
-    const uint32_t p = (uint32_t)p0 + k * DPI + g;
-    const bool ok = p < D;
-    const uint32_t off = __shfl_sync(0xffffffffu, my_off, (k * DPI + g) & 31);
+  for (int k = 0; k < RS; ++k) {
+    const int dk = k * DPI + g;                 // domain of this lane in step k
+    const bool ok = FULL || (uint32_t)p0 + dk < D;
+    const uint32_t off = __shfl_sync(0xffffffffu, my_off, dk);
     unsigned long long r = 0ull;
-    if (ok) r = (RS == 8 && a.trows) ? __ldg(a.trows + off + i) : bytes8_at(a.planes + off + ip);
+    if (ok) r = TROWS ? __ldg(trow + off) : bytes8_at(prow + off);
     const uint32_t w0 = (uint32_t)r, w1 = RS == 8 ? (uint32_t)(r >> 32) : 0u;
     // row sums with byte dot products: sum x and sum x^2
     uint32_t sd = __dp4a(w0, 0x01010101u, 0u), sdd = __dp4a(w0, w0, 0u);
@@ -1111,12 +1121,16 @@ __global__ void __launch_bounds__(256, 8) k_pool(PoolArgs a) {
       my_sd = t_sd;
       my_sdd = t_sdd;
     }
-    if (!ok || !a.bh) continue;
-    // B row: fp16(fp32(K x - sum_d) * rsqrt(K den)); x from the byte via
-    // 0x4B0000xx - 2^23 (exact), K x - sum_d by an exact FMA (|.| < 2^24),
-    // packed fp32 pairs.  rsqrtf's ~2 ulp are far inside the screen's slack.
+    if (a.bh != nullptr && ok) {
+    // x from the byte via 0x4B0000xx - 2^23 (exact), K x - sum_d by an exact
+    // FMA (|.| < 2^24), packed fp32 pairs; rsqrtf's ~2 ulp are far inside the
+    // screen's slack
     const int den = K * (int)sdd - (int)sd * (int)sd;  // < 2^31
-    const float sc = den > 0 ? rsqrtf((float)K * (float)den) : 0.0f;
+    float sc = 0.0f;
+    if (den > 0) {  // K den >= K: no denormal fix-up needed
+      const float kd = (float)K * (float)den;
+      asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(sc) : "f"(kd));
+    }
     const float2 sc2 = make_float2(sc, sc), offs = make_float2(-(float)sd, -(float)sd);
     uint32_t h[RS / 2];
 #pragma unroll
@@ -1130,16 +1144,31 @@ __global__ void __launch_bounds__(256, 8) k_pool(PoolArgs a) {
       __half2 hv = __floats2half2_rn(f.x, f.y);
       h[e] = *reinterpret_cast<uint32_t*>(&hv);
     }
+    uint16_t* dst = bq + (size_t)k * DPI * K;
     if (RS == 8)
-      reinterpret_cast<uint4*>(a.bh + (size_t)p * K)[i] = make_uint4(h[0], h[1], h[2], h[3]);
+      *reinterpret_cast<uint4*>(dst) = make_uint4(h[0], h[1], h[2], h[3]);
     else
-      reinterpret_cast<uint2*>(a.bh + (size_t)p * K)[i] = make_uint2(h[0], h[1]);
+      *reinterpret_cast<uint2*>(dst) = make_uint2(h[0], h[1]);
+    }
   }
-  if (pm < D) {
+  if (mine) {
     const int64_t den = (int64_t)K * my_sdd - (int64_t)my_sd * my_sd;
-    a.inv_den[pm] = den != 0 ? __ddiv_rn(1.0, (double)den) : 0.0;
+    a.inv_den[pm] = den != 0 ? __drcp_rn((double)den) : 0.0;
     a.sums[pm] = make_uint2(my_sd, my_sdd);
   }
+}
+
+template <int RS, bool TROWS>
+__global__ void __launch_bounds__(256, 8) k_pool(PoolArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int64_t p0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32;
+  if (p0 >= a.D) return;
+  // whole warps skip the per-row bounds checks (a vote keeps the branch
+  // warp-uniform for the shuffles inside)
+  if (__all_sync(0xffffffffu, p0 + 32 <= a.D))
+    pool_warp<RS, TROWS, true>(a, p0, lane);
+  else
+    pool_warp<RS, TROWS, false>(a, p0, lane);
 }
 
 __global__ void k_pool_generic(PoolArgs a, int rs) {
@@ -1161,7 +1190,7 @@ __global__ void k_pool_generic(PoolArgs a, int rs) {
     }
   for (int k = K; k < a.KP; ++k) out[k] = 0;  // zero padding: dp4a over whole words
   int64_t den = (int64_t)K * sdd - (int64_t)sd * sd;
-  a.inv_den[p] = den != 0 ? __ddiv_rn(1.0, (double)den) : 0.0;
+  a.inv_den[p] = den != 0 ? __drcp_rn((double)den) : 0.0;
   a.sums[p] = make_uint2(sd, sdd);
 }
 
@@ -1177,16 +1206,16 @@ void launch_pool(const PoolArgs& a, cudaStream_t s) {
     k_domrows<<<grid, 256, smem, s>>>(a.img, a.H, a.W, a.st, a.ndx, a.mh, a.trows);
     FIC_CHECK_LAUNCH();
     if (a.ev_main) FIC_CUDA(cudaEventRecord(a.ev_main, s));
-    k_pool<8><<<blocks, 256, 0, s>>>(a);
+    k_pool<8, true><<<blocks, 256, 0, s>>>(a);
   } else if ((a.rs == 8 || a.rs == 4) && a.planes) {
     dim3 grid((unsigned)cdiv(cdiv(a.W - 1, 16), 256), (unsigned)(a.H - 1));
     k_boxplanes<<<grid, 256, 0, s>>>(a.img, a.H, a.W, a.pitch, a.planes);
     FIC_CHECK_LAUNCH();
     if (a.ev_main) FIC_CUDA(cudaEventRecord(a.ev_main, s));
     if (a.rs == 8)
-      k_pool<8><<<blocks, 256, 0, s>>>(a);
+      k_pool<8, false><<<blocks, 256, 0, s>>>(a);
     else
-      k_pool<4><<<blocks, 256, 0, s>>>(a);
+      k_pool<4, false><<<blocks, 256, 0, s>>>(a);
   } else {
     if (a.ev_main) FIC_CUDA(cudaEventRecord(a.ev_main, s));
     k_pool_generic<<<blocks, 256, 0, s>>>(a, a.rs);

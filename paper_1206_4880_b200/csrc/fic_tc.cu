@@ -752,6 +752,26 @@ __global__ void __maxnreg__(MAXREG)
             handover = __shfl_sync(0xffffffffu, handover, lane & ~(n_iso - 1));
             if (handover) m = 0;
           }
+          if (a.sl) {
+            // survivors the row's queue cannot take now go to the survivor
+            // list as one (row, chunk, mask) entry: the screener never waits
+            // for the rescoring warp on a chunk with many survivors
+            const uint32_t n = (uint32_t)__popcll(m);
+            const bool to_list = n > (uint32_t)QCAP - (qt - *myhead);
+            const unsigned lm = __ballot_sync(0xffffffffu, to_list);
+            if (lm) {
+              const int leader = __ffs(lm) - 1;
+              uint32_t base = 0;
+              if (lane == leader) base = atomicAdd(a.sl_count, (uint32_t)__popc(lm));
+              base = __shfl_sync(0xffffffffu, base, leader);
+              const uint32_t idx = base + (uint32_t)__popc(lm & ((1u << lane) - 1u));
+              if (to_list && idx < a.sl_cap) {
+                a.sl[idx] = make_uint4((rid << 3) | (uint32_t)iso, (uint32_t)(c0 + rel), (uint32_t)m,
+                                       (uint32_t)(m >> 32));
+                m = 0;
+              }
+            }
+          }
           while (m) {
             const int e = __ffsll((long long)m) - 1;
             m &= m - 1;

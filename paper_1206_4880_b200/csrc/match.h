@@ -147,12 +147,33 @@ struct TcArgs {
   // CUDA-core bulk pass over its whole slab is cheaper than rescoring them
   // one by one -- gets bulk_idx[r] = its list slot + 1 and no more survivors
   // are pushed for it.  nullptr = off.
+  // Survivor list: a hit chunk whose row queue cannot take its survivors
+  // writes one 16-byte entry (range id << 3 | isometry, pool column of bit
+  // 0, 64-bit survivor mask) here instead of waiting for the rescoring warp;
+  // k_sl_rescore evaluates them after the matcher.  nullptr = off.
+  uint4* sl;
+  uint32_t* sl_count;          // [1] entries appended (may exceed sl_cap: the rest were queued)
+  uint32_t sl_cap;
   uint32_t* surv_g;            // [R] survivors pushed so far
   uint32_t* bulk_idx;          // [R] 0 or list slot + 1
   uint32_t* bulk_list;         // [bulk_cap] range ids
   uint32_t* n_bulk;            // [1] ranges handed over (may exceed bulk_cap: those are not)
   int bulk_cap, bulk_min, bulk_shift;
 };
+
+// Rescoring of the survivor list: every candidate of every entry, exactly;
+// per-range lexicographic (err, dom, iso) minimum by a 128-bit CAS on
+// best[r] = {dom << 32 | iso << 24 | s_q << 16 | o_q << 8, err bits} and the
+// pre-quantisation minimum by a 64-bit atomicMin on pre[r].
+struct SlArgs {
+  const uint4* sl;
+  const uint32_t* sl_count;
+  uint32_t sl_cap;
+  unsigned long long* best;    // [R][2]
+  unsigned long long* pre;     // [R]
+  unsigned long long* counters;  // [0] exact evaluations
+};
+void launch_sl_rescore(const PoolView& P, const RangeView& Rv, const SlArgs& a, cudaStream_t s);
 
 constexpr int kBulkPieces = 64;  // column pieces (blocks) per bulk range
 struct BulkArgs {
@@ -207,6 +228,8 @@ struct MergeArgs {
   double n;                    // pixels per range
   const uint32_t* bulk_idx;    // optional [R]: 0 or bulk list slot + 1
   const Partial* bulk_part;    // [cap * kBulkPieces]
+  const unsigned long long* sl_best;  // optional [R][2] (SlArgs)
+  const unsigned long long* sl_pre;   // [R]
 };
 void launch_merge(const MergeArgs& a, cudaStream_t s);
 
