@@ -288,7 +288,9 @@ __global__ void k_classify(ClassifyArgs a) {
     if (a.bin) {  // lo_rank orders like lo (rank_start is monotone)
       const uint32_t b = (uint32_t)cls * (uint32_t)(a.n_rank + 1) + a.lo_rank[r];
       a.bin[r] = b;
-      atomicAdd(a.bin_hist + b, 1u);
+      // neighbouring ranges often share a bin: one atomic per group of equal bins
+      const unsigned grp = __match_any_sync(__activemask(), b);
+      if ((int)(threadIdx.x & 31) == __ffs(grp) - 1) atomicAdd(a.bin_hist + b, (uint32_t)__popc(grp));
     }
     if (a.pool_out) a.pool_out[r] = (int64_t)pool;
   }
@@ -616,35 +618,53 @@ __global__ void k_expand(const int32_t* nseg, const int32_t* base, const DevPlan
   for (int s = 0; s < nseg[t]; ++s) items[b + s] = make_int2((int)t, s);
 }
 
-// Work items in segment-major order: (tile t, segment s) sorted by (s, t).
-// One block: for each segment index, a block-wide scan of "tile t has a
-// segment s" gives the rank of t among those tiles.
-__global__ void __launch_bounds__(1024) k_items_segmajor(const int32_t* nseg, const DevPlan* dp,
-                                                         int2* items) {
-  const int64_t n = dp->n_tt;
-  using Scan = cub::BlockScan<int, 1024>;
-  using Reduce = cub::BlockReduce<int, 1024>;
-  __shared__ typename Scan::TempStorage scan_tmp;
-  __shared__ typename Reduce::TempStorage red_tmp;
-  __shared__ int s_max, s_total;
-  int mx = 0;
-  for (int64_t t = threadIdx.x; t < n; t += 1024) mx = max(mx, nseg[t]);
-  mx = Reduce(red_tmp).Reduce(mx, cuda::maximum<>{});
-  if (threadIdx.x == 0) s_max = mx;
-  __syncthreads();
-  int64_t base = 0;
-  for (int seg = 0; seg < s_max; ++seg) {
-    for (int64_t t0 = 0; t0 < n; t0 += 1024) {
-      const int64_t t = t0 + threadIdx.x;
-      const int flag = (t < n && nseg[t] > seg) ? 1 : 0;
-      int rank = 0, total = 0;
-      Scan(scan_tmp).ExclusiveSum(flag, rank, total);
-      if (flag) items[base + rank] = make_int2((int)t, seg);
-      base += total;
-      __syncthreads();
-    }
+// Work items in segment-major order: every tile's segment s before any
+// segment s + 1, so later segments start from the thresholds the earlier
+// ones found.  k_seg_hist counts the tiles per segment count, k_seg_base
+// turns that into each segment's first item, k_seg_fill places the items
+// (warp-aggregated atomics: inside a segment the tiles come roughly in tile
+// order, i.e. neighbouring FD windows run together; the order is scheduling
+// only, results do not depend on it).
+__global__ void k_seg_hist(const int32_t* nseg, const DevPlan* dp, int smax, uint32_t* hist) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= dp->n_tt) return;
+  atomicAdd(hist + min((int)nseg[t], smax), 1u);
+}
+
+__global__ void __launch_bounds__(1024) k_seg_base(const uint32_t* hist, int smax, uint32_t* base,
+                                                   uint32_t* cursor) {
+  // cnt[s] = tiles with more than s segments; base = exclusive scan of cnt
+  if (threadIdx.x != 0) return;
+  uint32_t above = 0, acc = 0;
+  for (int v = smax; v >= 1; --v) {  // cnt[v - 1] = sum of hist[v .. smax]
+    above += hist[v];
+    cursor[v - 1] = above;           // temporarily the count
+  }
+  for (int s2 = 0; s2 < smax; ++s2) {
+    const uint32_t c = cursor[s2];
+    base[s2] = acc;
+    acc += c;
+    cursor[s2] = 0;
   }
 }
+
+__global__ void k_seg_fill(const int32_t* nseg, const DevPlan* dp, const uint32_t* base,
+                           uint32_t* cursor, int2* items) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int ns = t < dp->n_tt ? nseg[t] : 0;
+  const int mx = __reduce_max_sync(0xffffffffu, ns);
+  for (int sg = 0; sg < mx; ++sg) {
+    const bool act = ns > sg;
+    const unsigned bal = __ballot_sync(0xffffffffu, act);
+    const int leader = __ffs(bal) - 1;
+    uint32_t off = 0;
+    if (lane == leader) off = atomicAdd(cursor + sg, (uint32_t)__popc(bal));
+    off = __shfl_sync(0xffffffffu, off, leader);
+    if (act) items[base[sg] + off + __popc(bal & ((1u << lane) - 1u))] = make_int2((int)t, sg);
+  }
+}
+
 // ---- compact FD sort ---------------------------------------------------
 // With a few scales and small counts the domain FDs take few distinct values
 // (side 16: FD depends on (N2, N8) only, the middle weight being 0.0), so the
@@ -1233,7 +1253,16 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
   if (n_tt_max) {
     // segment-major order: every tile's first segment runs before any second
     // segment, so later segments start from the thresholds the earlier ones found
-    k_items_segmajor<<<1, 1024, 0, s>>>(tnseg, d_plan, titems);
+    const int smax = (int)segs_max;
+    uint32_t* shist = sc.get<uint32_t>(smax + 1);
+    uint32_t* sbase2 = sc.get<uint32_t>(smax);
+    uint32_t* scur = sc.get<uint32_t>(smax);
+    FIC_CUDA(cudaMemsetAsync(shist, 0, (smax + 1) * sizeof(uint32_t), s));
+    k_seg_hist<<<(unsigned)cdiv(n_tt_max, 256), 256, 0, s>>>(tnseg, d_plan, smax, shist);
+    FIC_CHECK_LAUNCH();
+    k_seg_base<<<1, 32, 0, s>>>(shist, smax, sbase2, scur);
+    FIC_CHECK_LAUNCH();
+    k_seg_fill<<<(unsigned)cdiv(n_tt_max, 256), 256, 0, s>>>(tnseg, d_plan, sbase2, scur, titems);
     FIC_CHECK_LAUNCH();
   }
   k_expand<<<(unsigned)cdiv(n_er_max, 128), 128, 0, s>>>(enseg, ebase, d_plan, eitems);
@@ -1267,6 +1296,7 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
       if (getenv("FIC_SL_CAP")) ta.sl_cap = (uint32_t)std::max(1, atoi(getenv("FIC_SL_CAP")));
       ta.sl = sc.get<uint4>(ta.sl_cap);
       ta.sl_count = d_rb->n_bulk + 1;
+      ta.sl_all = getenv("FIC_SL_ALL") ? atoi(getenv("FIC_SL_ALL")) : 0;
       sla.sl = ta.sl;
       sla.sl_count = ta.sl_count;
       sla.sl_cap = ta.sl_cap;

@@ -365,58 +365,64 @@ void launch_exact(const PoolView& P, const RangeView& Rv, const ExactArgs& a, cu
   FIC_CHECK_LAUNCH();
 }
 
-// K6: merge partials (per range) into the raster-order outputs.
+// K6: merge partials (per range) into the raster-order outputs.  One warp
+// per range: the lanes stride over its partial slots (and bulk pieces),
+// then a lexicographic warp reduction; the survivor list's best joins in.
 __global__ void k_merge(MergeArgs a) {
-  int r = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (r >= a.R) return;
-  int ns = a.nslots[r];
+  const int ns = a.nslots[r];
   if (ns == 0) return;
   const Partial* p = a.partials + a.slot_base[r];
-  // a range the bulk pass took over also has its kBulkPieces partials there
+  // a range the bulk pass took over also has its kBulkPieces partials
   const uint32_t bi = a.bulk_idx ? a.bulk_idx[r] : 0u;
   const Partial* pb = bi ? a.bulk_part + (int64_t)(bi - 1) * kBulkPieces : nullptr;
-  double err = INFINITY, pre = INFINITY;
-  uint32_t dom = 0xffffffffu;
-  int iso = 0, sq = 0, oq = 0;
-  if (a.sl_best) {  // the survivor list's best for this range (k_sl_rescore)
-    const unsigned long long hi = a.sl_best[2 * (int64_t)r + 1], lo = a.sl_best[2 * (int64_t)r];
+  Best b;
+  best_init(b);
+  if (a.sl_best && lane == 0) {  // the survivor list's best for this range (k_sl_rescore)
+    const unsigned long long hi = a.sl_best[2 * r + 1], lo = a.sl_best[2 * r];
     if (hi != ord_bits(INFINITY)) {
-      err = unord_bits(hi);
-      dom = (uint32_t)(lo >> 32);
-      iso = (int)((lo >> 24) & 255u);
-      sq = (int)((lo >> 16) & 255u);
-      oq = (int)((lo >> 8) & 255u);
+      b.err = unord_bits(hi);
+      b.dom = (uint32_t)(lo >> 32);
+      b.iso = (int)((lo >> 24) & 255u);
+      b.sq = (int)((lo >> 16) & 255u);
+      b.oq = (int)((lo >> 8) & 255u);
     }
-    pre = unord_bits(a.sl_pre[r]);
+    b.pre = unord_bits(a.sl_pre[r]);
   }
-  for (int i = 0; i < ns + (pb ? kBulkPieces : 0); ++i) {
-    Partial q = i < ns ? p[i] : pb[i - ns];
+  const int n = ns + (pb ? kBulkPieces : 0);
+  for (int i = lane; i < n; i += 32) {
+    const Partial q = i < ns ? p[i] : pb[i - ns];
     if (!q.valid) continue;
-    pre = fmin(pre, q.pre);
-    if (better(q.err, q.dom, q.iso, err, dom, iso)) {
-      err = q.err;
-      dom = q.dom;
-      iso = q.iso;
-      sq = q.sq;
-      oq = q.oq;
-    }
+    Best c;
+    c.err = q.err;
+    c.pre = q.pre;
+    c.dom = q.dom;
+    c.iso = q.iso;
+    c.sq = q.sq;
+    c.oq = q.oq;
+    best_merge(b, c);
   }
-  uint8_t* rec = a.records + (int64_t)r * 7;
-  rec[0] = dom & 255;
-  rec[1] = (dom >> 8) & 255;
-  rec[2] = (dom >> 16) & 255;
-  rec[3] = dom >> 24;
-  rec[4] = (uint8_t)iso;
-  rec[5] = (uint8_t)sq;
-  rec[6] = (uint8_t)oq;
+#pragma unroll
+  for (int m = 16; m >= 1; m >>= 1) best_merge(b, shfl_best(b, m));
+  if (lane != 0) return;
+  uint8_t* rec = a.records + r * 7;
+  rec[0] = b.dom & 255;
+  rec[1] = (b.dom >> 8) & 255;
+  rec[2] = (b.dom >> 16) & 255;
+  rec[3] = b.dom >> 24;
+  rec[4] = (uint8_t)b.iso;
+  rec[5] = (uint8_t)b.sq;
+  rec[6] = (uint8_t)b.oq;
   // codec.py:263-264
-  a.post_rms[r] = __dsqrt_rn(__ddiv_rn(fmax(err, 0.0), a.n));
-  a.pre_rms[r] = __dsqrt_rn(__ddiv_rn(fmax(pre, 0.0), a.n));
+  a.post_rms[r] = __dsqrt_rn(__ddiv_rn(fmax(b.err, 0.0), a.n));
+  a.pre_rms[r] = __dsqrt_rn(__ddiv_rn(fmax(b.pre, 0.0), a.n));
 }
 
 void launch_merge(const MergeArgs& a, cudaStream_t s) {
   if (a.R == 0) return;
-  k_merge<<<(unsigned)cdiv(a.R, 256), 256, 0, s>>>(a);
+  k_merge<<<(unsigned)cdiv((int64_t)a.R * 32, 256), 256, 0, s>>>(a);
   FIC_CHECK_LAUNCH();
 }
 

@@ -757,7 +757,7 @@ __global__ void __maxnreg__(MAXREG)
             // list as one (row, chunk, mask) entry: the screener never waits
             // for the rescoring warp on a chunk with many survivors
             const uint32_t n = (uint32_t)__popcll(m);
-            const bool to_list = n > (uint32_t)QCAP - (qt - *myhead);
+            const bool to_list = a.sl_all ? n > 0 : n > (uint32_t)QCAP - (qt - *myhead);
             const unsigned lm = __ballot_sync(0xffffffffu, to_list);
             if (lm) {
               const int leader = __ffs(lm) - 1;

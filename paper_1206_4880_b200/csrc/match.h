@@ -154,6 +154,7 @@ struct TcArgs {
   uint4* sl;
   uint32_t* sl_count;          // [1] entries appended (may exceed sl_cap: the rest were queued)
   uint32_t sl_cap;
+  int sl_all;                  // 1: every survivor goes to the list (the queues carry seeds only)
   uint32_t* surv_g;            // [R] survivors pushed so far
   uint32_t* bulk_idx;          // [R] 0 or list slot + 1
   uint32_t* bulk_list;         // [bulk_cap] range ids
