@@ -1290,9 +1290,12 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
       ta.flat_c = fl.flat_c;
       ta.flat_canon = fl.canon;
     }
-    if (!getenv("FIC_NO_SL")) {
-      // survivor list (TcArgs::sl): capacity min(16 M, max(1 M, 128 R)) entries
-      ta.sl_cap = (uint32_t)std::min<int64_t>(16 << 20, std::max<int64_t>(1 << 20, 128 * (int64_t)g.R));
+    if (getenv("FIC_SL") && atoi(getenv("FIC_SL"))) {
+      // survivor list (TcArgs::sl, opt-in: measured no faster than the
+      // rescoring warp -- without its threshold feedback the list grows to
+      // billions of candidates at cfg4): 16-byte entries,
+      // capacity min(128 M, max(1 M, 2048 R)) (2 GB at most)
+      ta.sl_cap = (uint32_t)std::min<int64_t>(128 << 20, std::max<int64_t>(1 << 20, 2048 * (int64_t)g.R));
       if (getenv("FIC_SL_CAP")) ta.sl_cap = (uint32_t)std::max(1, atoi(getenv("FIC_SL_CAP")));
       ta.sl = sc.get<uint4>(ta.sl_cap);
       ta.sl_count = d_rb->n_bulk + 1;

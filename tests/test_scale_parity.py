@@ -160,30 +160,30 @@ def test_pool_builder_outputs_match_reference(cname, strategy, planes, monkeypat
 
 
 @pytest.mark.parametrize("env", [{"FIC_BULK": "1", "FIC_BULK_MIN": "1", "FIC_BULK_SHIFT": "31"},
-                                 {"FIC_NO_SL": "1"}, {"FIC_SL_CAP": "7"}])
+                                 {"FIC_SL": "1"}, {"FIC_SL": "1", "FIC_SL_ALL": "1"},
+                                 {"FIC_SL": "1", "FIC_SL_CAP": "7"}])
 @pytest.mark.parametrize("prefix", ["cfg2", "cfg2_ex"])
 def test_survivor_paths_match_reference(prefix, env, monkeypatch):
     """Every way a survivor can be rescored gives the reference's records:
-    the bulk hand-over of every range with one survivor, the rescoring warp
-    only (no survivor list), and a survivor list that overflows after 7
-    entries (the rest go through the rescoring warp)."""
+    the bulk hand-over of every range with one survivor, the survivor list
+    (overflow of the rescoring warp's queues, or every survivor), and a
+    survivor list that overflows after 7 entries (the rest go through the
+    rescoring warp)."""
     for k, v in env.items():
         monkeypatch.setenv(k, v)
     _, res = _check_full("scale_cfg2.npz", prefix)
     if "FIC_BULK" in env:
         assert res.stats["bulk_ranges"] > 0
-    if "FIC_NO_SL" in env:
-        assert res.stats["sl_entries"] == 0
+    if "FIC_SL_ALL" in env:
+        assert res.stats["sl_entries"] > 0
     if "FIC_SL_CAP" in env:
         assert res.stats["sl_entries"] <= 7
 
 
-def test_cfg4_survivor_list_takes_the_storm():
-    """cfg4 (4x4 ranges): the survivor list absorbs the screen's survivors
-    and the encode stays bit-exact (test_cfg4_exhaustive_every_range...);
-    here: it is actually used, and the bulk hand-over is off by default."""
-    import torch
-    g = _golden("scale_cfg4.npz")
-    strategy, kw = _kw(g, "cfg4_ex")
-    res = codec.encode_device(torch.from_numpy(g["cfg4_ex.image"]).cuda(), strategy, **kw)
-    assert res.stats["sl_entries"] > 0 and res.stats["bulk_ranges"] == 0
+def test_cfg4_exhaustive_with_survivor_list_matches_reference(monkeypatch):
+    """cfg4 with every survivor on the survivor list (billions of
+    candidates, capacity overflow into the rescoring warp): bit-exact."""
+    monkeypatch.setenv("FIC_SL", "1")
+    monkeypatch.setenv("FIC_SL_ALL", "1")
+    _, res = _check_full("scale_cfg4.npz", "cfg4_ex")
+    assert res.stats["sl_entries"] > 0
