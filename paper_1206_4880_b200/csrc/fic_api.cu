@@ -36,9 +36,19 @@ void smem_optin(const void* func, int bytes) {
 }
 
 // ---------------------------------------------------------------------------
-// stream-ordered scratch: every buffer of a call comes from the device's
-// default memory pool (kept cached across calls) and is freed on the stream.
+// stream-ordered scratch: a call's buffers are bump-allocated from an arena
+// kept per (thread, device, stream) across calls, so a repeated encode makes
+// no allocation at all.  The arena grows (stream-ordered free + malloc from
+// the device's default pool) when a call needed more; reuse by the next call
+// on the same stream is ordered after this call's kernels by the stream.
 // ---------------------------------------------------------------------------
+struct Arena {
+  char* base = nullptr;
+  size_t cap = 0, want = 0;
+  bool busy = false;
+};
+static thread_local std::map<std::pair<int, cudaStream_t>, Arena> g_arenas;
+
 class Scratch {
  public:
   explicit Scratch(cudaStream_t s) : s_(s) {
@@ -47,30 +57,58 @@ class Scratch {
     static std::set<int> done;
     int dev = 0;
     FIC_CUDA(cudaGetDevice(&dev));
-    std::lock_guard<std::mutex> lock(mu);
-    if (!done.count(dev)) {
-      cudaMemPool_t pool;
-      if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-        uint64_t thr = UINT64_MAX;
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    {
+      std::lock_guard<std::mutex> lock(mu);
+      if (!done.count(dev)) {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+          uint64_t thr = UINT64_MAX;
+          cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+        done.insert(dev);
       }
-      done.insert(dev);
+    }
+    Arena& ar = g_arenas[{dev, s}];
+    if (!ar.busy && !getenv("FIC_NO_ARENA")) {
+      ar.busy = true;
+      if (ar.cap < ar.want) {  // grow: the last call on this stream needed more
+        if (ar.base) FIC_CUDA(cudaFreeAsync(ar.base, s_));
+        ar.base = nullptr;
+        ar.cap = 0;
+        const size_t cap = ar.want + ar.want / 4;
+        FIC_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ar.base), cap, s_));
+        ar.cap = cap;
+      }
+      arena_ = &ar;
     }
   }
   ~Scratch() {
     for (void* p : ptrs_) cudaFreeAsync(p, s_);
+    if (arena_) {
+      arena_->want = std::max(arena_->want, used_);
+      arena_->busy = false;
+    }
   }
   template <class T>
   T* get(size_t n) {
     if (n == 0) n = 1;
-    void* p = nullptr;
-    FIC_CUDA(cudaMallocAsync(&p, n * sizeof(T), s_));
+    const size_t bytes = align_up(n * sizeof(T), 256);
+    used_ += bytes;
+    if (arena_ && off_ + bytes <= arena_->cap) {
+      T* p = reinterpret_cast<T*>(arena_->base + off_);
+      off_ += bytes;
+      return p;
+    }
+    void* p = nullptr;  // beyond the arena: a pool allocation freed at the end
+    FIC_CUDA(cudaMallocAsync(&p, bytes, s_));
     ptrs_.push_back(p);
     return static_cast<T*>(p);
   }
 
  private:
   cudaStream_t s_;
+  Arena* arena_ = nullptr;
+  size_t off_ = 0, used_ = 0;
   std::vector<void*> ptrs_;
 };
 
@@ -1798,6 +1836,14 @@ extern "C" int fic_abi_version(void) { return FIC_ABI_VERSION; }
 extern "C" void fic_release(void) {
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return;
+  for (auto it = g_arenas.begin(); it != g_arenas.end();) {  // this thread's arenas on dev
+    if (it->first.first == dev && !it->second.busy) {
+      if (it->second.base) cudaFreeAsync(it->second.base, it->first.second);
+      it = g_arenas.erase(it);
+    } else {
+      ++it;
+    }
+  }
   cudaMemPool_t pool;
   if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
     cudaDeviceSynchronize();

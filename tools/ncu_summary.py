@@ -85,6 +85,17 @@ def main():
             tr = to_bytes(*d["dram__bytes_read.sum"]) + to_bytes(*d["dram__bytes_write.sum"])
             with open(os.path.join(os.path.dirname(prefix) or ".", "tc_matcher_traffic.json"), "w") as f:
                 json.dump({"dram_bytes_per_launch": tr, "source": os.path.basename(rep)}, f)
+        for kname in ("k_pool", "k_domrows"):
+            if kname in name and "dram__bytes_read.sum" in d and "cfg3" in os.path.basename(rep):
+                tr = sum(float(d[m][0].replace(",", "")) *
+                         {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(d[m][1], 1)
+                         for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+                path = os.path.join(os.path.dirname(prefix) or ".", "k1_traffic.json")
+                cur = json.load(open(path)) if os.path.exists(path) else {}
+                cur[kname] = tr
+                cur["source"] = os.path.basename(rep)
+                with open(path, "w") as f:
+                    json.dump(cur, f)
     agg, tot = launches(lcsv)
     lines += ["## launch list (ncu gpu__time_duration, serialised, cold caches)", "",
               "| kernel | time (us) | share |", "|---|---|---|"]
