@@ -109,8 +109,8 @@ typedef struct fic_stats {
   int32_t tensor_tiles, exact_tiles, work_items;
   int32_t kernel_launches;   /* kernels this call launched (library-internal CUB passes excluded) */
   double ms_pool_main;       /* device time of the pool builder's main kernel (k_pool) alone */
-  int64_t bulk_ranges;       /* ranges the tensor screen handed to the CUDA-core bulk pass */
-  double ms_bulk;            /* device time of the survivor-list rescoring + bulk passes */
+  int64_t reserved0;         /* 0 */
+  double ms_sl;              /* device time of the survivor-list rescoring (k_sl_rescore) */
   int64_t sl_entries;        /* survivor-list entries (row, 64-column chunk, mask) rescored after the matcher */
 } fic_stats_t;
 

@@ -64,8 +64,8 @@ class FicStats(ctypes.Structure):
         ("work_items", ctypes.c_int32),
         ("kernel_launches", ctypes.c_int32),
         ("ms_pool_main", ctypes.c_double),
-        ("bulk_ranges", ctypes.c_int64),
-        ("ms_bulk", ctypes.c_double),
+        ("reserved0", ctypes.c_int64),
+        ("ms_sl", ctypes.c_double),
         ("sl_entries", ctypes.c_int64),
     ]
 

@@ -226,12 +226,15 @@ def encode_device(image_dev, strategy="dynamic_fd", *, range_size=8, domain_size
     image_dev, h, w = validate(image_dev, strategy, range_size, domain_size, stride, fd_source)
     dev = image_dev.device
     n_r = (h // range_size) * (w // range_size)
-    if out is None:  # (no clearing: a full encode writes every range's outputs)
+    if out is None:
+        # a full encode writes every range's outputs; a shard only its own
+        # ranges, the others are zero
+        new = torch.empty if tuple(shard) == (0, 1) else torch.zeros
         out = DeviceResult(
-            torch.empty((n_r, 7), dtype=torch.uint8, device=dev),
-            torch.empty(n_r, dtype=torch.float64, device=dev),
-            torch.empty(n_r, dtype=torch.float64, device=dev),
-            torch.empty(n_r, dtype=torch.int64, device=dev), {})
+            new((n_r, 7), dtype=torch.uint8, device=dev),
+            new(n_r, dtype=torch.float64, device=dev),
+            new(n_r, dtype=torch.float64, device=dev),
+            new(n_r, dtype=torch.int64, device=dev), {})
     img = image_dev.contiguous()
     prm = make_params(strategy, range_size, domain_size, stride, isometries, fd_source,
                       delta, matcher, shard, max_segment, small_pool)

@@ -1119,7 +1119,7 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
     double scal[4];
     DevPlan plan;
     unsigned long long flat[2];  // [0] flat count, [1] low word: canonical flat range
-    uint32_t n_bulk[2];          // [0] ranges handed to the bulk pass, [1] survivor-list entries
+    uint32_t sl_count[2];        // [0] survivor-list entries appended
   };
   Readback* d_rb = sc.get<Readback>(1);
   FIC_CUDA(cudaMemsetAsync(d_rb, 0, sizeof(Readback), s));
@@ -1312,9 +1312,6 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
   RangeView Rv{ra.info, ra.rows, pb.lo, pb.hi, g.n_iso, K, ra.KP};
   tm.mark();  // 3
   SlArgs sla{};                    // survivor list (k_sl_rescore)
-  BulkArgs bulk{};                 // ranges the screen hands over (k_bulk)
-  const uint32_t* bulk_idx = nullptr;
-  const uint32_t* surv_g = nullptr;
   if (n_tt_max && titems_n) {
     unsigned long long* thr_g = sc.get<unsigned long long>(g.R);
     k_fill_u64<<<(unsigned)cdiv(g.R, 256), 256, 0, s>>>(thr_g, 0x7ff0000000000000ull, g.R);
@@ -1336,7 +1333,7 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
       ta.sl_cap = (uint32_t)std::min<int64_t>(128 << 20, std::max<int64_t>(1 << 20, 2048 * (int64_t)g.R));
       if (getenv("FIC_SL_CAP")) ta.sl_cap = (uint32_t)std::max(1, atoi(getenv("FIC_SL_CAP")));
       ta.sl = sc.get<uint4>(ta.sl_cap);
-      ta.sl_count = d_rb->n_bulk + 1;
+      ta.sl_count = d_rb->sl_count;
       ta.sl_all = getenv("FIC_SL_ALL") ? atoi(getenv("FIC_SL_ALL")) : 0;
       sla.sl = ta.sl;
       sla.sl_count = ta.sl_count;
@@ -1346,24 +1343,6 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
       sla.counters = counters;
       k_sl_init<<<(unsigned)cdiv(g.R, 256), 256, 0, s>>>(sla.best, sla.pre, g.R);
       FIC_CHECK_LAUNCH();
-    }
-    if (getenv("FIC_BULK")) {
-      ta.surv_g = sc.get<uint32_t>(g.R);
-      ta.bulk_idx = sc.get<uint32_t>(g.R);
-      FIC_CUDA(cudaMemsetAsync(ta.surv_g, 0, g.R * sizeof(uint32_t), s));
-      FIC_CUDA(cudaMemsetAsync(ta.bulk_idx, 0, g.R * sizeof(uint32_t), s));
-      ta.bulk_cap = (int)std::min<int64_t>(g.R, 4096);
-      ta.bulk_list = sc.get<uint32_t>(ta.bulk_cap);
-      ta.n_bulk = d_rb->n_bulk;
-      ta.bulk_min = getenv("FIC_BULK_MIN") ? std::max(1, atoi(getenv("FIC_BULK_MIN"))) : 2048;
-      ta.bulk_shift = getenv("FIC_BULK_SHIFT") ? std::min(31, std::max(0, atoi(getenv("FIC_BULK_SHIFT")))) : 6;
-      bulk.list = ta.bulk_list;
-      bulk.n_bulk = ta.n_bulk;
-      bulk.cap = ta.bulk_cap;
-      bulk.partials = sc.get<Partial>((size_t)ta.bulk_cap * kBulkPieces);
-      bulk.counters = counters;
-      bulk_idx = ta.bulk_idx;
-      surv_g = ta.surv_g;
     }
     const char* dbg_env = getenv("FIC_TC_DEBUG");
     if (dbg_env && (atoi(dbg_env) & (32 | 8192))) {
@@ -1406,18 +1385,7 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
     }
   }
   FIC_CUDA(cudaEventRecord(tm.ev[21], s));
-  if (getenv("FIC_SURV_DUMP") && surv_g) {  // per-range survivors / hand-overs (analysis only)
-    std::vector<uint32_t> h(2 * (size_t)g.R);
-    FIC_CUDA(cudaMemcpyAsync(h.data(), surv_g, g.R * 4, cudaMemcpyDeviceToHost, s));
-    FIC_CUDA(cudaMemcpyAsync(h.data() + g.R, bulk_idx, g.R * 4, cudaMemcpyDeviceToHost, s));
-    FIC_CUDA(cudaStreamSynchronize(s));
-    if (FILE* f = fopen(getenv("FIC_SURV_DUMP"), "wb")) {
-      fwrite(h.data(), 4, h.size(), f);
-      fclose(f);
-    }
-  }
   launch_sl_rescore(P, Rv, sla, s);
-  launch_bulk(P, Rv, bulk, s);
   FIC_CUDA(cudaEventRecord(tm.ev[22], s));
   tm.mark();  // 4
   if (eitems_n) {
@@ -1425,8 +1393,8 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
     launch_exact(P, Rv, ea, s);
   }
   tm.mark();  // 5
-  MergeArgs ma{g.R, sbase, nslots, partials, records, pre_rms, post_rms, (double)K, bulk_idx,
-               bulk.partials, sla.best, sla.pre};
+  MergeArgs ma{g.R, sbase, nslots, partials, records, pre_rms, post_rms, (double)K, sla.best,
+               sla.pre};
   launch_merge(ma, s);
   tm.mark();  // 6
 
@@ -1479,9 +1447,8 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
     }
     st->ms_match = tm.ms(3, 6);
     st->ms_tensor = tm.ms(3, 21);
-    st->ms_bulk = tm.ms(21, 22);
-    st->bulk_ranges = std::min<int64_t>(hrb.n_bulk[0], bulk.cap);
-    st->sl_entries = std::min<int64_t>(hrb.n_bulk[1], sla.sl_cap);
+    st->ms_sl = tm.ms(21, 22);
+    st->sl_entries = std::min<int64_t>(hrb.sl_count[0], sla.sl_cap);
     st->ms_exact = tm.ms(4, 5);
     st->ms_total = n_flat ? tm.ms(0, 23) : tm.ms(0, 7);
     st->exact_evals = (int64_t)hc[0];

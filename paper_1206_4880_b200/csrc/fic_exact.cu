@@ -138,30 +138,6 @@ __global__ void __launch_bounds__(256) k_exact(PoolView P, RangeView Rv, ExactAr
   }
 }
 
-// Bulk pass for the ranges the tensor matcher handed over (TcArgs::bulk_*):
-// every candidate of each listed range, its slab cut into kBulkPieces equal
-// column pieces, one block per (range, piece); partial f * kBulkPieces + piece.
-template <int K>
-__global__ void __launch_bounds__(256) k_bulk(PoolView P, RangeView Rv, BulkArgs a) {
-  constexpr int KW = K / 4;
-  __shared__ uint32_t srow[8][KW];
-  __shared__ Best sbest[8];
-  const int64_t n_items = (int64_t)min(*a.n_bulk, (uint32_t)a.cap) * kBulkPieces;
-  for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
-    const int f = (int)(it / kBulkPieces), piece = (int)(it - (int64_t)f * kBulkPieces);
-    const uint32_t r = a.list[f];
-    const int64_t lo = Rv.lo[r], hi = Rv.hi[r];
-    const int64_t len = cdiv(hi - lo, (int64_t)kBulkPieces);
-    const int64_t c0 = min(hi, lo + piece * len), c1 = min(hi, c0 + len);
-    const uint32_t* rw = reinterpret_cast<const uint32_t*>(Rv.rows + (int64_t)r * Rv.n_iso * K);
-    for (int i = threadIdx.x; i < Rv.n_iso * KW; i += blockDim.x) srow[i / KW][i % KW] = rw[i];
-    __syncthreads();
-    const Best t = scan_columns<K>(P, Rv, r, c0, c1, srow, sbest, a.counters);
-    if (threadIdx.x == 0) a.partials[it] = to_partial(t, c1 > c0);
-    __syncthreads();
-  }
-}
-
 __device__ __forceinline__ void cas128(unsigned long long* addr, unsigned long long cmp_lo,
                                        unsigned long long cmp_hi, unsigned long long new_lo,
                                        unsigned long long new_hi, unsigned long long& old_lo,
@@ -269,18 +245,6 @@ void launch_sl_rescore(const PoolView& P, const RangeView& Rv, const SlArgs& a, 
   FIC_CHECK_LAUNCH();
 }
 
-void launch_bulk(const PoolView& P, const RangeView& Rv, const BulkArgs& a, cudaStream_t s) {
-  if (a.cap == 0) return;
-  const unsigned grid = 148 * 8;  // grid-stride over the device-side item count
-  if (Rv.K == 64)
-    k_bulk<64><<<grid, 256, 0, s>>>(P, Rv, a);
-  else if (Rv.K == 16)
-    k_bulk<16><<<grid, 256, 0, s>>>(P, Rv, a);
-  else
-    invalid("bulk pass supports range_size 4 and 8");
-  FIC_CHECK_LAUNCH();
-}
-
 // Generic K (any range size): rows zero-padded to KP = K rounded up to a
 // multiple of 4 on both sides, so whole-word dp4a products are exact.
 __global__ void __launch_bounds__(256) k_exact_generic(PoolView P, RangeView Rv, ExactArgs a) {
@@ -366,7 +330,7 @@ void launch_exact(const PoolView& P, const RangeView& Rv, const ExactArgs& a, cu
 }
 
 // K6: merge partials (per range) into the raster-order outputs.  One warp
-// per range: the lanes stride over its partial slots (and bulk pieces),
+// per range: the lanes stride over its partial slots,
 // then a lexicographic warp reduction; the survivor list's best joins in.
 __global__ void k_merge(MergeArgs a) {
   const int lane = threadIdx.x & 31;
@@ -375,9 +339,6 @@ __global__ void k_merge(MergeArgs a) {
   const int ns = a.nslots[r];
   if (ns == 0) return;
   const Partial* p = a.partials + a.slot_base[r];
-  // a range the bulk pass took over also has its kBulkPieces partials
-  const uint32_t bi = a.bulk_idx ? a.bulk_idx[r] : 0u;
-  const Partial* pb = bi ? a.bulk_part + (int64_t)(bi - 1) * kBulkPieces : nullptr;
   Best b;
   best_init(b);
   if (a.sl_best && lane == 0) {  // the survivor list's best for this range (k_sl_rescore)
@@ -391,9 +352,8 @@ __global__ void k_merge(MergeArgs a) {
     }
     b.pre = unord_bits(a.sl_pre[r]);
   }
-  const int n = ns + (pb ? kBulkPieces : 0);
-  for (int i = lane; i < n; i += 32) {
-    const Partial q = i < ns ? p[i] : pb[i - ns];
+  for (int i = lane; i < ns; i += 32) {
+    const Partial q = p[i];
     if (!q.valid) continue;
     Best c;
     c.err = q.err;

@@ -43,6 +43,9 @@
 #ifndef FIC_TC_XP
 #define FIC_TC_XP 0
 #endif
+#ifndef FIC_TC_SL
+#define FIC_TC_SL 1  // 0: compile the survivor-list append out of the screeners
+#endif
 #ifndef FIC_TC_PROF
 #define FIC_TC_PROF 0  // 1: cycle accounting (debug & 4 counters) in the production instantiation
 #endif
@@ -417,7 +420,6 @@ __global__ void __maxnreg__(MAXREG)
   // when the k-th starts, so the TMA producer can prefetch its first B tiles
   __shared__ long long s_item[2];
   __shared__ uint32_t s_rid[BM];  // CTA-local range kl -> range id (0xffffffff: none)
-  __shared__ uint32_t flag_s[BM];  // CTA-local range handed over to the bulk pass
   __shared__ int32_t s_rho[BM];
   if (CG == 1) {
     if (threadIdx.x == 0) s_item[0] = (long long)atomicAdd(a.item_ctr, 1ull);
@@ -546,7 +548,6 @@ __global__ void __maxnreg__(MAXREG)
       const int kl = (int)threadIdx.x;
       const uint32_t r = kl < BM / n_iso ? s_rid[kl] : 0xffffffffu;
       thr_s[threadIdx.x] = r != 0xffffffffu ? a.thr_g[r] : 0x7ff0000000000000ull;  // +inf
-      flag_s[threadIdx.x] = (r != 0xffffffffu && a.bulk_idx) ? (a.bulk_idx[r] != 0u) : 0u;
     }
     for (int i = threadIdx.x; i < NSLICE * BM; i += NTHREADS) {
       qtail[i] = 0;
@@ -684,9 +685,6 @@ __global__ void __maxnreg__(MAXREG)
             hit_lanes += hit ? 1 : 0;
           }
           const long long ts0 = TCLK();
-          // a range handed over to the bulk pass (by this CTA, or by another
-          // one before this item started): nothing more to screen
-          if (hit && a.bulk_idx && reinterpret_cast<volatile uint32_t*>(flag_s)[rk]) hit = false;
           const int32_t wl = max(e_lo, 0), wh = min(e_hi, CH);
           uint64_t wmask = 0;
           if (hit) wmask = ((wh >= 64) ? ~0ull : ((1ull << wh) - 1ull)) & ~((1ull << wl) - 1ull);
@@ -729,30 +727,7 @@ __global__ void __maxnreg__(MAXREG)
             for (int q = 0; q < CH; ++q) m |= (fabsf(v[q]) >= s_r || (debug & 64)) ? (1ull << q) : 0ull;
             m &= wmask;
           }
-          if (a.bulk_idx) {
-            // survivors of the range in this chunk (its n_iso rows are adjacent lanes)
-            uint32_t cnt = (uint32_t)__popcll(m);
-            for (int k = 1; k < n_iso; k <<= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, k);
-            int handover = 0;
-            if (iso == 0 && cnt) {
-              const uint32_t budget =
-                  max((uint32_t)a.bulk_min, (uint32_t)(((uint64_t)(rhi - rlo) * n_iso) >> a.bulk_shift));
-              const uint32_t old = atomicAdd(a.surv_g + rid, cnt);
-              if (old < budget && old + cnt >= budget) {
-                const uint32_t slot = atomicAdd(a.n_bulk, 1u);
-                if (slot < (uint32_t)a.bulk_cap) {
-                  a.bulk_list[slot] = rid;
-                  __threadfence();
-                  a.bulk_idx[rid] = slot + 1;
-                  flag_s[rk] = 1;
-                  handover = 1;
-                }
-              }
-            }
-            handover = __shfl_sync(0xffffffffu, handover, lane & ~(n_iso - 1));
-            if (handover) m = 0;
-          }
-          if (a.sl) {
+          if (FIC_TC_SL && a.sl) {
             // survivors the row's queue cannot take now go to the survivor
             // list as one (row, chunk, mask) entry: the screener never waits
             // for the rescoring warp on a chunk with many survivors

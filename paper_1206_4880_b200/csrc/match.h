@@ -141,12 +141,6 @@ struct TcArgs {
   const int16_t* flat_c;       // [R] pixel value of a flat range, -1 otherwise
   const uint32_t* flat_canon;  // [1] smallest flat range index (its slab is canonical)
   const DevPlan* plan;         // non-null: n_items / n_tr / n_split / tlist offset from the device
-  // Hand-over to the bulk pass (k_bulk): a range whose screen keeps more than
-  // max(bulk_min, pool * n_iso >> bulk_shift) survivors (default 2048, 6:
-  // one survivor rescored in the matcher costs ~60x a bulk evaluation) -- the point past which the
-  // CUDA-core bulk pass over its whole slab is cheaper than rescoring them
-  // one by one -- gets bulk_idx[r] = its list slot + 1 and no more survivors
-  // are pushed for it.  nullptr = off.
   // Survivor list: a hit chunk whose row queue cannot take its survivors
   // writes one 16-byte entry (range id << 3 | isometry, pool column of bit
   // 0, 64-bit survivor mask) here instead of waiting for the rescoring warp;
@@ -155,11 +149,6 @@ struct TcArgs {
   uint32_t* sl_count;          // [1] entries appended (may exceed sl_cap: the rest were queued)
   uint32_t sl_cap;
   int sl_all;                  // 1: every survivor goes to the list (the queues carry seeds only)
-  uint32_t* surv_g;            // [R] survivors pushed so far
-  uint32_t* bulk_idx;          // [R] 0 or list slot + 1
-  uint32_t* bulk_list;         // [bulk_cap] range ids
-  uint32_t* n_bulk;            // [1] ranges handed over (may exceed bulk_cap: those are not)
-  int bulk_cap, bulk_min, bulk_shift;
 };
 
 // Rescoring of the survivor list: every candidate of every entry, exactly;
@@ -176,15 +165,7 @@ struct SlArgs {
 };
 void launch_sl_rescore(const PoolView& P, const RangeView& Rv, const SlArgs& a, cudaStream_t s);
 
-constexpr int kBulkPieces = 64;  // column pieces (blocks) per bulk range
-struct BulkArgs {
-  const uint32_t* list;        // range ids
-  const uint32_t* n_bulk;      // device count (clamped to cap)
-  int cap;
-  Partial* partials;           // [cap * kBulkPieces]
-  unsigned long long* counters;  // [0] exact evaluations
-};
-void launch_bulk(const PoolView& P, const RangeView& Rv, const BulkArgs& a, cudaStream_t s);
+
 
 // Flat ranges (every pixel equal to c): all isometries give the same row and
 // the LS fit is s = 0, o = c exactly, so each candidate's error is a function
@@ -227,8 +208,6 @@ struct MergeArgs {
   double* pre_rms;
   double* post_rms;
   double n;                    // pixels per range
-  const uint32_t* bulk_idx;    // optional [R]: 0 or bulk list slot + 1
-  const Partial* bulk_part;    // [cap * kBulkPieces]
   const unsigned long long* sl_best;  // optional [R][2] (SlArgs)
   const unsigned long long* sl_pre;   // [R]
 };

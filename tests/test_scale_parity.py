@@ -159,21 +159,18 @@ def test_pool_builder_outputs_match_reference(cname, strategy, planes, monkeypat
     assert _sha(inv_den) == str(g[f"{cname}.inv_den_sha"])
 
 
-@pytest.mark.parametrize("env", [{"FIC_BULK": "1", "FIC_BULK_MIN": "1", "FIC_BULK_SHIFT": "31"},
-                                 {"FIC_SL": "1"}, {"FIC_SL": "1", "FIC_SL_ALL": "1"},
+@pytest.mark.parametrize("env", [{"FIC_SL": "1"}, {"FIC_SL": "1", "FIC_SL_ALL": "1"},
                                  {"FIC_SL": "1", "FIC_SL_CAP": "7"}])
 @pytest.mark.parametrize("prefix", ["cfg2", "cfg2_ex"])
 def test_survivor_paths_match_reference(prefix, env, monkeypatch):
     """Every way a survivor can be rescored gives the reference's records:
-    the bulk hand-over of every range with one survivor, the survivor list
-    (overflow of the rescoring warp's queues, or every survivor), and a
+    the survivor list (overflow of the rescoring warp's queues, or every
+    survivor), and a
     survivor list that overflows after 7 entries (the rest go through the
     rescoring warp)."""
     for k, v in env.items():
         monkeypatch.setenv(k, v)
     _, res = _check_full("scale_cfg2.npz", prefix)
-    if "FIC_BULK" in env:
-        assert res.stats["bulk_ranges"] > 0
     if "FIC_SL_ALL" in env:
         assert res.stats["sl_entries"] > 0
     if "FIC_SL_CAP" in env:

@@ -19,7 +19,7 @@ codec.encode_device(img, c.strategy, **kw)
 st = [codec.encode_device(img, c.strategy, **kw).stats for _ in range(int(sys.argv[2]))]
 ms = sorted(s["ms_total"] for s in st)
 s = st[-1]
-print(json.dumps({"ms": ms[len(ms) // 2], "ms_tensor": s["ms_tensor"], "ms_bulk": s["ms_bulk"],
+print(json.dumps({"ms": ms[len(ms) // 2], "ms_tensor": s["ms_tensor"], "ms_sl": s["ms_sl"],
                   "exact_evals": s["exact_evals"], "sl_entries": s["sl_entries"]}))
 '''
 for v in variants:

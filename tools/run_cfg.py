@@ -20,7 +20,7 @@ for i in range(reps):
                               stride=c.stride, isometries=True, delta=c.delta)
     torch.cuda.synchronize()
     st = res.stats
-    keys = ("ms_total", "ms_fd", "ms_pool", "ms_tensor", "ms_bulk", "ms_exact", "exact_evals",
-            "sl_entries", "bulk_ranges", "comparisons", "work_items")
+    keys = ("ms_total", "ms_fd", "ms_pool", "ms_tensor", "ms_sl", "ms_exact", "exact_evals",
+            "sl_entries", "comparisons", "work_items")
     print({k: st[k] for k in keys}, "matches/s %.3g" % (st["comparisons"] / st["ms_total"] * 1e3),
           flush=True)
