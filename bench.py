@@ -378,9 +378,24 @@ def run_ours(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    # FIC_BENCH_ONE_GPU=1: every rank on cuda:0 with gloo carrying the
+    # exchange -- a functional test of the multi-rank path on a one-GPU box
+    # (the ranks' kernels never wait on each other); its numbers are not
+    # bench values and the line says so
+    one_gpu = os.environ.get("FIC_BENCH_ONE_GPU") == "1"
+    if one_gpu:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def max_over_ranks(vals):
+        t = torch.tensor(vals, dtype=torch.float64, device="cpu" if one_gpu else "cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return [float(x) for x in t]
     img = synth.cfg3_image()
     d_img = torch.from_numpy(img).cuda()
 
@@ -420,9 +435,7 @@ def run_ours(args):
     ms = float(np.mean(times))
     ms_t = float(np.mean(tens))
     if world > 1:
-        t = torch.tensor([ms, ms_t], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms, ms_t = float(t[0]), float(t[1])
+        ms, ms_t = max_over_ranks([ms, ms_t])
     comps = int(stats[-1]["comparisons"])
     value = comps / (ms / 1e3)
     # untimed: the pool builder alone on the main stream (roofline_hbm.isolated)
@@ -430,12 +443,14 @@ def run_ours(args):
     serial_stats = [step() for _ in range(3)] if world == 1 else None
     os.environ.pop("FIC_POOL_SERIAL", None)
 
-    # the timed encode's records against the reference's own (rank 0, 1 GPU)
-    parity = None
+    # the encode's records (all-gathered when sharded) against the
+    # reference's own on every cfg3 range
     if world == 1:
         r = codec.encode_device(d_img, "dynamic_fd", **CFG)
-        parity = _parity_vs_reference(r.records.cpu().numpy(), r.pre_rms.cpu().numpy(),
-                                      r.post_rms.cpu().numpy())
+        recs, pre, post = r.records, r.pre_rms, r.post_rms
+    else:
+        recs, pre, post = encode_sharded(d_img, "dynamic_fd", **CFG)[:3]
+    parity = _parity_vs_reference(recs.cpu().numpy(), pre.cpu().numpy(), post.cpu().numpy())
     # e2e through the public API: host image in, host records/RMS out
     e2e_times = []
     for i in range(max(1, args.steps // 2) + 1):
@@ -452,9 +467,7 @@ def run_ours(args):
             e2e_times.append(time.perf_counter() - t0)
     e2e_s = float(np.mean(e2e_times))
     if world > 1:
-        t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t[0])
+        e2e_s = max_over_ranks([e2e_s])[0]
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -479,6 +492,8 @@ def run_ours(args):
                 "h2d_bytes_per_step": int(img.nbytes),
                 "d2h_bytes_per_step": n_r * (7 + 8 + 8 + 8)},
         "gpu_launches": int(stats[-1]["kernel_launches"]) * args.steps,
+        **({"harness": "FIC_BENCH_ONE_GPU: all ranks on cuda:0 with gloo -- a functional "
+                       "test of the multi-rank path, not a bench value"} if one_gpu else {}),
         "parity": parity,
         "clocks": clk.summary(),
         "device_stats": {k: stats[-1][k] for k in ("ms_fd", "ms_pool", "ms_match", "ms_tensor",

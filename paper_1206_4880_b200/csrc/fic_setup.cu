@@ -1095,13 +1095,22 @@ __device__ __forceinline__ void pool_warp(const PoolArgs& a, int64_t p0, int lan
   uint16_t* bq = a.bh ? a.bh + (size_t)(p0 + g) * K + i * RS : nullptr;
   uint32_t my_sd = 0, my_sdd = 0;
   const float2 kk = make_float2((float)K, (float)K);
+  // all of this lane's row loads first (memory-level parallelism: the rows
+  // of 32 random domains), then the arithmetic
+  unsigned long long rr[RS];
+#pragma unroll
+  for (int k = 0; k < RS; ++k) {
+    const int dk = k * DPI + g;
+    const bool ok = FULL || (uint32_t)p0 + dk < D;
+    const uint32_t off = __shfl_sync(0xffffffffu, my_off, dk);
+    rr[k] = 0ull;
+    if (ok) rr[k] = TROWS ? __ldg(trow + off) : bytes8_at(prow + off);
+  }
 #pragma unroll
   for (int k = 0; k < RS; ++k) {
     const int dk = k * DPI + g;                 // domain of this lane in step k
     const bool ok = FULL || (uint32_t)p0 + dk < D;
-    const uint32_t off = __shfl_sync(0xffffffffu, my_off, dk);
-    unsigned long long r = 0ull;
-    if (ok) r = TROWS ? __ldg(trow + off) : bytes8_at(prow + off);
+    const unsigned long long r = rr[k];
     const uint32_t w0 = (uint32_t)r, w1 = RS == 8 ? (uint32_t)(r >> 32) : 0u;
     // row sums with byte dot products: sum x and sum x^2
     uint32_t sd = __dp4a(w0, 0x01010101u, 0u), sdd = __dp4a(w0, w0, 0u);
@@ -1159,7 +1168,7 @@ __device__ __forceinline__ void pool_warp(const PoolArgs& a, int64_t p0, int lan
 }
 
 template <int RS, bool TROWS>
-__global__ void __launch_bounds__(256, 8) k_pool(PoolArgs a) {
+__global__ void __launch_bounds__(256, TROWS ? 6 : 4) k_pool(PoolArgs a) {
   const int lane = threadIdx.x & 31;
   const int64_t p0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32;
   if (p0 >= a.D) return;

@@ -4,9 +4,9 @@ set -e
 cd /root/repo
 # the other objects come from the last in-tree build (run `make` first);
 # the variant's fic_tc.cu is compiled on its own so the in-tree library is untouched
-mkdir -p build/var
+mkdir -p build/var vlib
 nvcc -O3 -std=c++17 -lineinfo -gencode arch=compute_100a,code=sm_100a -Xcompiler -fPIC --expt-relaxed-constexpr $2 \
   -c paper_1206_4880_b200/csrc/fic_tc.cu -o build/var/fic_tc_$1.o
 objs=$(ls build/*.o | grep -v fic_tc.o)
-nvcc -gencode arch=compute_100a,code=sm_100a -shared -o build/var/$1.so $objs build/var/fic_tc_$1.o -cudart static
-echo built build/var/$1.so
+nvcc -gencode arch=compute_100a,code=sm_100a -shared -o vlib/$1.so $objs build/var/fic_tc_$1.o -cudart static
+echo built vlib/$1.so
