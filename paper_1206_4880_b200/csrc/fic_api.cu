@@ -1152,18 +1152,18 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
   ra.info = sc.get<RangeInfo>(g.R);
   ra.KP = (int)align_up((size_t)K, 4);
   ra.rows = sc.get<uint8_t>((size_t)g.R * g.n_iso * ra.KP);
+  // FIC_POOL_SERIAL: the side-stream work (range preparation, pool builder)
+  // on the caller's stream -- a measurement of K1 with nothing beside it
+  const bool pool_serial = getenv("FIC_POOL_SERIAL") != nullptr;
   FIC_CUDA(cudaEventRecord(side.ev[0], s));
   FIC_CUDA(cudaStreamWaitEvent(side.s2, side.ev[0], 0));
-  launch_ranges(ra, side.s2);
+  launch_ranges(ra, pool_serial ? s : side.s2);
 
   PlanBufs pb = make_plan(sc, s, img, g, p, false, false, d_rb->scal);
   tm.mark();  // 1
 
   // K1 pool builder (side stream: needs the FD order, overlaps the planning)
   PoolArgs pa = pool_args(sc, g, img, pb.order, tensor_ok);
-  // FIC_POOL_SERIAL: the pool builder on the caller's stream (a measurement
-  // of K1 without the planning kernels running beside it)
-  const bool pool_serial = getenv("FIC_POOL_SERIAL") != nullptr;
   cudaStream_t ps = pool_serial ? s : side.s2;
   pa.ev_main = side.ev[5];
   FIC_CUDA(cudaEventRecord(side.ev[1], s));

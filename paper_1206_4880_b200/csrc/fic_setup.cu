@@ -1167,8 +1167,14 @@ __device__ __forceinline__ void pool_warp(const PoolArgs& a, int64_t p0, int lan
   }
 }
 
+#ifndef FIC_POOL_BLK_T
+#define FIC_POOL_BLK_T 6  // resident blocks per SM the register budget allows (row segments)
+#endif
+#ifndef FIC_POOL_BLK_P
+#define FIC_POOL_BLK_P 6  // (box planes)
+#endif
 template <int RS, bool TROWS>
-__global__ void __launch_bounds__(256, TROWS ? 6 : 4) k_pool(PoolArgs a) {
+__global__ void __launch_bounds__(256, TROWS ? FIC_POOL_BLK_T : FIC_POOL_BLK_P) k_pool(PoolArgs a) {
   const int lane = threadIdx.x & 31;
   const int64_t p0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32;
   if (p0 >= a.D) return;
@@ -1267,57 +1273,63 @@ __global__ void k_ranges(RangeArgs a) {
   }
 }
 
-// RS = 8 fast path: one thread per (range, isometry); rows are aligned 8-byte
-// loads, the permutation table lives in shared memory.
+// RS = 8 fast path: a block takes 32 ranges; their 8x8 pixels are staged
+// in shared memory (one aligned 8-byte row load per thread), then one thread
+// per (range, isometry) gathers its permuted row from there (no per-thread
+// local-memory copy of the block).
 __global__ void __launch_bounds__(256) k_ranges8(RangeArgs a) {
   __shared__ uint8_t perm[8 * 64];
+  __shared__ __align__(16) uint8_t blk[32][64];
   for (int i = threadIdx.x; i < a.n_iso * 64; i += blockDim.x) perm[i] = (uint8_t)a.inv_perm[i];
+  const int r0 = blockIdx.x * 32;
+  {  // thread t loads row t & 7 of range r0 + (t >> 3)
+    const int rl = threadIdx.x >> 3, row = threadIdx.x & 7, r = r0 + rl;
+    unsigned long long v = 0ull;
+    if (r < a.R) {
+      const int ry = r / a.nrx, rx = r - ry * a.nrx;
+      v = __ldg(reinterpret_cast<const unsigned long long*>(a.img + ((int64_t)ry * 8 + row) * a.W +
+                                                            (int64_t)rx * 8));
+    }
+    reinterpret_cast<unsigned long long*>(blk[rl])[row] = v;
+  }
   __syncthreads();
-  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= (int64_t)a.R * a.n_iso) return;
-  const int r = (int)(t / a.n_iso), iso = (int)(t - (int64_t)r * a.n_iso);
-  const int ry = r / a.nrx, rx = r - ry * a.nrx;
-  const uint8_t* base = a.img + (int64_t)ry * 8 * a.W + (int64_t)rx * 8;
-  uint8_t px[64];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    unsigned long long v = __ldg(reinterpret_cast<const unsigned long long*>(base + (int64_t)i * a.W));
-#pragma unroll
-    for (int j = 0; j < 8; ++j) px[8 * i + j] = (uint8_t)(v >> (8 * j));
-  }
-  if (iso == 0) {
-    int64_t sr = 0, srr = 0;
-#pragma unroll
-    for (int k = 0; k < 64; ++k) {
-      sr += px[k];
-      srr += px[k] * px[k];
+  for (int t = threadIdx.x; t < 32 * a.n_iso; t += blockDim.x) {
+    const int rl = t / a.n_iso, iso = t - rl * a.n_iso, r = r0 + rl;
+    if (r >= a.R) continue;
+    const uint8_t* px = blk[rl];
+    if (iso == 0) {
+      int64_t sr = 0, srr = 0;
+      for (int k = 0; k < 64; ++k) {
+        sr += px[k];
+        srr += px[k] * px[k];
+      }
+      RangeInfo inf;
+      inf.sr = (double)sr;
+      inf.srr = (double)srr;
+      inf.V = __dsub_rn((double)srr, __ddiv_rn((double)sr * (double)sr, 64.0));
+      inf.rho = (int32_t)((2 * sr + 64) / 128);
+      inf.pad = 0;
+      a.info[r] = inf;
     }
-    RangeInfo inf;
-    inf.sr = (double)sr;
-    inf.srr = (double)srr;
-    inf.V = __dsub_rn((double)srr, __ddiv_rn((double)sr * (double)sr, 64.0));
-    inf.rho = (int32_t)((2 * sr + 64) / 128);
-    inf.pad = 0;
-    a.info[r] = inf;
-  }
-  uint4* out = reinterpret_cast<uint4*>(a.rows + ((int64_t)r * a.n_iso + iso) * 64);
-  const uint8_t* pm = perm + iso * 64;
+    uint4* out = reinterpret_cast<uint4*>(a.rows + ((int64_t)r * a.n_iso + iso) * 64);
+    const uint8_t* pm = perm + iso * 64;
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    uint32_t w[4];
+    for (int q = 0; q < 4; ++q) {
+      uint32_t w[4];
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const int k = 16 * q + 4 * e;
-      w[e] = px[pm[k]] | (px[pm[k + 1]] << 8) | (px[pm[k + 2]] << 16) | ((uint32_t)px[pm[k + 3]] << 24);
+      for (int e = 0; e < 4; ++e) {
+        const int k = 16 * q + 4 * e;
+        w[e] = px[pm[k]] | (px[pm[k + 1]] << 8) | (px[pm[k + 2]] << 16) | ((uint32_t)px[pm[k + 3]] << 24);
+      }
+      out[q] = make_uint4(w[0], w[1], w[2], w[3]);
     }
-    out[q] = make_uint4(w[0], w[1], w[2], w[3]);
   }
 }
 
 void launch_ranges(const RangeArgs& a, cudaStream_t s) {
   if (a.R == 0) return;
   if (a.rs == 8 && a.W % 8 == 0) {
-    k_ranges8<<<(unsigned)cdiv((int64_t)a.R * a.n_iso, 256), 256, 0, s>>>(a);
+    k_ranges8<<<(unsigned)cdiv(a.R, 32), 256, 0, s>>>(a);
   } else {
     k_ranges<<<(unsigned)cdiv(a.R, 128), 128, 0, s>>>(a);
   }

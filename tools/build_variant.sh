@@ -3,10 +3,13 @@
 set -e
 cd /root/repo
 # the other objects come from the last in-tree build (run `make` first);
-# the variant's fic_tc.cu is compiled on its own so the in-tree library is untouched
+# the variant's source (default fic_tc.cu; SRC=fic_setup.cu ...) is compiled on
+# its own so the in-tree library is untouched
+SRC=${SRC:-fic_tc.cu}
+B=${SRC%.cu}
 mkdir -p build/var vlib
 nvcc -O3 -std=c++17 -lineinfo -gencode arch=compute_100a,code=sm_100a -Xcompiler -fPIC --expt-relaxed-constexpr $2 \
-  -c paper_1206_4880_b200/csrc/fic_tc.cu -o build/var/fic_tc_$1.o
-objs=$(ls build/*.o | grep -v fic_tc.o)
-nvcc -gencode arch=compute_100a,code=sm_100a -shared -o vlib/$1.so $objs build/var/fic_tc_$1.o -cudart static
+  -c paper_1206_4880_b200/csrc/$SRC -o build/var/${B}_$1.o
+objs=$(ls build/*.o | grep -v "/$B.o")
+nvcc -gencode arch=compute_100a,code=sm_100a -shared -o vlib/$1.so $objs build/var/${B}_$1.o -cudart static
 echo built vlib/$1.so
