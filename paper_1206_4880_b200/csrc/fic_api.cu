@@ -1312,9 +1312,23 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
   RangeView Rv{ra.info, ra.rows, pb.lo, pb.hi, g.n_iso, K, ra.KP};
   tm.mark();  // 3
   SlArgs sla{};                    // survivor list (k_sl_rescore)
+  // FIC_PRIME_THR (experiment only): the tensor matcher's per-range
+  // thresholds start from the final errors of the previous call with the
+  // same R on this device -- how much of K4 is threshold discovery
+  static std::map<std::pair<int, int>, unsigned long long*> prime_cache;
+  unsigned long long* prime_buf = nullptr;
+  bool prime_ok = false;
+  if (getenv("FIC_PRIME_THR")) {
+    auto& pb2 = prime_cache[{dev_id, g.R}];
+    prime_ok = pb2 != nullptr;
+    if (!pb2) FIC_CUDA(cudaMalloc(&pb2, g.R * 8));
+    prime_buf = pb2;
+  }
   if (n_tt_max && titems_n) {
     unsigned long long* thr_g = sc.get<unsigned long long>(g.R);
     k_fill_u64<<<(unsigned)cdiv(g.R, 256), 256, 0, s>>>(thr_g, 0x7ff0000000000000ull, g.R);
+    if (prime_buf && prime_ok)  // experiment: start from the previous call's final errors
+      FIC_CUDA(cudaMemcpyAsync(thr_g, prime_buf, g.R * 8, cudaMemcpyDeviceToDevice, s));
     FIC_CHECK_LAUNCH();
     TcArgs ta{titems, titems_n, rid_s, n_tt_max * RT, wlo, whi, seg_t, seg0, RT, sbase, partials,
               counters, counters + 15, thr_g, 0, nullptr};
@@ -1394,7 +1408,7 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
   }
   tm.mark();  // 5
   MergeArgs ma{g.R, sbase, nslots, partials, records, pre_rms, post_rms, (double)K, sla.best,
-               sla.pre};
+               sla.pre, prime_buf};
   launch_merge(ma, s);
   tm.mark();  // 6
 

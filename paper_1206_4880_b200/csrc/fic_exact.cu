@@ -367,6 +367,7 @@ __global__ void k_merge(MergeArgs a) {
 #pragma unroll
   for (int m = 16; m >= 1; m >>= 1) best_merge(b, shfl_best(b, m));
   if (lane != 0) return;
+  if (a.err_out) a.err_out[r] = (unsigned long long)__double_as_longlong(fmax(b.err, 0.0));
   uint8_t* rec = a.records + r * 7;
   rec[0] = b.dom & 255;
   rec[1] = (b.dom >> 8) & 255;

@@ -46,6 +46,9 @@
 #ifndef FIC_TC_SL
 #define FIC_TC_SL 1  // 0: compile the survivor-list append out of the screeners
 #endif
+#ifndef FIC_TC_BAL
+#define FIC_TC_BAL 0  // 1: balanced drain of the survivor queues (measured slower: DESIGN.md)
+#endif
 #ifndef FIC_TC_PROF
 #define FIC_TC_PROF 0  // 1: cycle accounting (debug & 4 counters) in the production instantiation
 #endif
@@ -56,10 +59,19 @@ namespace fic {
 namespace tc {
 
 constexpr int BM = 128;       // rows per tile (TMEM lanes)
-constexpr int BN = 128;       // columns per N-tile (one TMEM accumulator stage)
-constexpr int NACC = 4;       // TMEM accumulator stages (NACC * BN = 512 columns)
-constexpr int NGRP = 2;       // screening groups; group g handles stages j with j % NGRP == g
-constexpr int NSPLIT = 1;     // column slices per lane quarter within a group
+#ifndef FIC_TC_BN
+#define FIC_TC_BN 128
+#endif
+constexpr int BN = FIC_TC_BN;  // columns per N-tile (one TMEM accumulator stage)
+constexpr int NACC = 512 / BN;  // TMEM accumulator stages (NACC * BN = 512 columns)
+#ifndef FIC_TC_NGRP
+#define FIC_TC_NGRP 2
+#endif
+#ifndef FIC_TC_NSPLIT
+#define FIC_TC_NSPLIT 1
+#endif
+constexpr int NGRP = FIC_TC_NGRP;      // screening groups; group g handles stages j with j % NGRP == g
+constexpr int NSPLIT = FIC_TC_NSPLIT;  // column slices per lane quarter within a group
 constexpr int NEPI = 4 * NGRP * NSPLIT;  // screening warps: groups x slices x 4 lane quarters
 constexpr int NMMA = 2;       // MMA issuing warps; warp MMA0 + w issues tiles j % NMMA == w
 constexpr int NRES = 1;       // rescoring warps: thread t owns rows t + RSTRIDE * h
@@ -267,14 +279,14 @@ struct Cfg {
   static constexpr int ROWB = K * 2;                  // bytes per fp16 row
   static constexpr uint32_t LAYOUT = (K == 64) ? 2u : 6u;  // SW128 / SW32
   static constexpr uint32_t SBO = 8 * ROWB;           // bytes per 8-row core group
-  static constexpr int NST = (K == 64) ? 8 : 12;  // B smem stages
+  static constexpr int NST = ((K == 64) ? 8 : 12) * 128 / BN;  // B smem stages
   static constexpr int A_BYTES = BM * ROWB;
   static constexpr int B_BYTES = (BN / CG) * ROWB;       // this CTA's share of a B stage
   static constexpr int TX_BYTES = BN * ROWB;              // both shares (leader's barrier)
   static constexpr int BAR_BYTES = (2 * NST + 2 * NACC + 2) * 8;
   static constexpr int ROWS_BYTES = BM * K;               // u8 permuted range rows
   static constexpr int Q_BYTES = BM * NSLICE * QCAP * 4 + BM * NSLICE * 4 * 2 + 16;  // queues + tails/heads
-  static constexpr int RS_BYTES = BM * 40;                // rescorer row state
+  static constexpr int RS_BYTES = BM * 40 + 4096;         // rescorer row state + drain staging
   static constexpr int SMEM = 1024 /*align slack*/ + A_BYTES + NST * B_BYTES + BAR_BYTES + BM * 8 + ROWS_BYTES + Q_BYTES + RS_BYTES;
   static constexpr int KW = K / 4;                    // u32 words of a u8 row
 };
@@ -324,6 +336,17 @@ __global__ void __maxnreg__(MAXREG)
   struct RowState { double err, pre, sr, srr; uint32_t dom; uint8_t sq, oq, iso, valid; };
   RowState* rstate = reinterpret_cast<RowState*>(
       reinterpret_cast<uint8_t*>(const_cast<uint32_t*>(edone)) + 16);  // [BM]
+  // balanced drain staging (rescoring warp): per lane its inclusive pending
+  // count, per (lane, owned queue) pending count and head, per lane one
+  // evaluated candidate
+  uint32_t* s_incl = reinterpret_cast<uint32_t*>(rstate + BM);     // [32]
+  uint32_t* s_pend = s_incl + 32;                                   // [32][RROWS * NSLICE]
+  uint32_t* s_hd = s_pend + 32 * RROWS * NSLICE;                    // [32][RROWS * NSLICE]
+  uint32_t* s_crow = s_hd + 32 * RROWS * NSLICE;                    // [32]
+  uint32_t* s_cdom = s_crow + 32;                                   // [32]
+  uint32_t* s_csqoq = s_cdom + 32;                                  // [32]
+  double* s_cerr = reinterpret_cast<double*>(s_csqoq + 32);         // [32]
+  double* s_cpre = s_cerr + 32;                                     // [32]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   auto full_bar = [&](int s) { return smem_u32(bars + s); };
@@ -471,6 +494,11 @@ __global__ void __maxnreg__(MAXREG)
     int64_t c0 = 0, c1 = 0;
     item_cols(it, tile, slot, c0, c1);
     const int nt = (int)cdiv(c1 - c0, BN);
+    // survivors of this item: the rescoring warp's queues first (overflow to
+    // the survivor list), or all to the list -- for every item (sl_all 1) or
+    // after each tile's first segment, the pilot that sets the thresholds (2)
+    const bool pilot = a.sl_all == 2 && slot < a.nsub;  // no list: every survivor is rescored here
+    const bool list_all = FIC_TC_SL && (a.sl_all == 1 || (a.sl_all == 2 && !pilot));
 
     // item setup, two dependent rounds of global loads: (1) the tile's
     // range ids and rho (CTA-local range kl = row / n_iso), (2) everything
@@ -727,12 +755,12 @@ __global__ void __maxnreg__(MAXREG)
             for (int q = 0; q < CH; ++q) m |= (fabsf(v[q]) >= s_r || (debug & 64)) ? (1ull << q) : 0ull;
             m &= wmask;
           }
-          if (FIC_TC_SL && a.sl) {
+          if (FIC_TC_SL && a.sl && !pilot) {
             // survivors the row's queue cannot take now go to the survivor
             // list as one (row, chunk, mask) entry: the screener never waits
             // for the rescoring warp on a chunk with many survivors
             const uint32_t n = (uint32_t)__popcll(m);
-            const bool to_list = a.sl_all ? n > 0 : n > (uint32_t)QCAP - (qt - *myhead);
+            const bool to_list = list_all ? n > 0 : n > (uint32_t)QCAP - (qt - *myhead);
             const unsigned lm = __ballot_sync(0xffffffffu, to_list);
             if (lm) {
               const int leader = __ffs(lm) - 1;
@@ -874,7 +902,131 @@ __global__ void __maxnreg__(MAXREG)
           atomicMin(a.thr_g + s_rid[k], eb);
         }
       };
-      constexpr int NE = 4;  // candidates per pass
+      constexpr int NE = 4;  // candidates per lane and pass
+#if FIC_TC_BAL
+      // Balanced drain: the warp is the single consumer of all 2 x 128
+      // queues; each pass takes up to 32 x NE pending entries from any rows
+      // (lane-major prefix sum over the lanes' queues), so every lane
+      // evaluates even when the survivors sit in a few rows.  Heads advance
+      // only after every lane has read its entries (each head keeps one
+      // writer: its owner lane); results of the same row are merged by the
+      // row's lowest lane in that pass (one writer per row state).
+      constexpr int Q = RROWS * NSLICE;
+      static_assert(NRES == 1, "the balanced drain is one warp");
+      while (true) {
+        uint32_t pend[Q], mine = 0;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+          const int r = t + RSTRIDE * (q / NSLICE), qs = q % NSLICE;
+          pend[q] = qtail[r * NSLICE + qs] - hd[q];
+          mine += pend[q];
+        }
+        uint32_t incl = mine;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          const uint32_t v = __shfl_up_sync(0xffffffffu, incl, d);
+          if (t >= d) incl += v;
+        }
+        const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+        if (total == 0) {
+          if (*edone == (uint32_t)NEPI) {
+            __threadfence_block();
+            bool empty = true;
+#pragma unroll
+            for (int q = 0; q < Q; ++q)
+              empty = empty && (hd[q] == qtail[(t + RSTRIDE * (q / NSLICE)) * NSLICE + q % NSLICE]);
+            if (__all_sync(0xffffffffu, empty)) break;
+          } else {
+            __nanosleep(256);
+          }
+          continue;
+        }
+        __threadfence_block();  // the entries behind the tails we read
+        s_incl[t] = incl;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+          s_pend[t * Q + q] = pend[q];
+          s_hd[t * Q + q] = hd[q];
+        }
+        __syncwarp();
+        const uint32_t take = min(total, (uint32_t)(32 * NE));
+        Cand cd[NE];
+        uint32_t did[NE];
+        int rr[NE];
+#pragma unroll
+        for (int e = 0; e < NE; ++e) {
+          const uint32_t tt = min((uint32_t)t + 32u * e, take - 1);  // (duplicates are not applied)
+          int o = 0;  // owner lane: the first whose inclusive count exceeds tt
+#pragma unroll
+          for (int step = 16; step >= 1; step >>= 1)
+            if (s_incl[o + step - 1] <= tt) o += step;
+          uint32_t k = tt - (o ? s_incl[o - 1] : 0u);
+          int q = 0;
+          while (k >= s_pend[o * Q + q]) {
+            k -= s_pend[o * Q + q];
+            ++q;
+          }
+          const int r = o + RSTRIDE * (q / NSLICE), qs = q % NSLICE;
+          const uint32_t rel = qbuf[(r * NSLICE + qs) * QCAP + ((s_hd[o * Q + q] + k) & (QCAP - 1))];
+          const int64_t p = c0 + rel;
+          rr[e] = r;
+          did[e] = pool_id(P, p);
+          cd[e] = exact(p, did[e], r, rstate[r].sr, rstate[r].srr);
+        }
+        __syncwarp();  // every entry of this pass has been read
+        {
+          const uint32_t excl = incl - mine;
+          uint32_t cons = take > excl ? min(mine, take - excl) : 0u;
+#pragma unroll
+          for (int q = 0; q < Q; ++q) {
+            const uint32_t c = min(pend[q], cons);
+            cons -= c;
+            if (c) {
+              hd[q] += c;
+              qhead[(t + RSTRIDE * (q / NSLICE)) * NSLICE + q % NSLICE] = hd[q];
+            }
+          }
+        }
+#pragma unroll
+        for (int e = 0; e < NE; ++e) {
+          const bool ok = (uint32_t)t + 32u * e < take;
+          s_crow[t] = ok ? (uint32_t)rr[e] : 0xffffffffu;
+          s_cerr[t] = cd[e].err;
+          s_cpre[t] = cd[e].pre;
+          s_cdom[t] = did[e];
+          s_csqoq[t] = (uint32_t)cd[e].sq | ((uint32_t)cd[e].oq << 8);
+          __syncwarp();
+          const unsigned grp = __match_any_sync(0xffffffffu, s_crow[t]);
+          if (ok && t == __ffs(grp) - 1) {  // the row's lowest lane merges its pass results
+            const int r = rr[e];
+            RowState st = rstate[r];
+            unsigned g2 = grp;
+            while (g2) {
+              const int j = __ffs(g2) - 1;
+              g2 &= g2 - 1;
+              const double ej = s_cerr[j];
+              const uint32_t dj = s_cdom[j];
+              st.pre = fmin(st.pre, s_cpre[j]);
+              if (better(ej, dj, st.iso, st.err, st.dom, st.iso)) {
+                st.err = ej;
+                st.dom = dj;
+                st.sq = (uint8_t)(s_csqoq[j] & 255u);
+                st.oq = (uint8_t)(s_csqoq[j] >> 8);
+              }
+            }
+            rstate[r] = st;
+            const int k = r / n_iso;
+            const unsigned long long eb = (unsigned long long)__double_as_longlong(fmax(st.err, 0.0));
+            if (eb < thr_s[k]) {  // an improvement: publish to the screeners and the other segments
+              atomicMin(thr_s + k, eb);
+              atomicMin(a.thr_g + s_rid[k], eb);
+            }
+          }
+          __syncwarp();
+        }
+        evals += (uint32_t)t < take ? min((take - 1 - (uint32_t)t) / 32u + 1u, (uint32_t)NE) : 0u;
+      }
+#else
       while (true) {
         int got[NE];
         uint32_t rel[NE];
@@ -925,6 +1077,7 @@ __global__ void __maxnreg__(MAXREG)
           __nanosleep(256);
         }
       }
+#endif
       __syncwarp();
       // combine the n_iso rows of each range: lexicographic (err, dom, iso)
 #pragma unroll

@@ -148,7 +148,8 @@ struct TcArgs {
   uint4* sl;
   uint32_t* sl_count;          // [1] entries appended (may exceed sl_cap: the rest were queued)
   uint32_t sl_cap;
-  int sl_all;                  // 1: every survivor goes to the list (the queues carry seeds only)
+  int sl_all;                  // 1: every survivor goes to the list (the queues carry seeds only);
+                               // 2: the same after each tile's first segment (a pilot with the queues)
 };
 
 // Rescoring of the survivor list: every candidate of every entry, exactly;
@@ -210,6 +211,7 @@ struct MergeArgs {
   double n;                    // pixels per range
   const unsigned long long* sl_best;  // optional [R][2] (SlArgs)
   const unsigned long long* sl_pre;   // [R]
+  unsigned long long* err_out;  // optional [R]: each range's best error bits (FIC_PRIME_THR experiment)
 };
 void launch_merge(const MergeArgs& a, cudaStream_t s);
 
