@@ -1330,9 +1330,11 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
     if (prime_buf && prime_ok)  // experiment: start from the previous call's final errors
       FIC_CUDA(cudaMemcpyAsync(thr_g, prime_buf, g.R * 8, cudaMemcpyDeviceToDevice, s));
     FIC_CHECK_LAUNCH();
+    constexpr int BN_COLS = 128;
     TcArgs ta{titems, titems_n, rid_s, n_tt_max * RT, wlo, whi, seg_t, seg0, RT, sbase, partials,
               counters, counters + 15, thr_g, 0, nullptr};
     ta.nsub = nsub;
+    ta.pilot_cols = getenv("FIC_PILOT") ? std::max(0, atoi(getenv("FIC_PILOT"))) / BN_COLS * BN_COLS : 0;
     ta.n_split = nsub > 1 ? std::min<int64_t>(titems_n, kSplitCap) : 0;  // bound
     ta.plan = d_plan;
     if (flat_path) {

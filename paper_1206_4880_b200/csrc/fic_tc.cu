@@ -86,6 +86,8 @@ constexpr bool WIDE = FIC_TC_WIDE;  // load a whole stage before screening (need
 static_assert(NACC % NGRP == 0, "screening groups must own whole accumulator stages");
 static_assert((BN / NSPLIT) % CH == 0 && CH % 32 == 0, "slices hold whole chunks of x32 loads");
 constexpr int QCAP = 32;      // survivor queue entries per (row, slice)
+constexpr int PK = 8;         // pilot: |u| candidates kept per row and screening group
+static_assert(2 * NGRP * PK <= NSLICE * QCAP, "pilot lists live in the survivor-queue buffer");
 constexpr int MMA0 = 1;       // first MMA issuing warp (warp 0: TMA producer)
 constexpr int RES0 = MMA0 + NMMA;  // first rescoring warp
 constexpr int RSTRIDE = 32 * NRES;
@@ -302,6 +304,29 @@ __device__ __forceinline__ uint32_t swz(int r, int c) {
 
 using namespace tc;
 
+// Pilot list insertion: replace the smallest of the row's PK entries (stride
+// BM in shared memory) by (x, pos); returns the new smallest |u|, or -1
+// while the list still has free (negative) entries.  Out of line: the
+// screener's chunk values stay in registers at the call sites.
+__device__ __noinline__ float pilot_insert(float* lv, uint32_t* lp, float x, uint32_t pos) {
+  int km = 0;
+  float vm = lv[0];
+#pragma unroll
+  for (int k = 1; k < PK; ++k) {
+    const float y = lv[k * BM];
+    if (y < vm) {
+      vm = y;
+      km = k;
+    }
+  }
+  lv[km * BM] = x;
+  lp[km * BM] = pos;
+  float nk = lv[0];
+#pragma unroll
+  for (int k = 1; k < PK; ++k) nk = fminf(nk, lv[k * BM]);
+  return nk;
+}
+
 template <int K, int CG, bool DBG>
 __global__ void __maxnreg__(MAXREG)
     k_match_tc(const __grid_constant__ CUtensorMap tmB, PoolView P, RangeView Rv, TcArgs a) {
@@ -462,8 +487,18 @@ __global__ void __maxnreg__(MAXREG)
     tlist = a.tlist + a.plan->tb;
   }
   const int64_t n_whole = n_items - n_split;
-  const int64_t n_virt = n_whole + n_split * a.nsub;
+  // pilot items (TcArgs::pilot_cols): one per tile, before everything else
+  const int64_t n_pilot = a.pilot_cols > 0 ? (a.plan ? a.plan->n_tt : cdiv(n_tr, a.RT)) : 0;
+  const int64_t n_virt = n_pilot + n_whole + n_split * a.nsub;
   auto item_cols = [&](int64_t v, int& tile, int& slot, int64_t& c0, int64_t& c1) {
+    if (v < n_pilot) {  // pilot: the first pilot_cols columns of tile v's window, no partial slot
+      tile = (int)v;
+      slot = -1;
+      c0 = a.wlo[tile];
+      c1 = max(c0, min((int64_t)a.whi[tile], c0 + a.pilot_cols));
+      return;
+    }
+    v -= n_pilot;
     int64_t i = v;
     int sub = 0;
     if (v >= n_whole) {
@@ -497,6 +532,7 @@ __global__ void __maxnreg__(MAXREG)
     // survivors of this item: the rescoring warp's queues first (overflow to
     // the survivor list), or all to the list -- for every item (sl_all 1) or
     // after each tile's first segment, the pilot that sets the thresholds (2)
+    const bool pil = slot < 0;                         // a pilot item (top-PK |u| per row, no partials)
     const bool pilot = a.sl_all == 2 && slot < a.nsub;  // no list: every survivor is rescored here
     const bool list_all = FIC_TC_SL && (a.sl_all == 1 || (a.sl_all == 2 && !pilot));
 
@@ -660,6 +696,76 @@ __global__ void __maxnreg__(MAXREG)
         acc += NMMA;
         if (acc >= NACC) { acc -= NACC; acc_ph ^= 1; }
       }
+    } else if (is_scr && pil) {
+      // ------------------------------ pilot ---------------------------------
+      // Top-PK |u| per row over the pilot columns (no survivors, no seeds):
+      // their exact errors, min over the range's rows, are the range's
+      // starting threshold for the main items (thr_g).  The lists live in
+      // the (unused) survivor-queue buffer, one per (group, row).
+      float* lv = reinterpret_cast<float*>(qbuf);      // [NGRP][PK][BM]
+      uint32_t* lp = qbuf + NGRP * PK * BM;               // [NGRP][PK][BM]
+#pragma unroll
+      for (int k = 0; k < PK; ++k) lv[(group * PK + k) * BM + row] = -1.0f;
+      float kth = -1.0f;  // smallest |u| in the list (-1 while it has free entries)
+      const uint32_t lane_base = tmem_base + ((uint32_t)(32 * (warp & 3)) << 16);
+      const uint32_t tfull0 = tfull_bar(0), tempty0 = tempty_bar(0);
+      const int32_t lo32 = rvalid ? (int32_t)(max((int64_t)rlo, c0) - c0) : 0;
+      const int32_t hi32 = rvalid ? max(lo32, (int32_t)(min((int64_t)rhi, c1) - c0)) : 0;
+      for (int j = (int)((group - (int)(gt % NGRP) + NGRP) % NGRP); j < nt; j += NGRP) {
+        const uint32_t gj = gt + (uint32_t)j;
+        const int acc = (int)(gj % NACC), acc_ph = (int)((gj / NACC) & 1);
+        mbar_wait_sleep(tfull0 + 8 * acc, acc_ph);
+        fence_after();
+#pragma unroll
+        for (int h = 0; h < SW / CH; ++h) {
+          float v[CH];
+#pragma unroll
+          for (int c = 0; c < CH / 32; ++c)
+            tmem_ld32(lane_base + acc * BN + slice * SW + CH * h + 32 * c, v + 32 * c);
+          tmem_wait_ld();
+          if (h == SW / CH - 1) {
+            fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(tempty0 + 8 * acc);
+          }
+          const int32_t rel = j * BN + slice * SW + CH * h;
+          const int32_t e_lo = lo32 - rel, e_hi = hi32 - rel;
+          float mx = -1.0f;
+#pragma unroll
+          for (int q = 0; q < CH; ++q) mx = fmaxf(mx, fabsf(v[q]));
+          const bool in_window = (uint32_t)(e_hi - 1) < (uint32_t)(hi32 - lo32 + CH - 1);
+          if (in_window && !rflat && mx > kth) {
+            const int32_t wl = max(e_lo, 0), wh = min(e_hi, CH);
+#pragma unroll
+            for (int q = 0; q < CH; ++q) {
+              const float x = fabsf(v[q]);
+              if (x > kth && q >= wl && q < wh)
+                kth = pilot_insert(lv + group * PK * BM + row, lp + group * PK * BM + row, x,
+                                   (uint32_t)(rel + q));
+            }
+          }
+        }
+      }
+      // exact errors of the list; the range's minimum becomes its threshold
+      double tnew = INFINITY;
+      if (rvalid && !rflat) {
+        for (int k = 0; k < PK; ++k) {
+          if (lv[(group * PK + k) * BM + row] >= 0.0f) {
+            const int64_t pe = c0 + lp[(group * PK + k) * BM + row];
+            tnew = fmin(tnew, fmax(exact(pe, pool_id(P, pe), row, sr, srr).err, 0.0));
+            ++evals;
+          }
+        }
+      }
+      for (int m = 1; m < n_iso; m <<= 1) tnew = fmin(tnew, __shfl_xor_sync(0xffffffffu, tnew, m));
+      if (iso == 0 && rvalid && tnew < INFINITY) {
+        const unsigned long long tb = (unsigned long long)__double_as_longlong(tnew);
+        atomicMin(thr_s + rk, tb);
+        atomicMin(a.thr_g + rid, tb);
+      }
+      __threadfence_block();
+      __syncwarp();
+      if (lane == 0) atomicAdd((uint32_t*)edone, 1u);
     } else if (is_scr) {
       // ------------------------------ screening ------------------------------
       // Warp (group g, quarter q) owns TMEM lanes 32q.. of the stages j with
@@ -1103,7 +1209,7 @@ __global__ void __maxnreg__(MAXREG)
           }
           pre = fmin(pre, p2);
         }
-        if (st.iso == 0 && st.valid) {
+        if (st.iso == 0 && st.valid && !pil) {
           const int64_t g = (int64_t)tile * a.RT + (r + rbase) / n_iso;
           Partial out;
           out.err = err;
@@ -1115,7 +1221,7 @@ __global__ void __maxnreg__(MAXREG)
           out.valid = (dom != 0xffffffffu) ? 1 : 0;
           Partial* dst = a.partials + a.slot_base[tlist[g]] + slot;
           *dst = out;
-          if (it < n_whole)  // a whole segment: its piece slots stay empty
+          if (it - n_pilot < n_whole)  // a whole segment: its piece slots stay empty
             for (int q = 1; q < a.nsub; ++q) dst[q].valid = 0;
         }
       }

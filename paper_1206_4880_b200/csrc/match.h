@@ -148,6 +148,9 @@ struct TcArgs {
   uint4* sl;
   uint32_t* sl_count;          // [1] entries appended (may exceed sl_cap: the rest were queued)
   uint32_t sl_cap;
+  int pilot_cols;              // > 0: one pilot item per tile first (the first pilot_cols columns of its
+                               // window): per row the PK largest |u|, evaluated exactly, seed the
+                               // ranges' thresholds (thr_g) for the main items
   int sl_all;                  // 1: every survivor goes to the list (the queues carry seeds only);
                                // 2: the same after each tile's first segment (a pilot with the queues)
 };

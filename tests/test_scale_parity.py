@@ -160,12 +160,15 @@ def test_pool_builder_outputs_match_reference(cname, strategy, planes, monkeypat
 
 
 @pytest.mark.parametrize("env", [{"FIC_SL": "1"}, {"FIC_SL": "1", "FIC_SL_ALL": "1"},
+                                 {"FIC_PILOT": "4096"}, {"FIC_PILOT": "0"},
+                                 {"FIC_PILOT": "16384", "FIC_SL": "1", "FIC_SL_ALL": "1"},
                                  {"FIC_SL": "1", "FIC_SL_CAP": "7"}])
 @pytest.mark.parametrize("prefix", ["cfg2", "cfg2_ex"])
 def test_survivor_paths_match_reference(prefix, env, monkeypatch):
     """Every way a survivor can be rescored gives the reference's records:
     the survivor list (overflow of the rescoring warp's queues, or every
-    survivor), and a
+    survivor), with and without the pilot items that seed the thresholds,
+    and a
     survivor list that overflows after 7 entries (the rest go through the
     rescoring warp)."""
     for k, v in env.items():
