@@ -87,7 +87,6 @@ static_assert(NACC % NGRP == 0, "screening groups must own whole accumulator sta
 static_assert((BN / NSPLIT) % CH == 0 && CH % 32 == 0, "slices hold whole chunks of x32 loads");
 constexpr int QCAP = 32;      // survivor queue entries per (row, slice)
 constexpr int PK = 8;         // pilot: |u| candidates kept per row and screening group
-static_assert(2 * NGRP * PK <= NSLICE * QCAP, "pilot lists live in the survivor-queue buffer");
 constexpr int MMA0 = 1;       // first MMA issuing warp (warp 0: TMA producer)
 constexpr int RES0 = MMA0 + NMMA;  // first rescoring warp
 constexpr int RSTRIDE = 32 * NRES;
@@ -304,29 +303,6 @@ __device__ __forceinline__ uint32_t swz(int r, int c) {
 
 using namespace tc;
 
-// Pilot list insertion: replace the smallest of the row's PK entries (stride
-// BM in shared memory) by (x, pos); returns the new smallest |u|, or -1
-// while the list still has free (negative) entries.  Out of line: the
-// screener's chunk values stay in registers at the call sites.
-__device__ __noinline__ float pilot_insert(float* lv, uint32_t* lp, float x, uint32_t pos) {
-  int km = 0;
-  float vm = lv[0];
-#pragma unroll
-  for (int k = 1; k < PK; ++k) {
-    const float y = lv[k * BM];
-    if (y < vm) {
-      vm = y;
-      km = k;
-    }
-  }
-  lv[km * BM] = x;
-  lp[km * BM] = pos;
-  float nk = lv[0];
-#pragma unroll
-  for (int k = 1; k < PK; ++k) nk = fminf(nk, lv[k * BM]);
-  return nk;
-}
-
 template <int K, int CG, bool DBG>
 __global__ void __maxnreg__(MAXREG)
     k_match_tc(const __grid_constant__ CUtensorMap tmB, PoolView P, RangeView Rv, TcArgs a) {
@@ -495,7 +471,7 @@ __global__ void __maxnreg__(MAXREG)
       tile = (int)v;
       slot = -1;
       c0 = a.wlo[tile];
-      c1 = max(c0, min((int64_t)a.whi[tile], c0 + a.pilot_cols));
+      c1 = max(c0, min((int64_t)a.whi[tile], c0 + a.pilot_cols));  // (the whole window when strided)
       return;
     }
     v -= n_pilot;
@@ -528,7 +504,9 @@ __global__ void __maxnreg__(MAXREG)
     int tile = 0, slot = 0;
     int64_t c0 = 0, c1 = 0;
     item_cols(it, tile, slot, c0, c1);
-    const int nt = (int)cdiv(c1 - c0, BN);
+    // pilot items sample every pilot_stride-th N-tile of the window
+    const int tstep = slot < 0 ? BN * a.pilot_stride : BN;
+    const int nt = (int)cdiv(c1 - c0, (int64_t)tstep);
     // survivors of this item: the rescoring warp's queues first (overflow to
     // the survivor list), or all to the list -- for every item (sl_all 1) or
     // after each tile's first segment, the pilot that sets the thresholds (2)
@@ -635,7 +613,7 @@ __global__ void __maxnreg__(MAXREG)
             if (leader) mbar_expect_tx(full_bar(stage), C::TX_BYTES);
             const uint32_t fb = (CG == 2) ? map_to_rank(full_bar(stage), 0) : full_bar(stage);
             tma_load<CG>(smem_u32(sB + stage * C::B_BYTES), &tmB, fb, 0,
-                         (int)(c0 + (int64_t)j * BN + (BN / CG) * (int)crank));
+                         (int)(c0 + (int64_t)j * tstep + (BN / CG) * (int)crank));
           }
         }
         __syncwarp();
@@ -650,13 +628,14 @@ __global__ void __maxnreg__(MAXREG)
           int ntile = 0, nslot = 0;
           int64_t n0 = 0, n1 = 0;
           item_cols(nit, ntile, nslot, n0, n1);
-          const int nnt = (int)cdiv(n1 - n0, BN);
+          const int nstep = nslot < 0 ? BN * a.pilot_stride : BN;
+          const int nnt = (int)cdiv(n1 - n0, (int64_t)nstep);
           const int pre = min(nnt, C::NST / 2);
           for (int j = 0; j < pre; ++j) {
             mbar_wait(empty_bar(stage), ph ^ 1);
             if (elect_one()) {
               mbar_expect_tx(full_bar(stage), C::TX_BYTES);
-              tma_load<CG>(smem_u32(sB + stage * C::B_BYTES), &tmB, full_bar(stage), 0, (int)(n0 + (int64_t)j * BN));
+              tma_load<CG>(smem_u32(sB + stage * C::B_BYTES), &tmB, full_bar(stage), 0, (int)(n0 + (int64_t)j * nstep));
             }
             __syncwarp();
             if (++stage == C::NST) { stage = 0; ph ^= 1; }
@@ -698,14 +677,17 @@ __global__ void __maxnreg__(MAXREG)
       }
     } else if (is_scr && pil) {
       // ------------------------------ pilot ---------------------------------
-      // Top-PK |u| per row over the pilot columns (no survivors, no seeds):
-      // their exact errors, min over the range's rows, are the range's
-      // starting threshold for the main items (thr_g).  The lists live in
-      // the (unused) survivor-queue buffer, one per (group, row).
-      float* lv = reinterpret_cast<float*>(qbuf);      // [NGRP][PK][BM]
-      uint32_t* lp = qbuf + NGRP * PK * BM;               // [NGRP][PK][BM]
+      // The PK largest chunk maxima of |u| per row over the pilot columns
+      // (no survivors, no seeds), in registers: their exact errors, min over
+      // the range's rows, are the range's starting threshold for the main
+      // items (thr_g).
+      float lv[PK];
+      uint32_t lp[PK];
 #pragma unroll
-      for (int k = 0; k < PK; ++k) lv[(group * PK + k) * BM + row] = -1.0f;
+      for (int k = 0; k < PK; ++k) {
+        lv[k] = -1.0f;
+        lp[k] = 0;
+      }
       float kth = -1.0f;  // smallest |u| in the list (-1 while it has free entries)
       const uint32_t lane_base = tmem_base + ((uint32_t)(32 * (warp & 3)) << 16);
       const uint32_t tfull0 = tfull_bar(0), tempty0 = tempty_bar(0);
@@ -728,30 +710,58 @@ __global__ void __maxnreg__(MAXREG)
             __syncwarp();
             if (lane == 0) mbar_arrive(tempty0 + 8 * acc);
           }
-          const int32_t rel = j * BN + slice * SW + CH * h;
+          const int32_t rel = j * tstep + slice * SW + CH * h;
           const int32_t e_lo = lo32 - rel, e_hi = hi32 - rel;
-          float mx = -1.0f;
-#pragma unroll
-          for (int q = 0; q < CH; ++q) mx = fmaxf(mx, fabsf(v[q]));
           const bool in_window = (uint32_t)(e_hi - 1) < (uint32_t)(hi32 - lo32 + CH - 1);
-          if (in_window && !rflat && mx > kth) {
-            const int32_t wl = max(e_lo, 0), wh = min(e_hi, CH);
+          // the chunk's largest |u| inside the row's slab: four chains over
+          // the whole chunk, masked only for chunks cut by a slab edge
+          float mx;
+          const bool whole = e_lo <= 0 && e_hi >= CH;
+          if (whole) {
+            float m0 = -1.0f, m1 = -1.0f, m2 = -1.0f, m3 = -1.0f;
 #pragma unroll
-            for (int q = 0; q < CH; ++q) {
-              const float x = fabsf(v[q]);
-              if (x > kth && q >= wl && q < wh)
-                kth = pilot_insert(lv + group * PK * BM + row, lp + group * PK * BM + row, x,
-                                   (uint32_t)(rel + q));
+            for (int q = 0; q < CH; q += 8) {
+              m0 = fmaxf(fmaxf(m0, fabsf(v[q])), fabsf(v[q + 1]));
+              m1 = fmaxf(fmaxf(m1, fabsf(v[q + 2])), fabsf(v[q + 3]));
+              m2 = fmaxf(fmaxf(m2, fabsf(v[q + 4])), fabsf(v[q + 5]));
+              m3 = fmaxf(fmaxf(m3, fabsf(v[q + 6])), fabsf(v[q + 7]));
             }
+            mx = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3));
+          } else {
+            mx = -1.0f;
+#pragma unroll
+            for (int q = 0; q < CH; ++q) mx = fmaxf(mx, (q >= e_lo && q < e_hi) ? fabsf(v[q]) : -1.0f);
+          }
+          // keep the PK largest chunk maxima (one candidate per chunk): the
+          // insertion is rare once the list holds large values
+          if (in_window && !rflat && mx > kth) {
+            int idx = 0;
+#pragma unroll
+            for (int q = CH - 1; q >= 0; --q)
+              if (fabsf(v[q]) == mx && q >= e_lo && q < e_hi) idx = q;
+            // replace the smallest entry (the first one equal to kth), new smallest
+            bool done = false;
+#pragma unroll
+            for (int kk = 0; kk < PK; ++kk) {
+              const bool hitk = !done && lv[kk] == kth;
+              lv[kk] = hitk ? mx : lv[kk];
+              lp[kk] = hitk ? (uint32_t)(rel + idx) : lp[kk];
+              done = done || hitk;
+            }
+            float nk = lv[0];
+#pragma unroll
+            for (int kk = 1; kk < PK; ++kk) nk = fminf(nk, lv[kk]);
+            kth = nk;
           }
         }
       }
       // exact errors of the list; the range's minimum becomes its threshold
       double tnew = INFINITY;
       if (rvalid && !rflat) {
+#pragma unroll
         for (int k = 0; k < PK; ++k) {
-          if (lv[(group * PK + k) * BM + row] >= 0.0f) {
-            const int64_t pe = c0 + lp[(group * PK + k) * BM + row];
+          if (lv[k] >= 0.0f) {
+            const int64_t pe = c0 + lp[k];
             tnew = fmin(tnew, fmax(exact(pe, pool_id(P, pe), row, sr, srr).err, 0.0));
             ++evals;
           }

@@ -180,10 +180,18 @@ def test_survivor_paths_match_reference(prefix, env, monkeypatch):
         assert res.stats["sl_entries"] <= 7
 
 
-def test_cfg4_exhaustive_with_survivor_list_matches_reference(monkeypatch):
-    """cfg4 with every survivor on the survivor list (billions of
-    candidates, capacity overflow into the rescoring warp): bit-exact."""
-    monkeypatch.setenv("FIC_SL", "1")
-    monkeypatch.setenv("FIC_SL_ALL", "1")
+def test_cfg4_exhaustive_queue_path_matches_reference(monkeypatch):
+    """cfg4 without the pilot and the survivor list (the default for 4x4
+    ranges): every survivor through the rescoring warp, bit-exact too."""
+    monkeypatch.setenv("FIC_PILOT", "0")
+    monkeypatch.setenv("FIC_SL", "0")
     _, res = _check_full("scale_cfg4.npz", "cfg4_ex")
+    assert res.stats["sl_entries"] == 0
+
+
+def test_cfg4_default_uses_pilot_and_survivor_list():
+    import torch
+    g = _golden("scale_cfg4.npz")
+    strategy, kw = _kw(g, "cfg4_ex")
+    res = codec.encode_device(torch.from_numpy(g["cfg4_ex.image"]).cuda(), strategy, **kw)
     assert res.stats["sl_entries"] > 0
