@@ -658,11 +658,10 @@ __global__ void k_expand(const int32_t* nseg, const int32_t* base, const DevPlan
 
 // Work items in segment-major order: every tile's segment s before any
 // segment s + 1, so later segments start from the thresholds the earlier
-// ones found.  k_seg_hist counts the tiles per segment count, k_seg_base
-// turns that into each segment's first item, k_seg_fill places the items
-// (warp-aggregated atomics: inside a segment the tiles come roughly in tile
-// order, i.e. neighbouring FD windows run together; the order is scheduling
-// only, results do not depend on it).
+// ones found, and inside a segment in tile order, so the items running
+// together read neighbouring FD windows (L2 reuse).  k_seg_hist counts the
+// tiles per segment count, k_seg_base turns that into each segment's first
+// item, k_seg_place places each segment's items (one block per segment).
 __global__ void k_seg_hist(const int32_t* nseg, const DevPlan* dp, int smax, uint32_t* hist) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= dp->n_tt) return;
@@ -686,20 +685,24 @@ __global__ void __launch_bounds__(1024) k_seg_base(const uint32_t* hist, int sma
   }
 }
 
-__global__ void k_seg_fill(const int32_t* nseg, const DevPlan* dp, const uint32_t* base,
-                           uint32_t* cursor, int2* items) {
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int lane = threadIdx.x & 31;
-  const int ns = t < dp->n_tt ? nseg[t] : 0;
-  const int mx = __reduce_max_sync(0xffffffffu, ns);
-  for (int sg = 0; sg < mx; ++sg) {
-    const bool act = ns > sg;
-    const unsigned bal = __ballot_sync(0xffffffffu, act);
-    const int leader = __ffs(bal) - 1;
-    uint32_t off = 0;
-    if (lane == leader) off = atomicAdd(cursor + sg, (uint32_t)__popc(bal));
-    off = __shfl_sync(0xffffffffu, off, leader);
-    if (act) items[base[sg] + off + __popc(bal & ((1u << lane) - 1u))] = make_int2((int)t, sg);
+// Segment s's items in tile order: block s scans the flags (tile t has a
+// segment s) and places (t, s) at base[s] + its rank -- the (segment, tile)
+// order of the round-1 single-block loop, in parallel over the segments.
+__global__ void __launch_bounds__(1024) k_seg_place(const int32_t* nseg, const DevPlan* dp,
+                                                    const uint32_t* base, int2* items) {
+  using Scan = cub::BlockScan<int, 1024>;
+  __shared__ typename Scan::TempStorage tmp;
+  const int sg = blockIdx.x;
+  const int64_t n = dp->n_tt;
+  int64_t carry = base[sg];
+  for (int64_t t0 = 0; t0 < n; t0 += 1024) {
+    const int64_t t = t0 + threadIdx.x;
+    const int flag = (t < n && nseg[t] > sg) ? 1 : 0;
+    int rank = 0, total = 0;
+    Scan(tmp).ExclusiveSum(flag, rank, total);
+    if (flag) items[carry + rank] = make_int2((int)t, sg);
+    carry += total;
+    __syncthreads();
   }
 }
 
@@ -1300,7 +1303,7 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
     FIC_CHECK_LAUNCH();
     k_seg_base<<<1, 32, 0, s>>>(shist, smax, sbase2, scur);
     FIC_CHECK_LAUNCH();
-    k_seg_fill<<<(unsigned)cdiv(n_tt_max, 256), 256, 0, s>>>(tnseg, d_plan, sbase2, scur, titems);
+    k_seg_place<<<(unsigned)smax, 1024, 0, s>>>(tnseg, d_plan, sbase2, titems);
     FIC_CHECK_LAUNCH();
   }
   k_expand<<<(unsigned)cdiv(n_er_max, 128), 128, 0, s>>>(enseg, ebase, d_plan, eitems);

@@ -46,6 +46,9 @@
 #ifndef FIC_TC_SL
 #define FIC_TC_SL 1  // 0: compile the survivor-list append out of the screeners
 #endif
+#ifndef FIC_TC_PILOT
+#define FIC_TC_PILOT 1  // 0: compile the pilot screening out
+#endif
 #ifndef FIC_TC_BAL
 #define FIC_TC_BAL 0  // 1: balanced drain of the survivor queues (measured slower: DESIGN.md)
 #endif
@@ -303,7 +306,7 @@ __device__ __forceinline__ uint32_t swz(int r, int c) {
 
 using namespace tc;
 
-template <int K, int CG, bool DBG>
+template <int K, int CG, bool DBG, int SRC>
 __global__ void __maxnreg__(MAXREG)
     k_match_tc(const __grid_constant__ CUtensorMap tmB, PoolView P, RangeView Rv, TcArgs a) {
   using C = Cfg<K, CG>;
@@ -419,7 +422,7 @@ __global__ void __maxnreg__(MAXREG)
   // L2-resident row segments / planes (DomSrc)
   auto exact = [&](int64_t p, uint32_t id, int erow, double esr, double esrr) -> Cand {
     uint32_t dw[C::KW];
-    dom_words<K>(P, p, id, dw);
+    dom_words<K, SRC>(P, p, id, dw);
     uint32_t acc32 = 0;
     const uint4* rrow = reinterpret_cast<const uint4*>(sRows + erow * K);
 #pragma unroll
@@ -675,7 +678,7 @@ __global__ void __maxnreg__(MAXREG)
         acc += NMMA;
         if (acc >= NACC) { acc -= NACC; acc_ph ^= 1; }
       }
-    } else if (is_scr && pil) {
+    } else if (FIC_TC_PILOT && is_scr && pil) {
       // ------------------------------ pilot ---------------------------------
       // The PK largest chunk maxima of |u| per row over the pilot columns
       // (no survivors, no seeds), in registers: their exact errors, min over
@@ -1323,7 +1326,7 @@ static int tc_cg(int K) {
 }
 int tc_tile_rows(int K) { return BM * tc_cg(K); }
 
-template <int K, int CG>
+template <int K, int CG, int SRC>
 static void launch_tc_k(const PoolView& P, const RangeView& Rv, const TcArgs& a, cudaStream_t s) {
   using C = Cfg<K, CG>;
   CUtensorMap map;
@@ -1337,8 +1340,8 @@ static void launch_tc_k(const PoolView& P, const RangeView& Rv, const TcArgs& a,
                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (cr != CUDA_SUCCESS) throw Error{FIC_ECUDA, "cuTensorMapEncodeTiled failed"};
-  smem_optin_k(k_match_tc<K, CG, false>, C::SMEM);
-  smem_optin_k(k_match_tc<K, CG, true>, C::SMEM);
+  smem_optin_k(k_match_tc<K, CG, false, SRC>, C::SMEM);
+  smem_optin_k(k_match_tc<K, CG, true, SRC>, C::SMEM);
   int dev = 0, sms = 148;
   FIC_CUDA(cudaGetDevice(&dev));
   FIC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -1359,22 +1362,32 @@ static void launch_tc_k(const PoolView& P, const RangeView& Rv, const TcArgs& a,
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   if (aa.debug)
-    FIC_CUDA(cudaLaunchKernelEx(&cfg, k_match_tc<K, CG, true>, map, P, Rv, aa));
+    FIC_CUDA(cudaLaunchKernelEx(&cfg, k_match_tc<K, CG, true, SRC>, map, P, Rv, aa));
   else
-    FIC_CUDA(cudaLaunchKernelEx(&cfg, k_match_tc<K, CG, false>, map, P, Rv, aa));
+    FIC_CUDA(cudaLaunchKernelEx(&cfg, k_match_tc<K, CG, false, SRC>, map, P, Rv, aa));
   FIC_CHECK_LAUNCH();
 }
 
 void launch_tc(const PoolView& P, const RangeView& Rv, const TcArgs& a, cudaStream_t s) {
   if (a.n_items == 0) return;
-  if (Rv.K == 64 && tc_cg(64) == 2)
-    launch_tc_k<64, 2>(P, Rv, a, s);
-  else if (Rv.K == 64)
-    launch_tc_k<64, 1>(P, Rv, a, s);
-  else if (Rv.K == 16)
-    launch_tc_k<16, 1>(P, Rv, a, s);
-  else
+  // one instantiation per domain source (DomSrc): row segments or box planes
+  const bool trows = P.src.trows != nullptr;
+  if (!trows && !P.src.planes) invalid("tensor matcher needs the row segments or box planes");
+  if (Rv.K == 64 && tc_cg(64) == 2) {
+    if (trows)
+      launch_tc_k<64, 2, SRC_TROWS>(P, Rv, a, s);
+    else
+      launch_tc_k<64, 2, SRC_PLANES>(P, Rv, a, s);
+  } else if (Rv.K == 64) {
+    if (trows)
+      launch_tc_k<64, 1, SRC_TROWS>(P, Rv, a, s);
+    else
+      launch_tc_k<64, 1, SRC_PLANES>(P, Rv, a, s);
+  } else if (Rv.K == 16) {
+    launch_tc_k<16, 1, SRC_PLANES>(P, Rv, a, s);
+  } else {
     invalid("tensor matcher supports range_size 4 and 8");
+  }
 }
 
 }  // namespace fic

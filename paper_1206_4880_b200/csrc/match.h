@@ -39,15 +39,20 @@ __device__ __forceinline__ uint32_t bytes4_at(const uint8_t* q) {
 }
 
 // The K/4 little-endian words of the decimated domain at pool position p
-// (raster id `id`), K = 64 or 16 (RS 8 / 4).
-template <int K>
+// (raster id `id`), K = 64 or 16 (RS 8 / 4).  SRC selects the source at
+// compile time (the tensor matcher is instantiated per source: a runtime
+// three-way branch in its inlined rescoring costs the screeners registers);
+// SRC_ANY branches at run time (exact matchers, tests).
+enum { SRC_TROWS = 0, SRC_PLANES = 1, SRC_RAW = 2, SRC_ANY = 3 };
+
+template <int K, int SRC = SRC_ANY>
 __device__ __forceinline__ void dom_words(const PoolView& P, int64_t p, uint32_t id,
                                           uint32_t (&w)[K / 4]) {
   constexpr int RS = K == 64 ? 8 : 4;
   const DomSrc& d = P.src;
   const uint32_t dy = id / (uint32_t)d.ndx, dx = id - dy * (uint32_t)d.ndx;
   const uint32_t Y = dy * d.st, X = dx * d.st;
-  if (RS == 8 && d.trows) {
+  if (RS == 8 && (SRC == SRC_TROWS || (SRC == SRC_ANY && d.trows))) {
     const unsigned long long* t = d.trows + ((size_t)dx * 2 + (Y & 1)) * d.mh + (Y >> 1);
 #pragma unroll
     for (int i = 0; i < RS; ++i) {
@@ -55,7 +60,7 @@ __device__ __forceinline__ void dom_words(const PoolView& P, int64_t p, uint32_t
       w[2 * i] = (uint32_t)v;
       w[2 * i + 1] = (uint32_t)(v >> 32);
     }
-  } else if (d.planes) {
+  } else if (SRC == SRC_PLANES || (SRC == SRC_ANY && d.planes)) {
     const uint8_t* b = d.planes + (size_t)(X & 1) * d.plane_rows * d.pitch + (size_t)Y * d.pitch +
                        (X >> 1);
 #pragma unroll

@@ -1,5 +1,8 @@
 """A/B of library builds on one config, alternating processes:
     python tools/ab_lib.py cfg3 ROUNDS A.so B.so ...
+A directory argument is a whole package snapshot (DIR/paper_1206_4880_b200
+with its own library, e.g. an older round's build), imported instead of the
+in-tree package.
 Each process does a warm-up encode then 5 timed ones; prints the median
 device ms (ms_total, ms_tensor) per build and round."""
 import json
@@ -9,8 +12,8 @@ import sys
 
 name, rounds, libs = sys.argv[1], int(sys.argv[2]), sys.argv[3:]
 code = r'''
-import sys, json, torch
-sys.path.insert(0, ".")
+import os, sys, json, torch
+sys.path.insert(0, os.environ.get("AB_PKG_ROOT", "."))
 from paper_1206_4880_b200 import codec, synth
 c = synth.CONFIGS[sys.argv[1]]
 img = torch.from_numpy(c.make()).cuda()
@@ -18,11 +21,16 @@ kw = dict(range_size=c.range_size, domain_size=c.domain_size, stride=c.stride, i
 codec.encode_device(img, c.strategy, **kw)
 st = [codec.encode_device(img, c.strategy, **kw).stats for _ in range(5)]
 print(json.dumps({k: sorted(s[k] for s in st)[2] for k in ("ms_total", "ms_tensor")}))
+print("#", codec.__file__, file=sys.stderr)
 '''
 res = {lib: [] for lib in libs}
 for _ in range(rounds):
     for lib in libs:
-        env = dict(os.environ, FIC_B200_LIB=os.path.abspath(lib))
+        if os.path.isdir(lib):
+            env = dict(os.environ, AB_PKG_ROOT=os.path.abspath(lib))
+            env.pop("FIC_B200_LIB", None)
+        else:
+            env = dict(os.environ, FIC_B200_LIB=os.path.abspath(lib))
         out = subprocess.run([sys.executable, "-c", code, name], env=env, capture_output=True,
                              text=True)
         line = [l for l in out.stdout.splitlines() if l.startswith("{")]
