@@ -1319,9 +1319,11 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
   // thresholds start from the final errors of the previous call with the
   // same R on this device -- how much of K4 is threshold discovery
   static std::map<std::pair<int, int>, unsigned long long*> prime_cache;
+  static std::mutex prime_mu;
   unsigned long long* prime_buf = nullptr;
   bool prime_ok = false;
   if (getenv("FIC_PRIME_THR")) {
+    std::lock_guard<std::mutex> lock(prime_mu);
     auto& pb2 = prime_cache[{dev_id, g.R}];
     prime_ok = pb2 != nullptr;
     if (!pb2) FIC_CUDA(cudaMalloc(&pb2, g.R * 8));
