@@ -89,7 +89,10 @@ constexpr bool WIDE = FIC_TC_WIDE;  // load a whole stage before screening (need
 static_assert(NACC % NGRP == 0, "screening groups must own whole accumulator stages");
 static_assert((BN / NSPLIT) % CH == 0 && CH % 32 == 0, "slices hold whole chunks of x32 loads");
 constexpr int QCAP = 32;      // survivor queue entries per (row, slice)
-constexpr int PK = 8;         // pilot: |u| candidates kept per row and screening group
+constexpr int PK = 8;         // pilot: |u| candidates kept per row and screening group (4x4 ranges)
+#ifndef FIC_TC_PK64
+#define FIC_TC_PK64 2         // (8x8 ranges)
+#endif
 constexpr int MMA0 = 1;       // first MMA issuing warp (warp 0: TMA producer)
 constexpr int RES0 = MMA0 + NMMA;  // first rescoring warp
 constexpr int RSTRIDE = 32 * NRES;
@@ -680,14 +683,17 @@ __global__ void __maxnreg__(MAXREG)
       }
     } else if (FIC_TC_PILOT && is_scr && pil) {
       // ------------------------------ pilot ---------------------------------
-      // The PK largest chunk maxima of |u| per row over the pilot columns
+      // (8x8 ranges: the best |u| per row is already a near-final threshold,
+      // keep FIC_TC_PK64; 4x4 ranges need 8)
+      constexpr int PKK = (K == 64) ? FIC_TC_PK64 : PK;
+      // The PKK largest chunk maxima of |u| per row over the pilot columns
       // (no survivors, no seeds), in registers: their exact errors, min over
       // the range's rows, are the range's starting threshold for the main
       // items (thr_g).
-      float lv[PK];
-      uint32_t lp[PK];
+      float lv[PKK];
+      uint32_t lp[PKK];
 #pragma unroll
-      for (int k = 0; k < PK; ++k) {
+      for (int k = 0; k < PKK; ++k) {
         lv[k] = -1.0f;
         lp[k] = 0;
       }
@@ -735,7 +741,7 @@ __global__ void __maxnreg__(MAXREG)
 #pragma unroll
             for (int q = 0; q < CH; ++q) mx = fmaxf(mx, (q >= e_lo && q < e_hi) ? fabsf(v[q]) : -1.0f);
           }
-          // keep the PK largest chunk maxima (one candidate per chunk): the
+          // keep the PKK largest chunk maxima (one candidate per chunk): the
           // insertion is rare once the list holds large values
           if (in_window && !rflat && mx > kth) {
             int idx = 0;
@@ -745,7 +751,7 @@ __global__ void __maxnreg__(MAXREG)
             // replace the smallest entry (the first one equal to kth), new smallest
             bool done = false;
 #pragma unroll
-            for (int kk = 0; kk < PK; ++kk) {
+            for (int kk = 0; kk < PKK; ++kk) {
               const bool hitk = !done && lv[kk] == kth;
               lv[kk] = hitk ? mx : lv[kk];
               lp[kk] = hitk ? (uint32_t)(rel + idx) : lp[kk];
@@ -753,22 +759,29 @@ __global__ void __maxnreg__(MAXREG)
             }
             float nk = lv[0];
 #pragma unroll
-            for (int kk = 1; kk < PK; ++kk) nk = fminf(nk, lv[kk]);
+            for (int kk = 1; kk < PKK; ++kk) nk = fminf(nk, lv[kk]);
             kth = nk;
           }
         }
       }
-      // exact errors of the list; the range's minimum becomes its threshold
+      // exact errors of the list (all evaluated, branch-free, so their
+      // gathers overlap; free entries repeat the first used one); the
+      // range's minimum becomes its threshold
       double tnew = INFINITY;
-      if (rvalid && !rflat) {
+      int kv = -1;
 #pragma unroll
-        for (int k = 0; k < PK; ++k) {
-          if (lv[k] >= 0.0f) {
-            const int64_t pe = c0 + lp[k];
-            tnew = fmin(tnew, fmax(exact(pe, pool_id(P, pe), row, sr, srr).err, 0.0));
-            ++evals;
-          }
+      for (int k = PKK - 1; k >= 0; --k)
+        if (lv[k] >= 0.0f) kv = k;
+      uint32_t pfirst = lp[0];
+#pragma unroll
+      for (int k = 1; k < PKK; ++k) pfirst = (kv == k) ? lp[k] : pfirst;
+      if (rvalid && !rflat && kv >= 0) {
+#pragma unroll
+        for (int k = 0; k < PKK; ++k) {
+          const int64_t pe = c0 + (lv[k] >= 0.0f ? lp[k] : pfirst);
+          tnew = fmin(tnew, fmax(exact(pe, pool_id(P, pe), row, sr, srr).err, 0.0));
         }
+        evals += PKK;
       }
       for (int m = 1; m < n_iso; m <<= 1) tnew = fmin(tnew, __shfl_xor_sync(0xffffffffu, tnew, m));
       if (iso == 0 && rvalid && tnew < INFINITY) {
