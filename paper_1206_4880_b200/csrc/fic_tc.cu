@@ -89,6 +89,7 @@ constexpr bool WIDE = FIC_TC_WIDE;  // load a whole stage before screening (need
 static_assert(NACC % NGRP == 0, "screening groups must own whole accumulator stages");
 static_assert((BN / NSPLIT) % CH == 0 && CH % 32 == 0, "slices hold whole chunks of x32 loads");
 constexpr int QCAP = 32;      // survivor queue entries per (row, slice)
+constexpr uint32_t SLCH = 512;  // survivor-list entries per screening-warp chunk
 constexpr int PK = 8;         // pilot: |u| candidates kept per row and screening group (4x4 ranges)
 #ifndef FIC_TC_PK64
 #define FIC_TC_PK64 2         // (8x8 ranges)
@@ -415,6 +416,12 @@ __global__ void __maxnreg__(MAXREG)
   bool rvalid = false;
   bool rflat = false;  // flat range on the canonical slab: the flat kernels match it
   unsigned long long evals = 0, seed_rounds = 0, hit_rounds = 0, hit_lanes = 0;
+  // survivor list: each screening warp appends into its own chunk of SLCH
+  // entries [sl_pos, sl_end), refilled with one global atomic per chunk (one
+  // atomic per appending warp on a single counter serialised in L2); a chunk
+  // starting at or past sl_cap ends the warp's list use (the queues take the rest)
+  uint32_t sl_pos = 0, sl_end = 0;
+  bool sl_dead = false;
   long long tw0 = 0, tw1 = 0, tw2 = 0, tw3 = 0, tw4 = 0;  // stall cycles (debug & 4)
   const long long tstart = TCLK();
   unsigned long long gt_start = 0;  // debug & 8192: per-CTA start / end (globaltimer, ns)
@@ -722,32 +729,36 @@ __global__ void __maxnreg__(MAXREG)
           const int32_t rel = j * tstep + slice * SW + CH * h;
           const int32_t e_lo = lo32 - rel, e_hi = hi32 - rel;
           const bool in_window = (uint32_t)(e_hi - 1) < (uint32_t)(hi32 - lo32 + CH - 1);
-          // the chunk's largest |u| inside the row's slab: four chains over
-          // the whole chunk, masked only for chunks cut by a slab edge
+          // the chunk's largest |u| inside the row's slab, with its column:
+          // key = |u| with the column index in the low 6 mantissa bits (a
+          // non-negative float, so float max = integer max on the bits); the
+          // truncation (2^-17 relative) only affects which near-equal
+          // candidate seeds the threshold, never soundness.  Four chains over
+          // the whole chunk, masked only for chunks cut by a slab edge.
+          static_assert(CH == 64, "the pilot key holds a 6-bit column index");
+          const uint32_t km = 0x7FFFFFC0u;
+          auto key = [&](int q) { return __uint_as_float((__float_as_uint(v[q]) & km) | (uint32_t)q); };
           float mx;
           const bool whole = e_lo <= 0 && e_hi >= CH;
           if (whole) {
-            float m0 = -1.0f, m1 = -1.0f, m2 = -1.0f, m3 = -1.0f;
+            float m0 = 0.0f, m1 = 0.0f, m2 = 0.0f, m3 = 0.0f;
 #pragma unroll
             for (int q = 0; q < CH; q += 8) {
-              m0 = fmaxf(fmaxf(m0, fabsf(v[q])), fabsf(v[q + 1]));
-              m1 = fmaxf(fmaxf(m1, fabsf(v[q + 2])), fabsf(v[q + 3]));
-              m2 = fmaxf(fmaxf(m2, fabsf(v[q + 4])), fabsf(v[q + 5]));
-              m3 = fmaxf(fmaxf(m3, fabsf(v[q + 6])), fabsf(v[q + 7]));
+              m0 = fmaxf(fmaxf(m0, key(q)), key(q + 1));
+              m1 = fmaxf(fmaxf(m1, key(q + 2)), key(q + 3));
+              m2 = fmaxf(fmaxf(m2, key(q + 4)), key(q + 5));
+              m3 = fmaxf(fmaxf(m3, key(q + 6)), key(q + 7));
             }
             mx = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3));
           } else {
             mx = -1.0f;
 #pragma unroll
-            for (int q = 0; q < CH; ++q) mx = fmaxf(mx, (q >= e_lo && q < e_hi) ? fabsf(v[q]) : -1.0f);
+            for (int q = 0; q < CH; ++q) mx = fmaxf(mx, (q >= e_lo && q < e_hi) ? key(q) : -1.0f);
           }
           // keep the PKK largest chunk maxima (one candidate per chunk): the
           // insertion is rare once the list holds large values
           if (in_window && !rflat && mx > kth) {
-            int idx = 0;
-#pragma unroll
-            for (int q = CH - 1; q >= 0; --q)
-              if (fabsf(v[q]) == mx && q >= e_lo && q < e_hi) idx = q;
+            const int idx = (int)(__float_as_uint(mx) & 63u);
             // replace the smallest entry (the first one equal to kth), new smallest
             bool done = false;
 #pragma unroll
@@ -894,12 +905,21 @@ __global__ void __maxnreg__(MAXREG)
             const uint32_t n = (uint32_t)__popcll(m);
             const bool to_list = list_all ? n > 0 : n > (uint32_t)QCAP - (qt - *myhead);
             const unsigned lm = __ballot_sync(0xffffffffu, to_list);
-            if (lm) {
-              const int leader = __ffs(lm) - 1;
-              uint32_t base = 0;
-              if (lane == leader) base = atomicAdd(a.sl_count, (uint32_t)__popc(lm));
-              base = __shfl_sync(0xffffffffu, base, leader);
-              const uint32_t idx = base + (uint32_t)__popc(lm & ((1u << lane) - 1u));
+            if (lm && !sl_dead) {
+              const uint32_t cnt = (uint32_t)__popc(lm), left = sl_end - sl_pos;
+              const uint32_t k = (uint32_t)__popc(lm & ((1u << lane) - 1u));
+              uint32_t idx = sl_pos + k;
+              if (cnt > left) {  // warp-uniform: the rest goes to a fresh chunk
+                uint32_t nb = 0;
+                if (lane == 0) nb = atomicAdd(a.sl_count, (uint32_t)SLCH);
+                nb = __shfl_sync(0xffffffffu, nb, 0);
+                if (k >= left) idx = nb + (k - left);
+                sl_pos = nb + (cnt - left);
+                sl_end = nb + SLCH;
+                sl_dead = nb >= a.sl_cap;
+              } else {
+                sl_pos += cnt;
+              }
               if (to_list && idx < a.sl_cap) {
                 a.sl[idx] = make_uint4((rid << 3) | (uint32_t)iso, (uint32_t)(c0 + rel), (uint32_t)m,
                                        (uint32_t)(m >> 32));
@@ -1260,6 +1280,9 @@ __global__ void __maxnreg__(MAXREG)
     (void)ti1;
   }
 
+  if (FIC_TC_SL && is_scr && a.sl) {  // unused tail of the warp's chunk: empty entries
+    for (uint32_t i = sl_pos + lane; i < min(sl_end, a.sl_cap); i += 32) a.sl[i] = make_uint4(0, 0, 0, 0);
+  }
   if (is_res || is_scr) {
     for (int m = 16; m >= 1; m >>= 1) evals += __shfl_xor_sync(0xffffffffu, evals, m);
     if (lane == 0) atomicAdd(a.counters, evals);

@@ -151,7 +151,8 @@ struct TcArgs {
   // 0, 64-bit survivor mask) here instead of waiting for the rescoring warp;
   // k_sl_rescore evaluates them after the matcher.  nullptr = off.
   uint4* sl;
-  uint32_t* sl_count;          // [1] entries appended (may exceed sl_cap: the rest were queued)
+  uint32_t* sl_count;          // [1] entries handed out in per-warp chunks (unused chunk tails hold
+                               // empty entries; may exceed sl_cap: the rest were queued)
   uint32_t sl_cap;
   int pilot_cols;              // > 0: one pilot item per tile first (the first pilot_cols columns of its
                                // window): per row the PK largest |u|, evaluated exactly, seed the
