@@ -110,8 +110,10 @@ typedef struct fic_stats {
   int32_t kernel_launches;   /* kernels this call launched (library-internal CUB passes excluded) */
   double ms_pool_main;       /* device time of the pool builder's main kernel (k_pool) alone */
   int64_t reserved0;         /* 0 */
-  double ms_sl;              /* device time of the survivor-list rescoring (k_sl_rescore) */
+  double ms_sl;              /* device time of the survivor-list and hit-list rescoring (k_sl_rescore, k_hl_rescore) */
   int64_t sl_entries;        /* survivor-list entries (row, 64-column chunk, mask) rescored after the matcher */
+  int64_t hl_entries;        /* hit-list entries (warp of rows, 64-column chunk, hit ballot) rescored after the matcher */
+  int64_t hl_tests;          /* hit-list candidates tested against the exact lower bound */
 } fic_stats_t;
 
 /* Replaces fic.codec.encode (codec.py:290-427) for one image already in

@@ -67,6 +67,8 @@ class FicStats(ctypes.Structure):
         ("reserved0", ctypes.c_int64),
         ("ms_sl", ctypes.c_double),
         ("sl_entries", ctypes.c_int64),
+        ("hl_entries", ctypes.c_int64),
+        ("hl_tests", ctypes.c_int64),
     ]
 
     def as_dict(self) -> dict:

@@ -1122,7 +1122,8 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
     double scal[4];
     DevPlan plan;
     unsigned long long flat[2];  // [0] flat count, [1] low word: canonical flat range
-    uint32_t sl_count[2];        // [0] survivor-list entries appended
+    uint32_t sl_count[2];        // [0] survivor-list entries appended, [1] hit-list entries
+    unsigned long long hl_tests;  // hit-list lower-bound tests
   };
   Readback* d_rb = sc.get<Readback>(1);
   FIC_CUDA(cudaMemsetAsync(d_rb, 0, sizeof(Readback), s));
@@ -1315,6 +1316,7 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
   RangeView Rv{ra.info, ra.rows, pb.lo, pb.hi, g.n_iso, K, ra.KP};
   tm.mark();  // 3
   SlArgs sla{};                    // survivor list (k_sl_rescore)
+  HlArgs hla{};                    // hit list (k_hl_rescore)
   // FIC_PRIME_THR (experiment only): the tensor matcher's per-range
   // thresholds start from the final errors of the previous call with the
   // same R on this device -- how much of K4 is threshold discovery
@@ -1372,6 +1374,24 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
       sla.counters = counters;
       k_sl_init<<<(unsigned)cdiv(g.R, 256), 256, 0, s>>>(sla.best, sla.pre, g.R);
       FIC_CHECK_LAUNCH();
+      // hit list (every survivor to the lists): one entry per hit warp-chunk,
+      // capacity min(128 M, max(1 M, 512 R)) entries; FIC_HL=0 turns it off
+      if (ta.sl_all == 1 && (!getenv("FIC_HL") || atoi(getenv("FIC_HL")) != 0)) {
+        ta.hl_cap = (uint32_t)std::min<int64_t>(128 << 20, std::max<int64_t>(1 << 20, 512 * (int64_t)g.R));
+        if (getenv("FIC_HL_CAP")) ta.hl_cap = (uint32_t)std::max(1, atoi(getenv("FIC_HL_CAP")));
+        ta.hl = sc.get<uint4>(ta.hl_cap);
+        ta.hl_count = d_rb->sl_count + 1;
+        hla.hl = ta.hl;
+        hla.hl_count = ta.hl_count;
+        hla.hl_cap = ta.hl_cap;
+        hla.tlist = rid_s;
+        hla.plan = d_plan;
+        hla.thr_g = thr_g;
+        hla.best = sla.best;
+        hla.pre = sla.pre;
+        hla.counters = counters;
+        hla.tests = &d_rb->hl_tests;
+      }
     }
     const char* dbg_env = getenv("FIC_TC_DEBUG");
     if (dbg_env && (atoi(dbg_env) & (32 | 8192))) {
@@ -1405,16 +1425,18 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
       FIC_CUDA(cudaMemcpyAsync(h.data(), ta.dbg, h.size() * 8, cudaMemcpyDeviceToHost, s));
       FIC_CUDA(cudaStreamSynchronize(s));
       unsigned long long t0 = h[0];
-      fprintf(stderr, "tile: tma_issue mma_issue | screener0: full ld_done max_done pre_release arrived\n");
-      for (int j = 0; j < 40; ++j) {
-        fprintf(stderr, "%3d: %7lld %7lld |", j, (long long)(h[j * 24] - t0), (long long)(h[j * 24 + 1] - t0));
-        for (int w = 4; w < 9; ++w) fprintf(stderr, " %7lld", (long long)(h[j * 24 + w] - t0));
+      fprintf(stderr, "tile: tma_issue mma_issue mma_tempty_ok | screener (group j%%2, quarter 0): tfull_ok ld0_done ld1_done\n");
+      for (int j = 0; j < 64; ++j) {
+        fprintf(stderr, "%3d: %7lld %7lld %7lld |", j, (long long)(h[j * 24] - t0), (long long)(h[j * 24 + 1] - t0),
+                (long long)(h[j * 24 + 2] - t0));
+        for (int w = 4; w < 7; ++w) fprintf(stderr, " %7lld", (long long)(h[j * 24 + w] - t0));
         fprintf(stderr, "\n");
       }
     }
   }
   FIC_CUDA(cudaEventRecord(tm.ev[21], s));
   launch_sl_rescore(P, Rv, sla, s);
+  launch_hl_rescore(P, Rv, hla, s);
   FIC_CUDA(cudaEventRecord(tm.ev[22], s));
   tm.mark();  // 4
   if (eitems_n) {
@@ -1478,6 +1500,8 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
     st->ms_tensor = tm.ms(3, 21);
     st->ms_sl = tm.ms(21, 22);
     st->sl_entries = std::min<int64_t>(hrb.sl_count[0], sla.sl_cap);
+    st->hl_entries = std::min<int64_t>(hrb.sl_count[1], hla.hl_cap);
+    st->hl_tests = (int64_t)hrb.hl_tests;
     st->ms_exact = tm.ms(4, 5);
     st->ms_total = n_flat ? tm.ms(0, 23) : tm.ms(0, 7);
     st->exact_evals = (int64_t)hc[0];

@@ -245,6 +245,182 @@ void launch_sl_rescore(const PoolView& P, const RangeView& Rv, const SlArgs& a, 
   FIC_CHECK_LAUNCH();
 }
 
+// Hit list (TcArgs::hl): one warp per entry.  Each lane holds two of the
+// chunk's 64 columns (decimated words, sum_d, K den) and, for lane j < the
+// number of hit rows, the j-th hit row's range data, all loaded at once.
+// The rows are then taken in turn (shuffled from their lane): every column
+// of the row's slab gets the exact lower bound test in integer / fp32
+// arithmetic, and the candidates that can still win or tie go to a per-warp
+// queue in shared memory that is evaluated 32 at a time with all lanes
+// (codec.py:218-258 via eval_candidate), publishing to the survivor list's
+// best / pre arrays only when a candidate beats what they hold.
+namespace {
+constexpr int HLQ = 128;  // queue slots per warp (< 32 queued + 64 of one row)
+}
+
+template <int K>
+__device__ __forceinline__ void hl_flush(const PoolView& P, const RangeView& Rv, const HlArgs& a,
+                                         const uint4* q, uint32_t head, int cnt, int lane,
+                                         unsigned long long& evals) {
+  if (lane < cnt) {
+    const uint4 c = q[(head + lane) & (HLQ - 1)];  // (rid, pool position, cross, iso)
+    const uint32_t rid = c.x, iso = c.w;
+    const int64_t p = c.y;
+    // every load first (one round trip): column, range, and the current bests
+    unsigned long long* slot = a.best + 2 * (int64_t)rid;
+    const uint2 sm = __ldg(P.sums + p);
+    const uint32_t did = pool_id(P, p);
+    const double inv = __ldg(P.inv_den + p);
+    const RangeInfo inf = Rv.info[rid];
+    const unsigned long long cpre = __ldcg(a.pre + rid);
+    unsigned long long clo = __ldcg(slot), chi = __ldcg(slot + 1);
+    const Cand cd = eval_candidate((double)c.z, (double)sm.x, (double)sm.y, inv, inf.sr, inf.srr, (double)K);
+    ++evals;
+    const unsigned long long kpre = ord_bits(cd.pre);
+    if (kpre < cpre) atomicMin(a.pre + rid, kpre);
+    const unsigned long long khi = ord_bits(cd.err);
+    const unsigned long long klo = ((unsigned long long)did << 32) | (iso << 24) |
+                                   ((uint32_t)cd.sq << 16) | ((uint32_t)cd.oq << 8);
+    while (khi < chi || (khi == chi && klo < clo)) {
+      unsigned long long olo, ohi;
+      cas128(slot, clo, chi, klo, khi, olo, ohi);
+      if (olo == clo && ohi == chi) break;
+      clo = olo;
+      chi = ohi;
+    }
+  }
+}
+
+template <int K>
+__global__ void __launch_bounds__(256, 3) k_hl_rescore(PoolView P, RangeView Rv, HlArgs a) {
+  constexpr int KW = K / 4;
+  __shared__ uint4 s_q[8][HLQ];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  uint4* q = s_q[wib];
+  uint32_t head = 0, tail = 0;  // queue (warp-uniform counters)
+  const int64_t n = (int64_t)min(*a.hl_count, a.hl_cap);
+  const int64_t warp0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int n_iso = Rv.n_iso;
+  const uint32_t* tl = a.tlist + (a.plan ? a.plan->tb : 0);
+  unsigned long long evals = 0, tests = 0;
+  uint4 en = warp0 < n ? a.hl[warp0] : make_uint4(0, 0, 0, 0);  // next entry (prefetched)
+  for (int64_t i = warp0; i < n; i += nwarps) {
+    const uint4 e = en;
+    if (i + nwarps < n) en = a.hl[i + nwarps];
+    if (e.w == 0) continue;
+    // this lane's hit row (lane < popc): range id, isometry, slab, sum_r, bound, pixels
+    const int nrows = __popc(e.w);
+    uint32_t rid = 0, iso = 0;
+    int32_t lo = 0, hi = 0, sr = 0;
+    float cth = -1.0f;  // V - threshold - margin, rounded down (<= 0: no bound)
+    uint32_t rw[KW];
+#pragma unroll
+    for (int w = 0; w < KW; ++w) rw[w] = 0;
+    if (lane < nrows) {
+      const int row = (int)e.y + (int)__fns(e.w, 0, lane + 1), kl = row / n_iso;
+      iso = (uint32_t)(row - kl * n_iso);
+      rid = __ldg(tl + e.x + kl);
+      lo = Rv.lo[rid];
+      hi = Rv.hi[rid];
+      const RangeInfo inf = Rv.info[rid];
+      sr = (int32_t)inf.sr;
+      const double thr = fmin(__longlong_as_double((long long)__ldcg(a.thr_g + rid)),
+                              unord_bits(__ldcg(a.best + 2 * (int64_t)rid + 1)));
+      cth = __double2float_rd(inf.V - thr - 1e-5);
+      const uint4* rrow = reinterpret_cast<const uint4*>(Rv.rows + ((int64_t)rid * n_iso + iso) * K);
+#pragma unroll
+      for (int q4 = 0; q4 < KW / 4; ++q4) {
+        const uint4 v = __ldg(rrow + q4);
+        rw[4 * q4] = v.x;
+        rw[4 * q4 + 1] = v.y;
+        rw[4 * q4 + 2] = v.z;
+        rw[4 * q4 + 3] = v.w;
+      }
+    }
+    // the chunk's columns: lane and lane + 32 (sum_d, and K den = K (K sum_dd -
+    // sum_d^2) rounded up to fp32; 0 for a flat domain)
+    uint32_t pc[2], dw[2][KW];
+    int32_t sd[2];
+    float kden[2];
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      pc[c] = e.z + (uint32_t)(lane + 32 * c);
+      sd[c] = 0;
+      kden[c] = 0.0f;
+#pragma unroll
+      for (int w = 0; w < KW; ++w) dw[c][w] = 0;
+      if ((int64_t)pc[c] < P.D) {
+        dom_words<K>(P, pc[c], pool_id(P, pc[c]), dw[c]);
+        const uint2 sm = __ldg(P.sums + pc[c]);
+        sd[c] = (int32_t)sm.x;
+        const long long den = (long long)K * sm.y - (long long)sm.x * sm.x;
+        kden[c] = __ll2float_ru((long long)K * den);
+      }
+    }
+    for (int j = 0; j < nrows; ++j) {
+      const uint32_t rj = __shfl_sync(0xffffffffu, rid, j), ij = __shfl_sync(0xffffffffu, iso, j);
+      const int32_t loj = __shfl_sync(0xffffffffu, lo, j), hij = __shfl_sync(0xffffffffu, hi, j);
+      const int32_t srj = __shfl_sync(0xffffffffu, sr, j);
+      const float cthj = __shfl_sync(0xffffffffu, cth, j);
+      uint32_t rwj[KW];
+#pragma unroll
+      for (int w = 0; w < KW; ++w) rwj[w] = __shfl_sync(0xffffffffu, rw[w], j);
+      bool pass[2];
+      uint32_t cross[2];
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        uint32_t acc = 0;
+#pragma unroll
+        for (int w = 0; w < KW; ++w) acc = __dp4a(dw[c][w], rwj[w], acc);
+        cross[c] = acc;
+        const bool in = (int32_t)pc[c] >= loj && (int32_t)pc[c] < hij;
+        // every (s, o) has error >= V - num^2 / (K den) (>= V for a flat
+        // domain): num = K cross - sum_r sum_d is an exact int32 (|num| <
+        // 2^31 for K <= 64); the fp32 comparison keeps a 2^-18 relative
+        // margin over its few roundings, so it never drops a candidate the
+        // exact bound keeps
+        const int32_t num = K * (int32_t)acc - srj * sd[c];
+        const float nf = (float)num;
+        pass[c] = in && (cthj <= 0.0f || (kden[c] > 0.0f && nf * nf >= kden[c] * cthj * (1.0f - 0x1p-18f)));
+        tests += in ? 1 : 0;
+      }
+      // queue the passing candidates (lane order), evaluate in batches of 32
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const unsigned m = __ballot_sync(0xffffffffu, pass[c]);
+        if (pass[c]) q[(tail + __popc(m & ((1u << lane) - 1u))) & (HLQ - 1)] = make_uint4(rj, pc[c], cross[c], ij);
+        tail += (uint32_t)__popc(m);
+      }
+      __syncwarp();
+      while (tail - head >= 32u) {
+        hl_flush<K>(P, Rv, a, q, head, 32, lane, evals);
+        head += 32;
+        __syncwarp();
+      }
+    }
+  }
+  if (tail != head) hl_flush<K>(P, Rv, a, q, head, (int)(tail - head), lane, evals);
+  for (int m = 16; m >= 1; m >>= 1) {
+    evals += __shfl_xor_sync(0xffffffffu, evals, m);
+    tests += __shfl_xor_sync(0xffffffffu, tests, m);
+  }
+  if (lane == 0 && evals) atomicAdd(a.counters, evals);
+  if (lane == 0 && tests) atomicAdd(a.tests, tests);
+}
+
+void launch_hl_rescore(const PoolView& P, const RangeView& Rv, const HlArgs& a, cudaStream_t s) {
+  if (!a.hl) return;
+  const unsigned grid = 148 * 8;  // grid-stride over the device-side entry count
+  if (Rv.K == 64)
+    k_hl_rescore<64><<<grid, 256, 0, s>>>(P, Rv, a);
+  else if (Rv.K == 16)
+    k_hl_rescore<16><<<grid, 256, 0, s>>>(P, Rv, a);
+  else
+    invalid("hit list supports range_size 4 and 8");
+  FIC_CHECK_LAUNCH();
+}
+
 // Generic K (any range size): rows zero-padded to KP = K rounded up to a
 // multiple of 4 on both sides, so whole-word dp4a products are exact.
 __global__ void __launch_bounds__(256) k_exact_generic(PoolView P, RangeView Rv, ExactArgs a) {

@@ -90,6 +90,7 @@ static_assert(NACC % NGRP == 0, "screening groups must own whole accumulator sta
 static_assert((BN / NSPLIT) % CH == 0 && CH % 32 == 0, "slices hold whole chunks of x32 loads");
 constexpr int QCAP = 32;      // survivor queue entries per (row, slice)
 constexpr uint32_t SLCH = 512;  // survivor-list entries per screening-warp chunk
+constexpr uint32_t HLCH = 256;  // hit-list entries per screening-warp chunk
 constexpr int PK = 8;         // pilot: |u| candidates kept per row and screening group (4x4 ranges)
 #ifndef FIC_TC_PK64
 #define FIC_TC_PK64 2         // (8x8 ranges)
@@ -422,6 +423,8 @@ __global__ void __maxnreg__(MAXREG)
   // starting at or past sl_cap ends the warp's list use (the queues take the rest)
   uint32_t sl_pos = 0, sl_end = 0;
   bool sl_dead = false;
+  uint32_t hl_pos = 0, hl_end = 0;  // hit list: the same per-warp chunks (HLCH entries)
+  bool hl_dead = false;
   long long tw0 = 0, tw1 = 0, tw2 = 0, tw3 = 0, tw4 = 0;  // stall cycles (debug & 4)
   const long long tstart = TCLK();
   unsigned long long gt_start = 0;  // debug & 8192: per-CTA start / end (globaltimer, ns)
@@ -478,7 +481,8 @@ __global__ void __maxnreg__(MAXREG)
   const int64_t n_whole = n_items - n_split;
   // pilot items (TcArgs::pilot_cols): one per tile, before everything else
   const int64_t n_pilot = a.pilot_cols > 0 ? (a.plan ? a.plan->n_tt : cdiv(n_tr, a.RT)) : 0;
-  const int64_t n_virt = n_pilot + n_whole + n_split * a.nsub;
+  // (debug & 16384: the pilot items only -- a timing split, results invalid)
+  const int64_t n_virt = (debug & 16384) ? n_pilot : n_pilot + n_whole + n_split * a.nsub;
   auto item_cols = [&](int64_t v, int& tile, int& slot, int64_t& c0, int64_t& c1) {
     if (v < n_pilot) {  // pilot: the first pilot_cols columns of tile v's window, no partial slot
       tile = (int)v;
@@ -617,7 +621,7 @@ __global__ void __maxnreg__(MAXREG)
       // TMA producer: the whole warp walks the pipeline, one lane issues
       for (int j = npre; j < nt; ++j) {
         { long long t0 = TCLK(); mbar_wait(empty_bar(stage), ph ^ 1); tw0 += TCLK() - t0; }
-        if ((debug & 32) && blockIdx.x == 0 && it == 0 && j < 64 && lane == 0) a.dbg[j * 24] = TCLK();
+        if ((debug & 32) && blockIdx.x == 0 && kitem == 1 && j < 64 && lane == 0) a.dbg[j * 24] = TCLK();
         if (elect_one()) {
           if ((debug & 16) || ((debug & 1024) && (j & 1))) {
             if (leader) mbar_arrive(full_bar(stage));
@@ -670,9 +674,10 @@ __global__ void __maxnreg__(MAXREG)
       const uint32_t full0 = full_bar(0), empty0 = empty_bar(0), tfull0 = tfull_bar(0), tempty0 = tempty_bar(0);
       for (int j = warp - MMA0; j < nt; j += NMMA) {
         { long long t0 = TCLK(); mbar_wait(tempty0 + 8 * acc, acc_ph ^ 1); tw1 += TCLK() - t0; }
+        if ((debug & 32) && blockIdx.x == 0 && kitem == 1 && j < 64 && lane == 0) a.dbg[j * 24 + 2] = TCLK();
         { long long t0 = TCLK(); mbar_wait(full0 + 8 * stage, ph); tw2 += TCLK() - t0; }
         fence_after();
-        if ((debug & 32) && blockIdx.x == 0 && it == 0 && j < 64 && lane == 0) a.dbg[j * 24 + 1] = TCLK();
+        if ((debug & 32) && blockIdx.x == 0 && kitem == 1 && j < 64 && lane == 0) a.dbg[j * 24 + 1] = TCLK();
         if (elect_one()) {
           const uint32_t d = tmem_base + acc * BN;
           const uint64_t bs = bdesc + (uint64_t)((stage * C::B_BYTES) >> 4);
@@ -824,11 +829,12 @@ __global__ void __maxnreg__(MAXREG)
       volatile uint32_t* myhead = qhead + row * NSLICE + qsl;
       uint32_t qt = 0;
       unsigned long long thr_bits = 0x7ff0000000000000ull;
-      float s_r = -1.0f;  // |u| threshold; negative = every candidate survives
+      float s_r = (debug & 128) ? INFINITY : -1.0f;  // |u| threshold; negative = every candidate survives
       auto set_threshold = [&](unsigned long long tb) {
         thr_bits = tb;
         const double cth = V - __longlong_as_double((long long)tb) - 1e-5;
         s_r = (cth > 0.0) ? __double2float_rd(sqrt(cth) * (1.0 - 1e-9) - eps) : -1.0f;
+        if (debug & 128) s_r = INFINITY;  // timing: the max computed, no chunk ever hits (results invalid)
       };
       auto push = [&](uint32_t rel) {
         while (qt - *myhead >= (uint32_t)QCAP) __nanosleep(32);
@@ -841,7 +847,7 @@ __global__ void __maxnreg__(MAXREG)
         const uint32_t gj = gt + (uint32_t)j;
         const int acc = (int)(gj % NACC), acc_ph = (int)((gj / NACC) & 1);
         { long long t0 = TCLK(); mbar_wait_sleep(tfull0 + 8 * acc, acc_ph); tw3 += TCLK() - t0; }
-        const bool dbgw = (debug & 32) && blockIdx.x == 0 && it == 0 && j < 64 && lane == 0 && warp == SCR0;
+        const bool dbgw = (debug & 32) && blockIdx.x == 0 && kitem == 1 && j < 64 && lane == 0 && (warp == SCR0 || warp == SCR0 + 4);
         if (dbgw) a.dbg[j * 24 + 4] = TCLK();
         fence_after();
         if (!(debug & 4096)) {  // thresholds published by the rescorers
@@ -934,6 +940,46 @@ __global__ void __maxnreg__(MAXREG)
           }
           tw4 += TCLK() - ts0;
         };
+        // hit list: one entry for the warp's hit rows of this chunk (no
+        // per-row masks, no seeding: rows without a threshold take slow_path)
+        // a slot for one entry in the warp's chunk (refilled when used up)
+        auto hl_reserve = [&]() -> bool {
+          if (hl_dead) return false;
+          if (hl_pos == hl_end) {  // warp-uniform
+            uint32_t nb = 0;
+            if (lane == 0) nb = atomicAdd(a.hl_count, HLCH);
+            nb = __shfl_sync(0xffffffffu, nb, 0);
+            hl_pos = nb;
+            hl_end = nb + HLCH;
+          }
+          if (hl_pos >= a.hl_cap) {
+            hl_dead = true;
+            return false;
+          }
+          return true;
+        };
+        auto hl_write = [&](int32_t rel, unsigned bal) {  // into the reserved slot
+          if (lane == 0)
+            a.hl[hl_pos] = make_uint4((uint32_t)((int64_t)tile * a.RT), (uint32_t)(32 * (warp & 3) + rbase),
+                                      (uint32_t)(c0 + rel), bal);
+          ++hl_pos;
+        };
+        // the warp's rows can go to the hit list (no row still needs a seed)
+        auto hl_ok = [&](bool hit) {
+          return K == 16 && FIC_TC_SL && a.hl && list_all &&
+                 !__any_sync(0xffffffffu, hit && thr_bits == 0x7ff0000000000000ull);
+        };
+        auto hl_append = [&](int32_t rel, bool hit) -> bool {
+          const unsigned bal = __ballot_sync(0xffffffffu, hit);
+          if (!hl_reserve()) return false;
+          hl_write(rel, bal);
+          return true;
+        };
+        auto on_hit = [&](const float* v, int32_t rel, int32_t e_lo, int32_t e_hi, bool hit) {
+          // (4x4 ranges only: the 8x8 screeners keep their registers)
+          if (hl_ok(hit) && hl_append(rel, hit)) return;
+          slow_path(v, rel, e_lo, e_hi, hit);
+        };
         // |u| max of CH values: four FMNMX3 chains
         auto chunk_max = [&](const float* v) {
           float m0 = fmaxf(fmaxf(fabsf(v[0]), fabsf(v[1])), fabsf(v[2]));
@@ -979,7 +1025,7 @@ __global__ void __maxnreg__(MAXREG)
             const int32_t rel = j * BN + slice * SW + CH * h;
             const int32_t e_lo = lo32 - rel, e_hi = hi32 - rel;
             const bool hit = !(debug & 8) & rvalid & !rflat & (e_lo < CH) & (e_hi > 0) & (mx[h] >= s_r);
-            if (__any_sync(0xffffffffu, hit)) slow_path(v + CH * h, rel, e_lo, e_hi, hit);
+            if (__any_sync(0xffffffffu, hit)) on_hit(v + CH * h, rel, e_lo, e_hi, hit);
           }
         } else {
 #pragma unroll
@@ -991,6 +1037,7 @@ __global__ void __maxnreg__(MAXREG)
                 tmem_ld32(lane_base + acc * BN + slice * SW + CH * h + 32 * c, v + 32 * c);
             }
             tmem_wait_ld();
+            if (dbgw) a.dbg[j * 24 + 5 + h] = TCLK();
             if (h == SW / CH - 1) release();  // release the stage before screening its last chunk
             if (debug & 1) continue;
             const int32_t rel = j * BN + slice * SW + CH * h;  // chunk start, relative to c0
@@ -1000,7 +1047,7 @@ __global__ void __maxnreg__(MAXREG)
             // [rel, rel + CH) meets [lo32, hi32) (hi32 > lo32 when valid): one unsigned compare
             const bool in_window = (uint32_t)(e_hi - 1) < (uint32_t)(hi32 - lo32 + CH - 1);
             const bool hit = !(debug & 8) & in_window & !rflat & (mx >= s_r);
-            if (__any_sync(0xffffffffu, hit)) slow_path(v, rel, e_lo, e_hi, hit);
+            if (__any_sync(0xffffffffu, hit)) on_hit(v, rel, e_lo, e_hi, hit);
           }
         }
       }
@@ -1282,6 +1329,9 @@ __global__ void __maxnreg__(MAXREG)
 
   if (FIC_TC_SL && is_scr && a.sl) {  // unused tail of the warp's chunk: empty entries
     for (uint32_t i = sl_pos + lane; i < min(sl_end, a.sl_cap); i += 32) a.sl[i] = make_uint4(0, 0, 0, 0);
+  }
+  if (K == 16 && FIC_TC_SL && is_scr && a.hl) {
+    for (uint32_t i = hl_pos + lane; i < min(hl_end, a.hl_cap); i += 32) a.hl[i] = make_uint4(0, 0, 0, 0);
   }
   if (is_res || is_scr) {
     for (int m = 16; m >= 1; m >>= 1) evals += __shfl_xor_sync(0xffffffffu, evals, m);

@@ -160,6 +160,15 @@ struct TcArgs {
   int pilot_stride;            // pilot items sample every pilot_stride-th 128-column tile (>= 1)
   int sl_all;                  // 1: every survivor goes to the list (the queues carry seeds only);
                                // 2: the same after each tile's first segment (a pilot with the queues)
+  // Hit list (with sl_all == 1): a screening warp whose chunk has any lane
+  // with max |u| over the row's threshold writes ONE 16-byte entry (tlist
+  // index of the tile's first range, first row of the warp, pool column of
+  // the chunk, 32-bit ballot of the hit rows) instead of building per-row
+  // survivor masks; k_hl_rescore filters those chunks with the exact
+  // integer lower bound and evaluates the rest.  nullptr = off.
+  uint4* hl;
+  uint32_t* hl_count;          // [1] entries handed out in per-warp chunks (tails: empty entries)
+  uint32_t hl_cap;
 };
 
 // Rescoring of the survivor list: every candidate of every entry, exactly;
@@ -175,6 +184,25 @@ struct SlArgs {
   unsigned long long* counters;  // [0] exact evaluations
 };
 void launch_sl_rescore(const PoolView& P, const RangeView& Rv, const SlArgs& a, cudaStream_t s);
+
+// Rescoring of the hit list (TcArgs::hl): one warp per entry, two chunk
+// columns per lane; for every hit row, each column of the row's slab whose
+// exact lower bound V - num^2 / (K den) (num = K cross - sum_r sum_d, den =
+// K sum_dd - sum_d^2, integers) can reach the range's threshold is evaluated
+// with eval_candidate into the survivor list's best / pre arrays.
+struct HlArgs {
+  const uint4* hl;
+  const uint32_t* hl_count;
+  uint32_t hl_cap;
+  const uint32_t* tlist;       // the tensor matcher's tlist (plan offset applied here)
+  const DevPlan* plan;
+  const unsigned long long* thr_g;  // [R] thresholds from the matcher (double bits)
+  unsigned long long* best;    // [R][2] (SlArgs::best)
+  unsigned long long* pre;     // [R]
+  unsigned long long* counters;  // [0] exact evaluations
+  unsigned long long* tests;     // [1] lower-bound tests
+};
+void launch_hl_rescore(const PoolView& P, const RangeView& Rv, const HlArgs& a, cudaStream_t s);
 
 
 

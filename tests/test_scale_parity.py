@@ -189,9 +189,23 @@ def test_cfg4_exhaustive_queue_path_matches_reference(monkeypatch):
     assert res.stats["sl_entries"] == 0
 
 
-def test_cfg4_default_uses_pilot_and_survivor_list():
+def test_cfg4_default_uses_pilot_and_hit_list():
     import torch
     g = _golden("scale_cfg4.npz")
     strategy, kw = _kw(g, "cfg4_ex")
     res = codec.encode_device(torch.from_numpy(g["cfg4_ex.image"]).cuda(), strategy, **kw)
-    assert res.stats["sl_entries"] > 0
+    assert res.stats["hl_entries"] > 0 and res.stats["hl_tests"] > 0
+
+
+@pytest.mark.parametrize("env", [{"FIC_HL": "0"}, {"FIC_HL_CAP": "5000"}, {"FIC_HL_CAP": "1"}])
+def test_cfg4_hit_list_variants_match_reference(env, monkeypatch):
+    """cfg4 with the hit list off (per-row survivor masks to the survivor
+    list), and with a hit list that overflows (the rest of the hit chunks
+    take the survivor-mask path): bit-exact on every range."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    _, res = _check_full("scale_cfg4.npz", "cfg4_ex")
+    if env.get("FIC_HL") == "0":
+        assert res.stats["hl_entries"] == 0 and res.stats["sl_entries"] > 0
+    else:
+        assert res.stats["hl_entries"] <= int(env["FIC_HL_CAP"]) and res.stats["sl_entries"] > 0

@@ -21,6 +21,6 @@ for i in range(reps):
     torch.cuda.synchronize()
     st = res.stats
     keys = ("ms_total", "ms_fd", "ms_pool", "ms_tensor", "ms_sl", "ms_exact", "exact_evals",
-            "sl_entries", "comparisons", "work_items")
+            "sl_entries", "hl_entries", "hl_tests", "comparisons", "work_items")
     print({k: st[k] for k in keys}, "matches/s %.3g" % (st["comparisons"] / st["ms_total"] * 1e3),
           flush=True)
