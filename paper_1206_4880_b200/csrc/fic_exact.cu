@@ -301,6 +301,7 @@ __global__ void __launch_bounds__(256, 3) k_hl_rescore(PoolView P, RangeView Rv,
   const int64_t n = (int64_t)min(*a.hl_count, a.hl_cap);
   const int64_t warp0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int iso_sh = Rv.n_iso == 8 ? 3 : 0;  // n_iso is 8 or 1 (launch_hl_rescore checks)
   const int n_iso = Rv.n_iso;
   const uint32_t* tl = a.tlist + (a.plan ? a.plan->tb : 0);
   unsigned long long evals = 0, tests = 0;
@@ -309,17 +310,17 @@ __global__ void __launch_bounds__(256, 3) k_hl_rescore(PoolView P, RangeView Rv,
     const uint4 e = en;
     if (i + nwarps < n) en = a.hl[i + nwarps];
     if (e.w == 0) continue;
-    // this lane's hit row (lane < popc): range id, isometry, slab, sum_r, bound, pixels
-    const int nrows = __popc(e.w);
+    // lane L with bit L of the ballot loads row e.y + L: range id, isometry,
+    // slab, sum_r, bound, pixels (n_iso is 1 or 8: a shift)
     uint32_t rid = 0, iso = 0;
     int32_t lo = 0, hi = 0, sr = 0;
     float cth = -1.0f;  // V - threshold - margin, rounded down (<= 0: no bound)
     uint32_t rw[KW];
 #pragma unroll
     for (int w = 0; w < KW; ++w) rw[w] = 0;
-    if (lane < nrows) {
-      const int row = (int)e.y + (int)__fns(e.w, 0, lane + 1), kl = row / n_iso;
-      iso = (uint32_t)(row - kl * n_iso);
+    if ((e.w >> lane) & 1u) {
+      const int row = (int)e.y + lane, kl = row >> iso_sh;
+      iso = (uint32_t)(row - (kl << iso_sh));
       rid = __ldg(tl + e.x + kl);
       lo = Rv.lo[rid];
       hi = Rv.hi[rid];
@@ -354,11 +355,16 @@ __global__ void __launch_bounds__(256, 3) k_hl_rescore(PoolView P, RangeView Rv,
         dom_words<K>(P, pc[c], pool_id(P, pc[c]), dw[c]);
         const uint2 sm = __ldg(P.sums + pc[c]);
         sd[c] = (int32_t)sm.x;
-        const long long den = (long long)K * sm.y - (long long)sm.x * sm.x;
-        kden[c] = __ll2float_ru((long long)K * den);
+        if (K == 16) {  // K sum_dd, sum_d^2 < 2^31: int32, then K den in fp32 (2^-24 rounding)
+          kden[c] = (float)K * (float)((int32_t)(K * sm.y) - (int32_t)(sm.x * sm.x));
+        } else {
+          const long long den = (long long)K * sm.y - (long long)sm.x * sm.x;
+          kden[c] = __ll2float_rn((long long)K * den);
+        }
       }
     }
-    for (int j = 0; j < nrows; ++j) {
+    for (unsigned bal = e.w; bal; bal &= bal - 1) {
+      const int j = __ffs(bal) - 1;  // the row's lane
       const uint32_t rj = __shfl_sync(0xffffffffu, rid, j), ij = __shfl_sync(0xffffffffu, iso, j);
       const int32_t loj = __shfl_sync(0xffffffffu, lo, j), hij = __shfl_sync(0xffffffffu, hi, j);
       const int32_t srj = __shfl_sync(0xffffffffu, sr, j);
@@ -411,6 +417,7 @@ __global__ void __launch_bounds__(256, 3) k_hl_rescore(PoolView P, RangeView Rv,
 
 void launch_hl_rescore(const PoolView& P, const RangeView& Rv, const HlArgs& a, cudaStream_t s) {
   if (!a.hl) return;
+  if (Rv.n_iso != 8 && Rv.n_iso != 1) invalid("hit list needs 1 or 8 isometries");
   const unsigned grid = 148 * 8;  // grid-stride over the device-side entry count
   if (Rv.K == 64)
     k_hl_rescore<64><<<grid, 256, 0, s>>>(P, Rv, a);
