@@ -315,7 +315,27 @@ def _k1_traffic():
         return {}
 
 
-def _pool_roofline(stats, peak_gbs, src, serial_stats=None, H=1024, W=1024, D=1009 * 1009, K=64):
+def _write_stream_gbs(nbytes=1 << 30, reps=5):
+    """Measured HBM write-stream bandwidth on this device: torch fill_ of a
+    1 GiB buffer (8x L2), best of `reps` (CUDA events).  K1 is ~99% writes
+    by SURVEY 8(d)'s byte count, and a pure write stream runs far below the
+    copy figure in MEASURED_PEAKS.json (B200: ~3.9 vs 6.55 TB/s)."""
+    import torch
+    buf = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    best = float("inf")
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        buf.fill_(1)
+        e1.record()
+        torch.cuda.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    del buf
+    return nbytes / (best / 1e3) / 1e9
+
+
+def _pool_roofline(stats, peak_gbs, src, serial_stats=None, H=1024, W=1024, D=1009 * 1009, K=64,
+                   write_gbs=None):
     """HBM roofline of the pool builder K1 on SURVEY §8(d)'s algorithmic
     bytes: H*W image bytes read + D*(2K + 16) written (fp16 B row, sum_d and
     sum_dd u32, inv_den f64) = 147.6 MB at cfg3.  Reported for the main
@@ -338,6 +358,17 @@ def _pool_roofline(stats, peak_gbs, src, serial_stats=None, H=1024, W=1024, D=10
            "k1_stage": {"kernels": "k_domrows + k_pool", "ms": ms_k1, "achieved": g_k1,
                         "frac": g_k1 / peak_gbs,
                         "traffic": (tr["k_pool"] + tr["k_domrows"]) if "k_domrows" in tr else None}}
+    if write_gbs:
+        # the same kernel against the measured write-stream rate (its bytes
+        # are H*W reads + D*(2K+16) writes: the writes bound it)
+        wb = D * (2 * K + 16)
+        out["write_stream"] = {"peak": write_gbs, "unit": "GB/s",
+                               "peak_source": "measured in this run: torch fill_ of 1 GiB, best of 5",
+                               "achieved_write": wb / (ms / 1e3) / 1e9 if ms > 0 else 0.0,
+                               "frac": (wb / (ms / 1e3) / 1e9) / write_gbs if ms > 0 else 0.0,
+                               "note": "cfg3 writes 147 MB, partly absorbed by the 126 MB L2 inside the "
+                                       "kernel's window (frac can exceed 1); cfg5's 2.4 GB is not: "
+                                       "profiles/r02b_k1.jsonl"}
     if serial_stats:
         ms_s = float(np.median([s["ms_pool_main"] for s in serial_stats]))
         ms_s1 = float(np.median([s["ms_pool"] for s in serial_stats]))
@@ -478,6 +509,7 @@ def run_ours(args):
             dist.destroy_process_group()
         return
     peak_tf, peak_gbs, src = _peaks()
+    write_gbs = _write_stream_gbs()
     # N GPUs: the shards' useful flops over the slowest rank's matcher time,
     # against N x the single-GPU peak
     peak_tf_all = peak_tf * world
@@ -494,7 +526,7 @@ def run_ours(args):
                      "frac": achieved / peak_tf_all, "peak_source": f"{src} bf16 dense burst "
                      f"(fp16 same rate) x {world} GPU", "algorithmic_flops_per_launch": 2 * 64 * tcomp,
                      "ms_per_launch": ms_t, "traffic": _traffic_from_profile()},
-        "roofline_hbm": _pool_roofline(stats, peak_gbs, src, serial_stats),
+        "roofline_hbm": _pool_roofline(stats, peak_gbs, src, serial_stats, write_gbs=write_gbs),
         "e2e": {"value": comps / e2e_s, "unit": UNIT, "encode_ms": 1e3 * e2e_s,
                 "h2d_bytes_per_step": int(img.nbytes),
                 "d2h_bytes_per_step": n_r * (7 + 8 + 8 + 8)},

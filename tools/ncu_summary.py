@@ -78,7 +78,7 @@ def main():
             if k in d:
                 lines.append(f"| {k} | {d[k][0]} | {d[k][1]} |")
         lines.append("")
-        if "k_match_tc" in name and "dram__bytes_read.sum" in d:
+        if "k_match_tc" in name and "dram__bytes_read.sum" in d and "cfg3" in os.path.basename(rep):
             def to_bytes(v, u):
                 v = float(v.replace(",", ""))
                 return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)

@@ -13,6 +13,8 @@ os.environ["FIC_POOL_SERIAL"] = "1"
 from paper_1206_4880_b200 import codec, synth  # noqa: E402
 
 peak = json.load(open("MEASURED_PEAKS.json"))["hbm_gbs"] if os.path.exists("MEASURED_PEAKS.json") else 6552.3
+import bench  # noqa: E402
+wpeak = bench._write_stream_gbs()
 for name in sys.argv[1:] or ["cfg3"]:
     c = synth.CONFIGS[name]
     img = torch.from_numpy(c.make()).cuda()
@@ -27,4 +29,7 @@ for name in sys.argv[1:] or ["cfg3"]:
     nbytes = img.numel() + D * (2 * K + 16)
     print(json.dumps({"config": name, "bytes": nbytes, "k_pool_ms": mm, "k1_ms": m1,
                       "k_pool_frac": nbytes / (mm * 1e-3) / 1e9 / peak,
-                      "k1_frac": nbytes / (m1 * 1e-3) / 1e9 / peak}), flush=True)
+                      "k1_frac": nbytes / (m1 * 1e-3) / 1e9 / peak,
+                      "write_stream_gbs": wpeak,
+                      "k_pool_frac_of_write_stream": D * (2 * K + 16) / (mm * 1e-3) / 1e9 / wpeak}),
+          flush=True)
