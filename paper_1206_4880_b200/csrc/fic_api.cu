@@ -1122,7 +1122,7 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
     double scal[4];
     DevPlan plan;
     unsigned long long flat[2];  // [0] flat count, [1] low word: canonical flat range
-    uint32_t sl_count[2];        // [0] survivor-list entries appended, [1] hit-list entries
+    uint32_t sl_count[4];        // [0] survivor-list entries appended, [1] hit-list entries, [2] sorted
     unsigned long long hl_tests;  // hit-list lower-bound tests
   };
   Readback* d_rb = sc.get<Readback>(1);
@@ -1391,6 +1391,11 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
         hla.pre = sla.pre;
         hla.counters = counters;
         hla.tests = &d_rb->hl_tests;
+        if (!getenv("FIC_HL_SORT") || atoi(getenv("FIC_HL_SORT")) != 0) {
+          hla.sorted = sc.get<uint4>(ta.hl_cap);
+          hla.n_sorted = d_rb->sl_count + 2;
+          hla.bins = sc.get<uint32_t>((size_t)(g.D + 63) / 64 + 2);
+        }
       }
     }
     const char* dbg_env = getenv("FIC_TC_DEBUG");
@@ -1436,6 +1441,7 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
   }
   FIC_CUDA(cudaEventRecord(tm.ev[21], s));
   launch_sl_rescore(P, Rv, sla, s);
+  launch_hl_sort(hla, g.D, s);
   launch_hl_rescore(P, Rv, hla, s);
   FIC_CUDA(cudaEventRecord(tm.ev[22], s));
   tm.mark();  // 4

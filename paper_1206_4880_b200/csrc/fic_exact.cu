@@ -254,6 +254,9 @@ void launch_sl_rescore(const PoolView& P, const RangeView& Rv, const SlArgs& a, 
 // queue in shared memory that is evaluated 32 at a time with all lanes
 // (codec.py:218-258 via eval_candidate), publishing to the survivor list's
 // best / pre arrays only when a candidate beats what they hold.
+#ifndef FIC_HL_BLK
+#define FIC_HL_BLK 3  // resident blocks per SM (register budget) of k_hl_rescore
+#endif
 namespace {
 constexpr int HLQ = 128;  // queue slots per warp (< 32 queued + 64 of one row)
 }
@@ -292,23 +295,39 @@ __device__ __forceinline__ void hl_flush(const PoolView& P, const RangeView& Rv,
 }
 
 template <int K>
-__global__ void __launch_bounds__(256, 3) k_hl_rescore(PoolView P, RangeView Rv, HlArgs a) {
+__global__ void __launch_bounds__(256, FIC_HL_BLK) k_hl_rescore(PoolView P, RangeView Rv, HlArgs a) {
   constexpr int KW = K / 4;
   __shared__ uint4 s_q[8][HLQ];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   uint4* q = s_q[wib];
   uint32_t head = 0, tail = 0;  // queue (warp-uniform counters)
-  const int64_t n = (int64_t)min(*a.hl_count, a.hl_cap);
   const int64_t warp0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  // sorted by chunk column (k_hl_sort): each warp takes a contiguous run and
+  // loads a chunk's columns once for all its entries; else a grid stride
+  const uint4* L = a.sorted ? a.sorted : a.hl;
+  const int64_t n = a.sorted ? (int64_t)*a.n_sorted : (int64_t)min(*a.hl_count, a.hl_cap);
+  int64_t i0 = warp0, i1 = n, step = nwarps;
+  if (a.sorted) {
+    const int64_t run = (n + nwarps - 1) / nwarps;
+    i0 = min(n, warp0 * run);
+    i1 = min(n, i0 + run);
+    step = 1;
+  }
   const int iso_sh = Rv.n_iso == 8 ? 3 : 0;  // n_iso is 8 or 1 (launch_hl_rescore checks)
   const int n_iso = Rv.n_iso;
   const uint32_t* tl = a.tlist + (a.plan ? a.plan->tb : 0);
   unsigned long long evals = 0, tests = 0;
-  uint4 en = warp0 < n ? a.hl[warp0] : make_uint4(0, 0, 0, 0);  // next entry (prefetched)
-  for (int64_t i = warp0; i < n; i += nwarps) {
+  // the current chunk's columns: lane and lane + 32 (sum_d, and K den = K (K
+  // sum_dd - sum_d^2) in fp32; 0 for a flat domain)
+  uint32_t cur_z = 0xffffffffu;
+  uint32_t pc[2], dw[2][KW];
+  int32_t sd[2];
+  float kden[2];
+  uint4 en = i0 < i1 ? L[i0] : make_uint4(0, 0, 0, 0);  // next entry (prefetched)
+  for (int64_t i = i0; i < i1; i += step) {
     const uint4 e = en;
-    if (i + nwarps < n) en = a.hl[i + nwarps];
+    if (i + step < i1) en = L[i + step];
     if (e.w == 0) continue;
     // lane L with bit L of the ballot loads row e.y + L: range id, isometry,
     // slab, sum_r, bound, pixels (n_iso is 1 or 8: a shift)
@@ -339,11 +358,8 @@ __global__ void __launch_bounds__(256, 3) k_hl_rescore(PoolView P, RangeView Rv,
         rw[4 * q4 + 3] = v.w;
       }
     }
-    // the chunk's columns: lane and lane + 32 (sum_d, and K den = K (K sum_dd -
-    // sum_d^2) rounded up to fp32; 0 for a flat domain)
-    uint32_t pc[2], dw[2][KW];
-    int32_t sd[2];
-    float kden[2];
+    if (e.z != cur_z) {  // warp-uniform
+    cur_z = e.z;
 #pragma unroll
     for (int c = 0; c < 2; ++c) {
       pc[c] = e.z + (uint32_t)(lane + 32 * c);
@@ -362,6 +378,7 @@ __global__ void __launch_bounds__(256, 3) k_hl_rescore(PoolView P, RangeView Rv,
           kden[c] = __ll2float_rn((long long)K * den);
         }
       }
+    }
     }
     for (unsigned bal = e.w; bal; bal &= bal - 1) {
       const int j = __ffs(bal) - 1;  // the row's lane
@@ -413,6 +430,74 @@ __global__ void __launch_bounds__(256, 3) k_hl_rescore(PoolView P, RangeView Rv,
   }
   if (lane == 0 && evals) atomicAdd(a.counters, evals);
   if (lane == 0 && tests) atomicAdd(a.tests, tests);
+}
+
+// Counting sort of the hit list by chunk column (bin = column / 64), so
+// k_hl_rescore can load a chunk's column data once for all of its entries
+// (cfg4: ~2,600 entries per chunk from 4,096 tiles).  Order inside a bin is
+// arbitrary: the per-range lexicographic minimum does not depend on it.
+__global__ void k_hl_hist(const uint4* hl, const uint32_t* cnt, uint32_t cap, uint32_t* hist) {
+  const int64_t n = (int64_t)min(*cnt, cap);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint4 e = hl[i];
+    if (e.w) atomicAdd(hist + (e.z >> 6), 1u);
+  }
+}
+
+// exclusive scan of nbins counts in place (one block), total to *total
+__global__ void __launch_bounds__(1024) k_hl_scan(uint32_t* hist, int nbins, uint32_t* total) {
+  __shared__ uint32_t s_w[32];
+  const int t = threadIdx.x, per = (nbins + 1023) / 1024;
+  const int b0 = min(nbins, t * per), b1 = min(nbins, b0 + per);
+  uint32_t sum = 0;
+  for (int b = b0; b < b1; ++b) sum += hist[b];
+  uint32_t incl = sum;
+  const int lane = t & 31, w = t >> 5;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t v = __shfl_up_sync(0xffffffffu, incl, d);
+    if (lane >= d) incl += v;
+  }
+  if (lane == 31) s_w[w] = incl;
+  __syncthreads();
+  if (w == 0) {
+    uint32_t x = s_w[lane];
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t v = __shfl_up_sync(0xffffffffu, x, d);
+      if (lane >= d) x += v;
+    }
+    s_w[lane] = x;
+  }
+  __syncthreads();
+  uint32_t run = incl - sum + (w ? s_w[w - 1] : 0u);
+  for (int b = b0; b < b1; ++b) {
+    const uint32_t c = hist[b];
+    hist[b] = run;
+    run += c;
+  }
+  if (t == 1023) *total = run;
+}
+
+__global__ void k_hl_scatter(const uint4* hl, const uint32_t* cnt, uint32_t cap, uint32_t* cursor,
+                             uint4* out) {
+  const int64_t n = (int64_t)min(*cnt, cap);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint4 e = hl[i];
+    if (e.w) out[atomicAdd(cursor + (e.z >> 6), 1u)] = e;
+  }
+}
+
+void launch_hl_sort(const HlArgs& a, int64_t D, cudaStream_t s) {
+  if (!a.hl || !a.sorted) return;
+  const int nbins = (int)((D + 63) / 64) + 1;
+  FIC_CUDA(cudaMemsetAsync(a.bins, 0, (size_t)nbins * sizeof(uint32_t), s));
+  k_hl_hist<<<148 * 8, 256, 0, s>>>(a.hl, a.hl_count, a.hl_cap, a.bins);
+  FIC_CHECK_LAUNCH();
+  k_hl_scan<<<1, 1024, 0, s>>>(a.bins, nbins, const_cast<uint32_t*>(a.n_sorted));
+  FIC_CHECK_LAUNCH();
+  k_hl_scatter<<<148 * 8, 256, 0, s>>>(a.hl, a.hl_count, a.hl_cap, a.bins, const_cast<uint4*>(a.sorted));
+  FIC_CHECK_LAUNCH();
 }
 
 void launch_hl_rescore(const PoolView& P, const RangeView& Rv, const HlArgs& a, cudaStream_t s) {

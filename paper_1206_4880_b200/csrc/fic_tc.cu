@@ -127,7 +127,14 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
 
 // blocking wait with a suspend-time hint: the warp sleeps in the barrier
 // instead of spinning through the issue slots
+#ifndef FIC_TC_SLEEP
+#define FIC_TC_SLEEP 0  // 1: the screeners wait on accumulator-full with a suspend-time hint (measured: no gain)
+#endif
 __device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity) {
+  if (!FIC_TC_SLEEP) {
+    mbar_wait(bar, parity);
+    return;
+  }
   uint32_t ok = 0;
   do {
     asm volatile(

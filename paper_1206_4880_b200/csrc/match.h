@@ -201,7 +201,12 @@ struct HlArgs {
   unsigned long long* pre;     // [R]
   unsigned long long* counters;  // [0] exact evaluations
   unsigned long long* tests;     // [1] lower-bound tests
+  // sorted copy (launch_hl_sort; nullptr: read the list as written)
+  const uint4* sorted;         // [hl_cap] entries ordered by chunk column / 64
+  const uint32_t* n_sorted;    // [1] entries in `sorted`
+  uint32_t* bins;              // [D / 64 + 2] histogram -> cursors
 };
+void launch_hl_sort(const HlArgs& a, int64_t D, cudaStream_t s);
 void launch_hl_rescore(const PoolView& P, const RangeView& Rv, const HlArgs& a, cudaStream_t s);
 
 
