@@ -290,6 +290,27 @@ __device__ __forceinline__ void tmem_wait_ld() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// pilot key of column Q: |u| with Q in the low 6 mantissa bits, one LOP3
+// ((v & km) | Q with km = 0x7FFFFFC0 in a register, Q an immediate)
+template <int Q>
+__device__ __forceinline__ float pilot_key(float v, uint32_t km) {
+  uint32_t d;
+  asm("lop3.b32 %0, %1, %2, %3, 0xEC;" : "=r"(d) : "r"(__float_as_uint(v)), "n"(Q), "r"(km));
+  return __uint_as_float(d);
+}
+// the largest key of a 64-column chunk: four FMNMX3 chains (Q = 0, 8, .., 56)
+template <int Q>
+__device__ __forceinline__ void pilot_max(const float* v, uint32_t km, float& m0, float& m1, float& m2,
+                                          float& m3) {
+  if constexpr (Q < 64) {
+    m0 = fmaxf(fmaxf(m0, pilot_key<Q>(v[Q], km)), pilot_key<Q + 1>(v[Q + 1], km));
+    m1 = fmaxf(fmaxf(m1, pilot_key<Q + 2>(v[Q + 2], km)), pilot_key<Q + 3>(v[Q + 3], km));
+    m2 = fmaxf(fmaxf(m2, pilot_key<Q + 4>(v[Q + 4], km)), pilot_key<Q + 5>(v[Q + 5], km));
+    m3 = fmaxf(fmaxf(m3, pilot_key<Q + 6>(v[Q + 6], km)), pilot_key<Q + 7>(v[Q + 7], km));
+    pilot_max<Q + 8>(v, km, m0, m1, m2, m3);
+  }
+}
+
 template <int K, int CG>
 struct Cfg {
   static constexpr int ROWB = K * 2;                  // bytes per fp16 row
@@ -711,12 +732,14 @@ __global__ void __maxnreg__(MAXREG)
       // items (thr_g).
       float lv[PKK];
       uint32_t lp[PKK];
+      // free entries hold distinct negative sentinels, so "the entries equal
+      // to the smallest" is one entry while the list fills
 #pragma unroll
       for (int k = 0; k < PKK; ++k) {
-        lv[k] = -1.0f;
+        lv[k] = -1.0f - (float)k;
         lp[k] = 0;
       }
-      float kth = -1.0f;  // smallest |u| in the list (-1 while it has free entries)
+      float kth = -(float)PKK;  // smallest key in the list (negative while it has free entries)
       const uint32_t lane_base = tmem_base + ((uint32_t)(32 * (warp & 3)) << 16);
       const uint32_t tfull0 = tfull_bar(0), tempty0 = tempty_bar(0);
       const int32_t lo32 = rvalid ? (int32_t)(max((int64_t)rlo, c0) - c0) : 0;
@@ -726,6 +749,8 @@ __global__ void __maxnreg__(MAXREG)
         const int acc = (int)(gj % NACC), acc_ph = (int)((gj / NACC) & 1);
         mbar_wait_sleep(tfull0 + 8 * acc, acc_ph);
         fence_after();
+        float mxh[SW / CH];   // each chunk's key (-inf: no column of the row's slab)
+        int32_t relh[SW / CH];
 #pragma unroll
         for (int h = 0; h < SW / CH; ++h) {
           float v[CH];
@@ -749,10 +774,17 @@ __global__ void __maxnreg__(MAXREG)
           // the whole chunk, masked only for chunks cut by a slab edge.
           static_assert(CH == 64, "the pilot key holds a 6-bit column index");
           const uint32_t km = 0x7FFFFFC0u;
-          auto key = [&](int q) { return __uint_as_float((__float_as_uint(v[q]) & km) | (uint32_t)q); };
+          // (debug & 512: plain |u|, a timing split)
+          auto key = [&](int q) {
+            return (debug & 512) ? fabsf(v[q]) : __uint_as_float((__float_as_uint(v[q]) & km) | (uint32_t)q);
+          };
           float mx;
           const bool whole = e_lo <= 0 && e_hi >= CH;
-          if (whole) {
+          if (whole && !(debug & 512)) {
+            float m0 = 0.0f, m1 = 0.0f, m2 = 0.0f, m3 = 0.0f;
+            pilot_max<0>(v, km, m0, m1, m2, m3);
+            mx = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3));
+          } else if (whole) {
             float m0 = 0.0f, m1 = 0.0f, m2 = 0.0f, m3 = 0.0f;
 #pragma unroll
             for (int q = 0; q < CH; q += 8) {
@@ -767,24 +799,45 @@ __global__ void __maxnreg__(MAXREG)
 #pragma unroll
             for (int q = 0; q < CH; ++q) mx = fmaxf(mx, (q >= e_lo && q < e_hi) ? key(q) : -1.0f);
           }
-          // keep the PKK largest chunk maxima (one candidate per chunk): the
-          // insertion is rare once the list holds large values
-          if (in_window && !rflat && mx > kth) {
-            const int idx = (int)(__float_as_uint(mx) & 63u);
-            // replace the smallest entry (the first one equal to kth), new smallest
-            bool done = false;
+          mxh[h] = (in_window && !rflat) ? mx : -INFINITY;
+          relh[h] = rel;
+        }
+        // keep the PKK largest chunk maxima (one candidate per chunk), after
+        // the stage is released: replace the first entry equal to the
+        // smallest (a bitmask and its lowest bit: independent selects, no
+        // chain; equal keys are common in smooth regions), new smallest by a
+        // min tree
+#pragma unroll
+        for (int h = 0; h < SW / CH; ++h) {
+          const float mx = mxh[h];
+          if (!(debug & 256) && mx > kth) {  // (debug & 256: no insertion, timing)
+            const uint32_t pos = (uint32_t)(relh[h] + (int)(__float_as_uint(mx) & 63u));
+            uint32_t eq = 0;
+#pragma unroll
+            for (int kk = 0; kk < PKK; ++kk) eq |= (lv[kk] == kth) ? (1u << kk) : 0u;
+            eq &= 0u - eq;
 #pragma unroll
             for (int kk = 0; kk < PKK; ++kk) {
-              const bool hitk = !done && lv[kk] == kth;
+              const bool hitk = (eq >> kk) & 1u;
               lv[kk] = hitk ? mx : lv[kk];
-              lp[kk] = hitk ? (uint32_t)(rel + idx) : lp[kk];
-              done = done || hitk;
+              lp[kk] = hitk ? pos : lp[kk];
             }
-            float nk = lv[0];
+            float t[PKK];
 #pragma unroll
-            for (int kk = 1; kk < PKK; ++kk) nk = fminf(nk, lv[kk]);
-            kth = nk;
+            for (int kk = 0; kk < PKK; ++kk) t[kk] = lv[kk];
+#pragma unroll
+            for (int w = PKK / 2; w >= 1; w >>= 1)
+#pragma unroll
+              for (int kk = 0; kk < w; ++kk) t[kk] = fminf(t[kk], t[kk + w]);
+            kth = t[0];
           }
+        }
+      }
+      if (debug & 256) {  // timing split: no insertions were made; evaluate 8 in-slab columns anyway
+#pragma unroll
+        for (int k = 0; k < PKK; ++k) {
+          lv[k] = 0.0f;
+          lp[k] = (uint32_t)min(lo32 + k, max(lo32, hi32 - 1));
         }
       }
       // exact errors of the list (all evaluated, branch-free, so their
@@ -798,7 +851,7 @@ __global__ void __maxnreg__(MAXREG)
       uint32_t pfirst = lp[0];
 #pragma unroll
       for (int k = 1; k < PKK; ++k) pfirst = (kv == k) ? lp[k] : pfirst;
-      if (rvalid && !rflat && kv >= 0) {
+      if (rvalid && !rflat && kv >= 0 && !(debug & 2048)) {  // (debug & 2048: not evaluated, timing)
 #pragma unroll
         for (int k = 0; k < PKK; ++k) {
           const int64_t pe = c0 + (lv[k] >= 0.0f ? lp[k] : pfirst);
