@@ -493,3 +493,24 @@ def test_dbc_grid_non_pow2_sides_match_reference(side):
     blocks = ODD[f"dbc{side}.blocks"]
     assert np.array_equal(codec.dbc_grid(blocks), ODD[f"dbc{side}.fd"])
     assert np.array_equal(codec.dbc_grid(blocks, clamp=False), ODD[f"dbc{side}.raw"])
+
+
+@pytest.mark.parametrize("strategy", ["dynamic_fd", "exhaustive"])
+def test_torch_op_encode_matches_oracle(strategy):
+    """torch.ops.fic.encode on a device image: the oracle's
+    records and RMS bit for bit, stats in STATS_FIELDS order."""
+    import torch
+
+    from paper_1206_4880_b200 import ops
+
+    img = np.random.default_rng(7).integers(0, 256, (96, 96), dtype=np.uint8)
+    rec, pre, post, pools, stats = torch.ops.fic.encode(
+        torch.from_numpy(img).cuda(), 8, 16, 2, True, codec.STRATEGY_IDS[strategy], None, 0)
+    ref = orc.encode(img, strategy, stride=2, isometries=True)
+    assert np.array_equal(_recs(rec.cpu().numpy()), ref.records)
+    assert np.array_equal(pre.cpu().numpy(), ref.pre_rms)
+    assert np.array_equal(post.cpu().numpy(), ref.post_rms)
+    st = dict(zip(ops.STATS_FIELDS, stats.tolist()))
+    assert st["comparisons"] == ref.comparisons and st["n_ranges"] == 144
+    with pytest.raises(ValueError):
+        torch.ops.fic.encode(torch.from_numpy(img).cuda(), 8, 16, 2, True, 9, None, 0)

@@ -286,3 +286,23 @@ def test_oracle_decode_matches_reference_snapshots(golden_decode):
         got = orc.decode(rec, img.shape[1], img.shape[0], 8, 16, stride, iterations=4,
                          initial=g[f"{name}.init_float"])
         assert np.array_equal(got, g[f"{name}.decoded_float_init"])
+
+
+def test_torch_op_registered_with_survey_schema():
+    """torch.ops.fic.encode (SURVEY §8(b)) exists with the named signature;
+    its fake implementation gives the output shapes without a device."""
+    import torch
+    from torch._subclasses.fake_tensor import FakeTensorMode
+
+    from paper_1206_4880_b200 import ops
+
+    schema = str(torch.ops.fic.encode.default._schema)
+    assert schema.startswith("fic::encode(Tensor image, SymInt range_size, SymInt domain_size, "
+                             "SymInt stride, bool isometries, SymInt strategy_id, float? delta, "
+                             "SymInt fd_source) -> (Tensor, Tensor, Tensor, Tensor, Tensor)"), schema
+    with FakeTensorMode():
+        x = torch.empty((96, 64), dtype=torch.uint8)
+        rec, pre, post, pools, stats = torch.ops.fic.encode(x, 8, 16, 4, True, 3, 0.1, 0)
+    assert rec.shape == (96, 7) and rec.dtype == torch.uint8
+    assert pre.shape == post.shape == (96,) and pools.dtype == torch.int64
+    assert stats.shape == (len(ops.STATS_FIELDS),) and stats.dtype == torch.float64
