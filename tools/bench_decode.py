@@ -1,5 +1,6 @@
 """Decoder measurement: decode the cfg3 code on the GPU
-(10 iterations, codec.py:516-598) and check it against the CPU oracle.
+(10 iterations, codec.py:516-598) and check it against the reference's own
+decoder (the unmodified package installed in baseline/_ref).
 
     python tools/bench_decode.py [--iters 10] [--reps 20]
 
@@ -18,8 +19,15 @@ sys.path.insert(0, ".")
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
-from oracle import fic_oracle as orc  # noqa: E402  (checker + CPU baseline only)
 from paper_1206_4880_b200 import _lib, codec, synth  # noqa: E402
+
+sys.path.insert(0, "baseline/_ref")  # the reference package (bench.py --impl reference installs it)
+import fic.codec as ref_codec  # noqa: E402
+
+
+def psnr(a, b):
+    mse = float(np.mean((a.astype(np.float64) - b.astype(np.float64)) ** 2))
+    return float("inf") if mse == 0 else 10.0 * np.log10(255.0 ** 2 / mse)
 
 
 def main():
@@ -60,17 +68,19 @@ def main():
     for _ in range(args.reps):
         gpu_img = codec.decode(code, iterations=args.iters)
     ms_e2e = (time.perf_counter() - t0) / args.reps * 1e3
-    # CPU oracle (the reference's algorithm in numpy)
+    # the reference's own decoder (numpy, one thread)
+    ref_code = ref_codec.FractalCode(w, h, code.range_size, code.domain_size, code.stride,
+                                     code.strategy_id, code.isometries,
+                                     np.ascontiguousarray(code.records).view(ref_codec.RECORD_DTYPE).ravel())
     t0 = time.perf_counter()
-    ref_img = orc.decode(code.records, w, h, code.range_size, code.domain_size, code.stride,
-                         iterations=args.iters)
+    ref_img = ref_codec.decode(ref_code, iterations=args.iters)
     ms_cpu = (time.perf_counter() - t0) * 1e3
     print(json.dumps({
         "what": "decode cfg3 code (1024x1024, 16384 transforms)", "iterations": args.iters,
-        "ms_device": ms_dev, "ms_e2e": ms_e2e, "ms_cpu_oracle_1thread": ms_cpu,
+        "ms_device": ms_dev, "ms_e2e": ms_e2e, "ms_cpu_reference_1thread": ms_cpu,
         "pixels_per_s_device": h * w * args.iters / (ms_dev / 1e3),
-        "identical_to_oracle": bool(np.array_equal(gpu_img, ref_img)),
-        "psnr_vs_source": orc.psnr(img, gpu_img),
+        "identical_to_reference": bool(np.array_equal(gpu_img, ref_img)),
+        "psnr_vs_source": psnr(img, gpu_img),
     }))
 
 

@@ -4,11 +4,30 @@ the reference's final errors (tests/golden/scale_cfg4.npz) as thresholds:
     python tools/qbound_check.py"""
 import sys, numpy as np
 sys.path.insert(0, ".")
-from oracle import fic_oracle as orc
+
+
+def range_blocks(image, rs):  # blocks.py:145-155, raster order
+    h, w = image.shape
+    return image.reshape(h // rs, rs, w // rs, rs).transpose(0, 2, 1, 3).reshape(-1, rs, rs)
+
+
+def decimated_domains(image, ds, st):  # blocks.py:58-82: windows, 2x2 floor means
+    win = np.lib.stride_tricks.sliding_window_view(image, (ds, ds))[::st, ::st].reshape(-1, ds, ds)
+    g = win.reshape(-1, ds // 2, 2, ds // 2, 2).astype(np.uint32)
+    return (g.sum(axis=(2, 4)) >> 2)
+
+
+def iso_perms(n):  # blocks.py:113-139: the 8 dihedral maps as gather tables
+    idx = np.arange(n * n).reshape(n, n)
+    out = []
+    for i in range(8):
+        b = np.rot90(idx, i % 4)
+        out.append((b.T if i >= 4 else b).ravel())
+    return np.stack(out)
 g=np.load('./tests/golden/scale_cfg4.npz'); im=g['cfg4_ex.image']
-r_mat = orc.range_blocks(im, 4).reshape(-1, 16).astype(np.float64)
-d_mat = orc.decimate(orc.domain_blocks(im, 8, 2)).reshape(-1, 16).astype(np.float64)
-K=16.0; perms=orc.iso_perms(4); inv_perms=np.stack([np.argsort(p) for p in perms])
+r_mat = range_blocks(im, 4).reshape(-1, 16).astype(np.float64)
+d_mat = decimated_domains(im, 8, 2).reshape(-1, 16).astype(np.float64)
+K=16.0; perms=iso_perms(4); inv_perms=np.stack([np.argsort(p) for p in perms])
 sd=d_mat.sum(1); sdd=(d_mat*d_mat).sum(1); den=K*sdd-sd*sd
 thr_all=g['cfg4_ex.post_rms']**2*K
 sr_all=r_mat.sum(1); V_all=(r_mat*r_mat).sum(1)-sr_all**2/K
