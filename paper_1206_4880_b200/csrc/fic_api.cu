@@ -1394,6 +1394,7 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
         if (!getenv("FIC_HL_SORT") || atoi(getenv("FIC_HL_SORT")) != 0) {
           hla.sorted = sc.get<uint4>(ta.hl_cap);
           hla.n_sorted = d_rb->sl_count + 2;
+          hla.run_ctr = d_rb->sl_count + 3;  // zeroed with the readback block
           hla.bins = sc.get<uint32_t>((size_t)(g.D + 63) / 64 + 2);
         }
       }

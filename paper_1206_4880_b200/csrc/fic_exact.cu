@@ -307,11 +307,16 @@ __global__ void __launch_bounds__(256, FIC_HL_BLK) k_hl_rescore(PoolView P, Rang
   // loads a chunk's columns once for all its entries; else a grid stride
   const uint4* L = a.sorted ? a.sorted : a.hl;
   const int64_t n = a.sorted ? (int64_t)*a.n_sorted : (int64_t)min(*a.hl_count, a.hl_cap);
+  // sorted: runs of HLRUN consecutive entries handed out by an atomic
+  // counter (their costs vary: a static cut leaves a tail)
+  constexpr int HLRUN = 64;
   int64_t i0 = warp0, i1 = n, step = nwarps;
   if (a.sorted) {
-    const int64_t run = (n + nwarps - 1) / nwarps;
-    i0 = min(n, warp0 * run);
-    i1 = min(n, i0 + run);
+    uint32_t r0 = 0;
+    if (lane == 0) r0 = atomicAdd(a.run_ctr, 1u);
+    r0 = __shfl_sync(0xffffffffu, r0, 0);
+    i0 = min(n, (int64_t)r0 * HLRUN);
+    i1 = min(n, i0 + HLRUN);
     step = 1;
   }
   const int iso_sh = Rv.n_iso == 8 ? 3 : 0;  // n_iso is 8 or 1 (launch_hl_rescore checks)
@@ -327,6 +332,16 @@ __global__ void __launch_bounds__(256, FIC_HL_BLK) k_hl_rescore(PoolView P, Rang
   uint4 en = i0 < i1 ? L[i0] : make_uint4(0, 0, 0, 0);  // next entry (prefetched)
   for (int64_t i = i0; i < i1; i += step) {
     const uint4 e = en;
+    if (a.sorted && i + 1 == i1) {  // next run
+      uint32_t r0 = 0;
+      if (lane == 0) r0 = atomicAdd(a.run_ctr, 1u);
+      r0 = __shfl_sync(0xffffffffu, r0, 0);
+      const int64_t n0 = min(n, (int64_t)r0 * HLRUN);
+      if (n0 < n) {
+        i = n0 - 1;  // the loop increment lands on n0
+        i1 = min(n, n0 + HLRUN);
+      }
+    }
     if (i + step < i1) en = L[i + step];
     if (e.w == 0) continue;
     // lane L with bit L of the ballot loads row e.y + L: range id, isometry,
@@ -503,7 +518,12 @@ void launch_hl_sort(const HlArgs& a, int64_t D, cudaStream_t s) {
 void launch_hl_rescore(const PoolView& P, const RangeView& Rv, const HlArgs& a, cudaStream_t s) {
   if (!a.hl) return;
   if (Rv.n_iso != 8 && Rv.n_iso != 1) invalid("hit list needs 1 or 8 isometries");
-  const unsigned grid = 148 * 8;  // grid-stride over the device-side entry count
+  // one resident wave (the sorted list is cut into one contiguous run per
+  // warp: a second, partial wave would leave SMs idle at the end)
+  int dev = 0, sms = 148;
+  FIC_CUDA(cudaGetDevice(&dev));
+  FIC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const unsigned grid = (unsigned)(sms * FIC_HL_BLK);
   if (Rv.K == 64)
     k_hl_rescore<64><<<grid, 256, 0, s>>>(P, Rv, a);
   else if (Rv.K == 16)

@@ -205,6 +205,7 @@ struct HlArgs {
   const uint4* sorted;         // [hl_cap] entries ordered by chunk column / 64
   const uint32_t* n_sorted;    // [1] entries in `sorted`
   uint32_t* bins;              // [D / 64 + 2] histogram -> cursors
+  uint32_t* run_ctr;           // [1] runs of the sorted list handed out (zeroed per call)
 };
 void launch_hl_sort(const HlArgs& a, int64_t D, cudaStream_t s);
 void launch_hl_rescore(const PoolView& P, const RangeView& Rv, const HlArgs& a, cudaStream_t s);
