@@ -514,3 +514,29 @@ def test_torch_op_encode_matches_oracle(strategy):
     assert st["comparisons"] == ref.comparisons and st["n_ranges"] == 144
     with pytest.raises(ValueError):
         torch.ops.fic.encode(torch.from_numpy(img).cuda(), 8, 16, 2, True, 9, None, 0)
+
+
+@pytest.mark.parametrize("iso", [True, False])
+@pytest.mark.parametrize("env", [{}, {"FIC_HL_SORT": "0"}, {"FIC_HL_CAP": "3"}, {"FIC_HL": "0"}])
+def test_4x4_hit_list_paths_match_oracle(iso, env, monkeypatch):
+    """4x4 ranges through the tensor matcher (pilot + hit list + k_hl_rescore):
+    with and without isometries (n_iso 8 / 1), the list unsorted, a list that
+    overflows after 3 entries (the rest through the survivor list) and the
+    list off -- the oracle's records and RMS bit for bit."""
+    import torch
+
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    rng = np.random.default_rng(11)
+    img = (np.add.outer(np.arange(96), np.arange(96)) // 3).astype(np.uint8)  # smooth half
+    img[40:, 40:] = rng.integers(0, 256, (56, 56), dtype=np.uint8)            # texture
+    res = codec.encode_device(torch.from_numpy(img).cuda(), "exhaustive", range_size=4,
+                              domain_size=8, stride=2, isometries=iso, small_pool=1,
+                              max_segment=256)
+    ref = orc.encode(img, "exhaustive", range_size=4, domain_size=8, stride=2, isometries=iso)
+    assert np.array_equal(_recs(res.records.cpu().numpy()), ref.records)
+    assert np.array_equal(res.pre_rms.cpu().numpy(), ref.pre_rms)
+    assert np.array_equal(res.post_rms.cpu().numpy(), ref.post_rms)
+    assert res.stats["tensor_tiles"] > 0
+    if not env:
+        assert res.stats["hl_entries"] > 0
