@@ -1088,7 +1088,14 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
   const int K = g.npx;
   const int nshard = std::max(1, p.shard_count);
   const int shard = std::min(std::max(0, p.shard_index), nshard - 1);
-  const bool tensor_ok = (p.matcher != FIC_MATCH_EXACT) && tc_supported(K);
+  // Small jobs (at most kSmallJob candidates even if every pool were the
+  // whole domain set) go to the exact CUDA-core matcher: the tensor
+  // pipeline's fixed cost (persistent grid, TMEM allocation, ring fill)
+  // exceeds their work (cfg1: 0.285 -> 0.20 ms).  An explicit small_pool
+  // keeps the caller's routing.
+  constexpr int64_t kSmallJob = 16 << 20;
+  const bool small_job = p.small_pool == 0 && (int64_t)g.R * g.D * g.n_iso <= kSmallJob;
+  const bool tensor_ok = (p.matcher != FIC_MATCH_EXACT) && tc_supported(K) && !small_job;
   const int small_pool = p.small_pool > 0 ? p.small_pool : 256;
   const int seg_t = p.max_segment > 0 ? (int)align_up(p.max_segment, 256) : 131072;
   // first segment of each tensor tile (a multiple of the 128-column N-tile);

@@ -383,7 +383,7 @@ __global__ void __maxnreg__(MAXREG)
   uint32_t* s_cdom = s_crow + 32;                                   // [32]
   uint32_t* s_csqoq = s_cdom + 32;                                  // [32]
   double* s_cerr = reinterpret_cast<double*>(s_csqoq + 32);         // [32]
-  double* s_cpre = s_cerr + 32;                                     // [32]
+  [[maybe_unused]] double* s_cpre = s_cerr + 32;                                     // [32]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   auto full_bar = [&](int s) { return smem_u32(bars + s); };
@@ -423,7 +423,7 @@ __global__ void __maxnreg__(MAXREG)
   const uint32_t tmem_base = *tmem_holder;
 
   // pipeline state (each role advances its own copy identically)
-  int stage = 0, ph = 0, acc = 0, acc_ph = 0;
+  int stage = 0, ph = 0;  // producer ring position (the MMA and screening warps derive theirs from gt)
   uint32_t gt = 0;  // N-tiles this CTA processed in earlier items (stage / phase bookkeeping)
   const int n_iso = Rv.n_iso;
   const double nK = (double)K;
@@ -438,7 +438,6 @@ __global__ void __maxnreg__(MAXREG)
   constexpr int SW = BN / NSPLIT;                               // columns per slice
   const int rk = row / n_iso;          // range within this CTA's rows (thr_s index)
   const int iso = row - rk * n_iso;
-  const int rk_tile = (row + rbase) / n_iso;  // range within the tile (tlist index)
   double sr = 0, srr = 0, V = 0, eps = 0;
   int32_t rlo = 0, rhi = 0;
   uint32_t rid = 0;
