@@ -503,15 +503,69 @@ __global__ void k_hl_scatter(const uint4* hl, const uint32_t* cnt, uint32_t cap,
   }
 }
 
+// Few bins (cfg4: 4,049 for 2,600 entries each): global atomics on one bin
+// serialise, so each block counts a contiguous slice in shared memory,
+// reserves its bins' ranges with one global atomic per (block, bin), and
+// places its entries with shared-memory atomics.
+__global__ void __launch_bounds__(512) k_hl_hist_smem(const uint4* hl, const uint32_t* cnt,
+                                                      uint32_t cap, uint32_t* hist, int nbins) {
+  extern __shared__ uint32_t sh[];  // [nbins]
+  for (int b = threadIdx.x; b < nbins; b += blockDim.x) sh[b] = 0;
+  __syncthreads();
+  const int64_t n = (int64_t)min(*cnt, cap);
+  const int64_t per = (n + gridDim.x - 1) / gridDim.x, s0 = min(n, per * blockIdx.x), s1 = min(n, s0 + per);
+  for (int64_t i = s0 + threadIdx.x; i < s1; i += blockDim.x) {
+    const uint4 e = hl[i];
+    if (e.w) atomicAdd(sh + (e.z >> 6), 1u);
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < nbins; b += blockDim.x)
+    if (sh[b]) atomicAdd(hist + b, sh[b]);
+}
+
+__global__ void __launch_bounds__(512) k_hl_scatter_smem(const uint4* hl, const uint32_t* cnt,
+                                                         uint32_t cap, uint32_t* cursor, uint4* out,
+                                                         int nbins) {
+  extern __shared__ uint32_t sh[];  // [nbins] counts -> bases
+  for (int b = threadIdx.x; b < nbins; b += blockDim.x) sh[b] = 0;
+  __syncthreads();
+  const int64_t n = (int64_t)min(*cnt, cap);
+  const int64_t per = (n + gridDim.x - 1) / gridDim.x, s0 = min(n, per * blockIdx.x), s1 = min(n, s0 + per);
+  for (int64_t i = s0 + threadIdx.x; i < s1; i += blockDim.x) {
+    const uint4 e = hl[i];
+    if (e.w) atomicAdd(sh + (e.z >> 6), 1u);
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < nbins; b += blockDim.x)
+    if (sh[b]) sh[b] = atomicAdd(cursor + b, sh[b]);  // this block's range of bin b
+  __syncthreads();
+  for (int64_t i = s0 + threadIdx.x; i < s1; i += blockDim.x) {
+    const uint4 e = hl[i];
+    if (e.w) out[atomicAdd(sh + (e.z >> 6), 1u)] = e;
+  }
+}
+
 void launch_hl_sort(const HlArgs& a, int64_t D, cudaStream_t s) {
   if (!a.hl || !a.sorted) return;
   const int nbins = (int)((D + 63) / 64) + 1;
   FIC_CUDA(cudaMemsetAsync(a.bins, 0, (size_t)nbins * sizeof(uint32_t), s));
-  k_hl_hist<<<148 * 8, 256, 0, s>>>(a.hl, a.hl_count, a.hl_cap, a.bins);
+  const size_t smem = (size_t)nbins * sizeof(uint32_t);
+  const bool in_smem = smem <= 96 * 1024;
+  if (in_smem) {
+    smem_optin_k(k_hl_hist_smem, (int)smem);
+    smem_optin_k(k_hl_scatter_smem, (int)smem);
+    k_hl_hist_smem<<<148 * 2, 512, smem, s>>>(a.hl, a.hl_count, a.hl_cap, a.bins, nbins);
+  } else {
+    k_hl_hist<<<148 * 8, 256, 0, s>>>(a.hl, a.hl_count, a.hl_cap, a.bins);
+  }
   FIC_CHECK_LAUNCH();
   k_hl_scan<<<1, 1024, 0, s>>>(a.bins, nbins, const_cast<uint32_t*>(a.n_sorted));
   FIC_CHECK_LAUNCH();
-  k_hl_scatter<<<148 * 8, 256, 0, s>>>(a.hl, a.hl_count, a.hl_cap, a.bins, const_cast<uint4*>(a.sorted));
+  if (in_smem)
+    k_hl_scatter_smem<<<148 * 2, 512, smem, s>>>(a.hl, a.hl_count, a.hl_cap, a.bins,
+                                                  const_cast<uint4*>(a.sorted), nbins);
+  else
+    k_hl_scatter<<<148 * 8, 256, 0, s>>>(a.hl, a.hl_count, a.hl_cap, a.bins, const_cast<uint4*>(a.sorted));
   FIC_CHECK_LAUNCH();
 }
 
