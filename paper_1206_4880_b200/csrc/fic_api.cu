@@ -24,15 +24,19 @@ thread_local int g_launches = 0;
 void set_error(const std::string& m) { g_err = m; }
 const char* last_error() { return g_err.c_str(); }
 
+// The attribute is per (device, function) and only ever raised: a launch
+// with less dynamic shared memory than the current limit is always valid,
+// while lowering it would break a later, larger launch of the same kernel.
 void smem_optin(const void* func, int bytes) {
   static std::mutex mu;
-  static std::set<std::tuple<int, const void*, int>> done;
+  static std::map<std::pair<int, const void*>, int> limit;
   int dev = 0;
   FIC_CUDA(cudaGetDevice(&dev));
   std::lock_guard<std::mutex> lock(mu);
-  if (done.count({dev, func, bytes})) return;
+  int& cur = limit[{dev, func}];
+  if (bytes <= cur) return;
   FIC_CUDA(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-  done.insert({dev, func, bytes});
+  cur = bytes;
 }
 
 // ---------------------------------------------------------------------------
