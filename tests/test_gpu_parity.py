@@ -540,3 +540,25 @@ def test_4x4_hit_list_paths_match_oracle(iso, env, monkeypatch):
     assert res.stats["tensor_tiles"] > 0
     if not env:
         assert res.stats["hl_entries"] > 0
+
+
+def test_kernels_with_per_call_shared_memory_any_size_order():
+    """Kernels whose dynamic shared memory depends on the call (the hit-list
+    sort: one counter per 64 pool columns) keep working when a smaller call
+    comes between two larger ones (the opt-in limit is only ever raised)."""
+    import torch
+
+    rng = np.random.default_rng(3)
+    small = rng.integers(0, 256, (64, 64), dtype=np.uint8)
+    large = rng.integers(0, 256, (384, 384), dtype=np.uint8)
+    kw = dict(range_size=4, domain_size=8, stride=2, isometries=True, small_pool=1)
+    first = None
+    for img in (large, small, large):
+        res = codec.encode_device(torch.from_numpy(img).cuda(), "exhaustive", **kw)
+        torch.cuda.synchronize()
+        assert res.stats["hl_entries"] > 0
+        if img is large:
+            if first is None:
+                first = res.records.clone()
+            else:
+                assert torch.equal(first, res.records)
