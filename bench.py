@@ -414,10 +414,14 @@ def run_ours(args):
     # (the ranks' kernels never wait on each other); its numbers are not
     # bench values and the line says so
     one_gpu = os.environ.get("FIC_BENCH_ONE_GPU") == "1"
+    # FIC_BENCH_DIST=1: the distributed code path (process group, sharded
+    # encode, packed exchange, max over ranks) even with one rank -- the NCCL
+    # path of `--gpus N` run on a one-GPU box
+    dist_on = world > 1 or os.environ.get("FIC_BENCH_DIST") == "1"
     if one_gpu:
         local = 0
     torch.cuda.set_device(local)
-    if world > 1:
+    if dist_on:
         if one_gpu:
             dist.init_process_group("gloo")
         else:
@@ -438,12 +442,12 @@ def run_ours(args):
         torch.empty(n_r, dtype=torch.int64, device="cuda"), {})
 
     def step():
-        if world == 1:
+        if not dist_on:
             return codec.encode_device(d_img, "dynamic_fd", out=out, **CFG).stats
         return encode_sharded(d_img, "dynamic_fd", **CFG)[4]
 
     def barrier():
-        if world > 1:
+        if dist_on:
             dist.barrier()
         torch.cuda.synchronize()
 
@@ -467,7 +471,7 @@ def run_ours(args):
     ms_t = float(np.mean(tens))
     # useful tensor-path matches of this rank's shard (summed over the ranks)
     tcomp = int(stats[-1]["tensor_comparisons"])
-    if world > 1:
+    if dist_on:
         ms, ms_t = max_over_ranks([ms, ms_t])
         t = torch.tensor([float(tcomp)], dtype=torch.float64, device="cpu" if one_gpu else "cuda")
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
@@ -476,12 +480,12 @@ def run_ours(args):
     value = comps / (ms / 1e3)
     # untimed: the pool builder alone on the main stream (roofline_hbm.isolated)
     os.environ["FIC_POOL_SERIAL"] = "1"
-    serial_stats = [step() for _ in range(3)] if world == 1 else None
+    serial_stats = [step() for _ in range(3)] if not dist_on else None
     os.environ.pop("FIC_POOL_SERIAL", None)
 
     # the encode's records (all-gathered when sharded) against the
     # reference's own on every cfg3 range
-    if world == 1:
+    if not dist_on:
         r = codec.encode_device(d_img, "dynamic_fd", **CFG)
         recs, pre, post = r.records, r.pre_rms, r.post_rms
     else:
@@ -492,7 +496,7 @@ def run_ours(args):
     for i in range(max(1, args.steps // 2) + 1):
         barrier()
         t0 = time.perf_counter()
-        if world == 1:
+        if not dist_on:
             code, es = codec.encode(img, "dynamic_fd", **CFG)
         else:
             di = torch.from_numpy(img).cuda()
@@ -502,10 +506,10 @@ def run_ours(args):
         if i:  # first call is a warm-up
             e2e_times.append(time.perf_counter() - t0)
     e2e_s = float(np.mean(e2e_times))
-    if world > 1:
+    if dist_on:
         e2e_s = max_over_ranks([e2e_s])[0]
     if rank != 0:
-        if world > 1:
+        if dist_on:
             dist.destroy_process_group()
         return
     peak_tf, peak_gbs, src = _peaks()
@@ -533,6 +537,9 @@ def run_ours(args):
         "gpu_launches": int(stats[-1]["kernel_launches"]) * args.steps,
         **({"harness": "FIC_BENCH_ONE_GPU: all ranks on cuda:0 with gloo -- a functional "
                        "test of the multi-rank path, not a bench value"} if one_gpu else {}),
+        **({"harness": "FIC_BENCH_DIST: the distributed path (NCCL group, sharded encode, "
+                       "packed all-gather, max over ranks) with one rank"}
+           if dist_on and world == 1 and not one_gpu else {}),
         "parity": parity,
         "clocks": clk.summary(),
         "device_stats": {k: stats[-1][k] for k in ("ms_fd", "ms_pool", "ms_match", "ms_tensor",
@@ -543,7 +550,7 @@ def run_ours(args):
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(img)
     print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist_on:
         dist.destroy_process_group()
 
 

@@ -173,6 +173,17 @@ int fic_decode_step_v1(const uint8_t* d_records, int32_t height, int32_t width,
                        int32_t range_size, int32_t domain_size, int32_t stride,
                        const double* d_src, double* d_dst, uint8_t* d_out, void* stream);
 
+/* Multi-GPU range sharding exchange (replaces the reference's per-thread
+ * result slots, codec.py:386-397, across processes).  pack: the rank's
+ * outputs (ranges it matched have post RMS >= 0) as an int64 [n][3] buffer
+ * -- record bytes | owner count << 56, pre RMS bits, post RMS bits -- zero
+ * elsewhere, for one all-reduce (SUM) over the ranks.  unpack: the reduced
+ * buffer back into records / RMS; *d_bad = ranges whose owner count != 1. */
+int fic_shard_pack_v1(const uint8_t* d_records, const double* d_pre_rms, const double* d_post_rms,
+                      int64_t n, int64_t* d_buf, void* stream);
+int fic_shard_unpack_v1(const int64_t* d_buf, int64_t n, uint8_t* d_records, double* d_pre_rms,
+                        double* d_post_rms, uint32_t* d_bad, void* stream);
+
 const char* fic_last_error(void);
 int fic_abi_version(void);
 /* Releases cached device workspaces of the calling thread's current device. */

@@ -77,7 +77,8 @@ class FicStats(ctypes.Structure):
 
 # every symbol include/fic_b200.h declares
 EXPORTS = ("fic_encode_v1", "fic_plan_v1", "fic_pool_v1", "fic_dbc_v1", "fic_decode_v1",
-           "fic_decode_step_v1", "fic_last_error", "fic_abi_version", "fic_release")
+           "fic_decode_step_v1", "fic_shard_pack_v1", "fic_shard_unpack_v1", "fic_last_error",
+           "fic_abi_version", "fic_release")
 
 _lib = None
 
@@ -102,8 +103,10 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.fic_decode_v1.argtypes = [vp, i32, i32, i32, i32, i32, i32, ctypes.c_double, vp, vp, vp]
     lib.fic_pool_v1.argtypes = [vp, i32, i32, P(FicParams), vp, vp, vp, vp, vp, vp]
     lib.fic_decode_step_v1.argtypes = [vp, i32, i32, i32, i32, i32, vp, vp, vp, vp]
+    lib.fic_shard_pack_v1.argtypes = [vp, vp, vp, i64, vp, vp]
+    lib.fic_shard_unpack_v1.argtypes = [vp, i64, vp, vp, vp, vp, vp]
     for name in ("fic_encode_v1", "fic_plan_v1", "fic_pool_v1", "fic_dbc_v1", "fic_decode_v1",
-                 "fic_decode_step_v1"):
+                 "fic_decode_step_v1", "fic_shard_pack_v1", "fic_shard_unpack_v1"):
         getattr(lib, name).restype = ctypes.c_int
     lib.fic_last_error.restype = ctypes.c_char_p
     lib.fic_last_error.argtypes = []

@@ -1787,6 +1787,44 @@ static void decode_step_impl(const uint8_t* rec, int H, int W, int rs, int ds, i
 }  // namespace fic
 
 // ===========================================================================
+// Multi-GPU exchange of range sharding (sharding.py): each rank's outputs
+// packed into an int64 (R, 3) buffer -- record bytes plus an owner-count
+// byte, pre and post RMS bits -- zero outside the ranges the rank matched
+// (post RMS >= 0), so one all-reduce (SUM) over the ranks reproduces every
+// range's bytes; the unpack writes them back and counts ranges whose owner
+// count is not 1 (a hole or an overlap in the partition).
+__global__ void k_shard_pack(const uint8_t* rec, const double* pre, const double* post, int64_t n,
+                             unsigned long long* buf) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double p = post[i];
+  unsigned long long w0 = 0, w1 = 0, w2 = 0;
+  if (p >= 0.0) {
+    const uint8_t* r = rec + i * 7;
+    for (int k = 0; k < 7; ++k) w0 |= (unsigned long long)r[k] << (8 * k);
+    w0 |= 1ull << 56;
+    w1 = (unsigned long long)__double_as_longlong(pre[i]);
+    w2 = (unsigned long long)__double_as_longlong(p);
+  }
+  buf[3 * i] = w0;
+  buf[3 * i + 1] = w1;
+  buf[3 * i + 2] = w2;
+}
+
+__global__ void k_shard_unpack(const unsigned long long* buf, int64_t n, uint8_t* rec, double* pre,
+                               double* post, unsigned int* bad) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool ok = i < n && (buf[3 * i] >> 56) == 1;
+  if (i < n) {
+    const unsigned long long w0 = buf[3 * i];
+    for (int k = 0; k < 7; ++k) rec[i * 7 + k] = (uint8_t)(w0 >> (8 * k));
+    pre[i] = __longlong_as_double((long long)buf[3 * i + 1]);
+    post[i] = __longlong_as_double((long long)buf[3 * i + 2]);
+  }
+  const unsigned m = __ballot_sync(0xffffffffu, i < n && !ok);
+  if (m && (threadIdx.x & 31) == 0) atomicAdd(bad, (unsigned)__popc(m));
+}
+
 // extern "C"
 // ===========================================================================
 using namespace fic;
@@ -1866,6 +1904,31 @@ extern "C" int fic_decode_step_v1(const uint8_t* d_records, int32_t height, int3
   return guarded([&] {
     decode_step_impl(d_records, height, width, range_size, domain_size, stride, d_src, d_dst,
                      d_out, as_stream(stream));
+  });
+}
+
+extern "C" int fic_shard_pack_v1(const uint8_t* d_records, const double* d_pre_rms,
+                                 const double* d_post_rms, int64_t n, int64_t* d_buf, void* stream) {
+  return guarded([&] {
+    if (n < 0) invalid("negative range count");
+    if (n == 0) return;
+    k_shard_pack<<<(unsigned)cdiv(n, 256), 256, 0, as_stream(stream)>>>(
+        d_records, d_pre_rms, d_post_rms, n, reinterpret_cast<unsigned long long*>(d_buf));
+    FIC_CHECK_LAUNCH();
+  });
+}
+
+extern "C" int fic_shard_unpack_v1(const int64_t* d_buf, int64_t n, uint8_t* d_records,
+                                   double* d_pre_rms, double* d_post_rms, uint32_t* d_bad,
+                                   void* stream) {
+  return guarded([&] {
+    if (n < 0) invalid("negative range count");
+    FIC_CUDA(cudaMemsetAsync(d_bad, 0, sizeof(uint32_t), as_stream(stream)));
+    if (n == 0) return;
+    // whole warps (the ballot), so the grid covers n rounded up to 256
+    k_shard_unpack<<<(unsigned)cdiv(n, 256), 256, 0, as_stream(stream)>>>(
+        reinterpret_cast<const unsigned long long*>(d_buf), n, d_records, d_pre_rms, d_post_rms, d_bad);
+    FIC_CHECK_LAUNCH();
   });
 }
 

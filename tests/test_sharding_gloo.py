@@ -3,10 +3,10 @@
 The per-rank match is stood in for by the oracle on that rank's ranges (the
 GPU shard partition itself is covered by the gpu tests, including
 tests/test_sharding_gpu.py, which runs the real library shard path in two
-processes); what is tested here is the host-side exchange: each rank packs
-only the ranges it owns, one all-gather of the padded shards, a scatter by
-range id -- which must reproduce the 1-process result byte for byte, for
-even and uneven shards, and reject a partition with a hole or an overlap.
+processes); what is tested here is the host-side exchange: each rank contributes only
+the ranges it owns (zeros elsewhere) to two all-reduces -- which must
+reproduce the 1-process result byte for byte, for even and uneven shards,
+and reject a partition with a hole or an overlap.
 """
 
 import os
