@@ -509,8 +509,12 @@ __global__ void __launch_bounds__(1024) k_cost_scan(const unsigned long long* ke
       if (k < R) {
         const unsigned long long kk = key[k];
         const unsigned long long pool = (uint32_t)kk - (uint32_t)((kk >> 32) & 0x7fffffffu);
-        // an exact-path candidate costs ~32x a screened one (as k_cost)
-        v[i] = pool * n_iso * ((kk >> 63) ? 32ull : 1ull) + 1ull;
+        // an exact-path candidate costs ~32x a screened one (as k_cost);
+        // every range also carries its share of a tensor tile's fixed cost
+        // (item setup, pipeline fill: ~0.7 us per 16-range tile at cfg3 =
+        // ~3.5e5 screened candidates per range), or the shard of the
+        // small-window ranges at the end of the order runs long
+        v[i] = pool * n_iso * ((kk >> 63) ? 32ull : 1ull) + (1ull << 18);
       }
     }
     unsigned long long t = 0;
