@@ -2,6 +2,7 @@
 golden outputs and the pinned oracle.  Bit-exact records, RMS and FD."""
 
 import hashlib
+import re
 
 import numpy as np
 import pytest
@@ -562,3 +563,56 @@ def test_kernels_with_per_call_shared_memory_any_size_order():
                 first = res.records.clone()
             else:
                 assert torch.equal(first, res.records)
+
+
+def _sweep_cases(n=150, seed=2026):
+    """Seeded random small encodes: strategy, range size (domain = 2x),
+    stride, isometries, delta, fd_source, matcher and forced tensor routing."""
+    rng = np.random.default_rng(seed)
+    out = []
+    for i in range(n):
+        rs = int(rng.choice([2, 3, 4, 5, 6, 8]))
+        strat = str(rng.choice(["exhaustive", "nosearch", "static2", "dynamic_fd"]))
+        fd_src = "downsampled" if rng.random() < 0.2 else "original"
+        side = rs if fd_src == "downsampled" else 2 * rs
+        if strat in ("static2", "dynamic_fd") and side < 8 and side not in (6,):
+            strat = "exhaustive"  # one DBC scale: the reference raises (covered elsewhere)
+        h = int(rng.integers(3, 9)) * rs * 2
+        w = int(rng.integers(3, 9)) * rs * 2
+        out.append(dict(i=i, rs=rs, strategy=strat, fd_source=fd_src, h=h, w=w,
+                        stride=int(rng.integers(1, rs + 1)), iso=bool(rng.random() < 0.7),
+                        delta=[None, 0.05, 0.1, 0.3][int(rng.integers(0, 4))],
+                        matcher=str(rng.choice(["auto", "exact"])),
+                        small_pool=int(rng.choice([0, 1])), seed=int(rng.integers(1 << 30))))
+    return out
+
+
+@pytest.mark.parametrize("case", _sweep_cases(), ids=lambda c: f"sweep{c['i']}")
+def test_random_small_encodes_match_oracle(case):
+    """Breadth net for the routing choices (small jobs to the CUDA-core
+    matcher, forced tensor path, pilot / hit list for 4x4 ranges, odd sizes,
+    every strategy): records and RMS equal the oracle's bit for bit, or both
+    raise the same error."""
+    import torch
+
+    c = case
+    rng = np.random.default_rng(c["seed"])
+    base = np.add.outer(np.arange(c["h"]), np.arange(c["w"])) * rng.integers(1, 4)
+    img = np.clip(base + rng.normal(0, rng.choice([2, 10, 40]), base.shape), 0, 255).astype(np.uint8)
+    if rng.random() < 0.3:
+        img[: c["h"] // 2] = img[0, 0]  # a flat band
+    kw = dict(range_size=c["rs"], domain_size=2 * c["rs"], stride=c["stride"], isometries=c["iso"],
+              fd_source=c["fd_source"])
+    delta = c["delta"] if c["strategy"] == "dynamic_fd" else None
+    try:
+        ref = orc.encode(img, c["strategy"], delta=delta, **kw)
+    except ValueError as e:
+        with pytest.raises(ValueError, match=re.escape(str(e))):
+            codec.encode_device(torch.from_numpy(img).cuda(), c["strategy"], delta=delta,
+                                matcher=c["matcher"], small_pool=c["small_pool"], **kw)
+        return
+    res = codec.encode_device(torch.from_numpy(img).cuda(), c["strategy"], delta=delta,
+                              matcher=c["matcher"], small_pool=c["small_pool"], **kw)
+    assert np.array_equal(_recs(res.records.cpu().numpy()), ref.records), c
+    assert np.array_equal(res.pre_rms.cpu().numpy(), ref.pre_rms), c
+    assert np.array_equal(res.post_rms.cpu().numpy(), ref.post_rms), c
