@@ -545,7 +545,7 @@ def run_ours(args):
         "device_stats": {k: stats[-1][k] for k in ("ms_fd", "ms_pool", "ms_match", "ms_tensor",
                                                   "ms_exact", "exact_evals", "tensor_candidates",
                                                   "tensor_tiles", "exact_tiles", "work_items",
-                                                  "sl_entries", "ms_sl")},
+                                                  "sl_entries", "ms_sl", "graph")},
     }
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(img)

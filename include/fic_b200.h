@@ -109,7 +109,7 @@ typedef struct fic_stats {
   int32_t tensor_tiles, exact_tiles, work_items;
   int32_t kernel_launches;   /* kernels this call launched (library-internal CUB passes excluded) */
   double ms_pool_main;       /* device time of the pool builder's main kernel (k_pool) alone */
-  int64_t reserved0;         /* 0 */
+  int64_t graph;             /* 0 enqueued directly, 1 recorded as a CUDA graph and launched, 2 replayed */
   double ms_sl;              /* device time of the survivor-list and hit-list rescoring (k_sl_rescore, k_hl_rescore) */
   int64_t sl_entries;        /* survivor-list entries (row, 64-column chunk, mask) rescored after the matcher */
   int64_t hl_entries;        /* hit-list entries (warp of rows, 64-column chunk, hit ballot) rescored after the matcher */

@@ -64,7 +64,7 @@ class FicStats(ctypes.Structure):
         ("work_items", ctypes.c_int32),
         ("kernel_launches", ctypes.c_int32),
         ("ms_pool_main", ctypes.c_double),
-        ("reserved0", ctypes.c_int64),
+        ("graph", ctypes.c_int64),
         ("ms_sl", ctypes.c_double),
         ("sl_entries", ctypes.c_int64),
         ("hl_entries", ctypes.c_int64),

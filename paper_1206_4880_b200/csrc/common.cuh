@@ -32,6 +32,12 @@ struct Error {
   } while (0)
 
 extern thread_local int g_launches;  // kernels launched by the current call
+// true while this thread records a CUDA graph of an encode (fic_api.cu):
+// timing events are then recorded as external (timestamp) nodes
+extern thread_local bool g_capturing;
+inline cudaError_t record_timing_event(cudaEvent_t e, cudaStream_t s) {
+  return g_capturing ? cudaEventRecordWithFlags(e, s, cudaEventRecordExternal) : cudaEventRecord(e, s);
+}
 #define FIC_CHECK_LAUNCH() do { ++::fic::g_launches; FIC_CUDA(cudaGetLastError()); } while (0)
 
 inline void invalid(const std::string& msg) { throw Error{FIC_EINVAL, msg}; }

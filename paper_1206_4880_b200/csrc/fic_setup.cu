@@ -1220,19 +1220,19 @@ void launch_pool(const PoolArgs& a, cudaStream_t s) {
     dim3 grid((unsigned)cdiv(a.ndx, DR_COLS), (unsigned)cdiv(2 * a.mh, DR_ROWS));
     k_domrows<<<grid, 256, smem, s>>>(a.img, a.H, a.W, a.st, a.ndx, a.mh, a.trows);
     FIC_CHECK_LAUNCH();
-    if (a.ev_main) FIC_CUDA(cudaEventRecord(a.ev_main, s));
+    if (a.ev_main) FIC_CUDA(record_timing_event(a.ev_main, s));
     k_pool<8, true><<<blocks, 256, 0, s>>>(a);
   } else if ((a.rs == 8 || a.rs == 4) && a.planes) {
     dim3 grid((unsigned)cdiv(cdiv(a.W - 1, 16), 256), (unsigned)(a.H - 1));
     k_boxplanes<<<grid, 256, 0, s>>>(a.img, a.H, a.W, a.pitch, a.planes);
     FIC_CHECK_LAUNCH();
-    if (a.ev_main) FIC_CUDA(cudaEventRecord(a.ev_main, s));
+    if (a.ev_main) FIC_CUDA(record_timing_event(a.ev_main, s));
     if (a.rs == 8)
       k_pool<8, false><<<blocks, 256, 0, s>>>(a);
     else
       k_pool<4, false><<<blocks, 256, 0, s>>>(a);
   } else {
-    if (a.ev_main) FIC_CUDA(cudaEventRecord(a.ev_main, s));
+    if (a.ev_main) FIC_CUDA(record_timing_event(a.ev_main, s));
     k_pool_generic<<<blocks, 256, 0, s>>>(a, a.rs);
   }
   FIC_CHECK_LAUNCH();

@@ -616,3 +616,40 @@ def test_random_small_encodes_match_oracle(case):
     assert np.array_equal(_recs(res.records.cpu().numpy()), ref.records), c
     assert np.array_equal(res.pre_rms.cpu().numpy(), ref.pre_rms), c
     assert np.array_equal(res.post_rms.cpu().numpy(), ref.post_rms), c
+
+
+@pytest.mark.parametrize("cname", ["cfg1", "cfg2", "cfg4"])
+def test_graph_replay_rewrites_outputs_and_stats(cname):
+    """A call that repeats the previous one exactly (same image and output
+    buffers, parameters) is recorded as a CUDA graph and replayed: with the
+    outputs cleared before every call, each replay writes the same records
+    and RMS as the first (direct) call, and its stats are live."""
+    import torch
+
+    c = synth.CONFIGS[cname]
+    img = torch.from_numpy(c.make()).cuda()
+    n_r = (img.shape[0] // c.range_size) * (img.shape[1] // c.range_size)
+    out = codec.DeviceResult(torch.empty((n_r, 7), dtype=torch.uint8, device="cuda"),
+                             torch.empty(n_r, dtype=torch.float64, device="cuda"),
+                             torch.empty(n_r, dtype=torch.float64, device="cuda"),
+                             torch.empty(n_r, dtype=torch.int64, device="cuda"), {})
+    kw = dict(range_size=c.range_size, domain_size=c.domain_size, stride=c.stride,
+              isometries=True, delta=c.delta)
+    first, modes = None, []
+    for _ in range(5):  # direct (arena settling), record + launch, replays
+        for t in (out.records, out.pre_rms, out.post_rms, out.pool_sizes):
+            t.zero_()
+        r = codec.encode_device(img, c.strategy, out=out, **kw)
+        torch.cuda.synchronize()
+        cur = (r.records.clone(), r.pre_rms.clone(), r.post_rms.clone(), r.pool_sizes.clone())
+        assert r.stats["ms_total"] > 0 and r.stats["comparisons"] > 0
+        modes.append(int(r.stats["graph"]))
+        if first is None:
+            first = cur
+        else:
+            for a, b in zip(first, cur):
+                assert torch.equal(a, b)
+    # direct until a call repeats the previous one with a settled arena (the
+    # arena grows on the second call), then recorded once and replayed
+    assert modes[0] == 0 and modes[-2:] == [1, 2] or modes[-2:] == [2, 2], modes
+    assert 1 in modes and modes[-1] == 2, modes
