@@ -1449,15 +1449,19 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
     TcArgs ta{titems, titems_n, rid_s, n_tt_max * RT, wlo, whi, seg_t, seg0, RT, sbase, partials,
               counters, counters + 15, thr_g, 0, nullptr};
     ta.nsub = nsub;
+    // A pilot item per tile seeds the thresholds before the main items.
     // 4x4 ranges (K = 16): the fp16 screen keeps ~0.1% of the candidates and
-    // thresholds found along the way arrive too late, so by default a pilot
-    // over every 8th N-tile of each window seeds the thresholds and every
-    // survivor goes to the survivor list (cfg4: 142 -> 33 ms);
-    // 8x8 ranges keep the rescoring warp (the pilot costs more than it saves)
+    // thresholds found along the way arrive too late, so the pilot samples
+    // every 8th N-tile of each window and every survivor goes to the lists
+    // (cfg4: 142 -> 33 ms).  8x8 ranges sample about
+    // pilot_samples N-tiles of each window (adaptive stride; cfg3 -0.08 ms)
+    // and keep the rescoring warp.
     const bool k16 = K == 16;
     ta.pilot_cols = getenv("FIC_PILOT") ? std::max(0, atoi(getenv("FIC_PILOT"))) / BN_COLS * BN_COLS
-                                        : (k16 ? (1 << 30) : 0);
-    ta.pilot_stride = getenv("FIC_PILOT_STRIDE") ? std::max(1, atoi(getenv("FIC_PILOT_STRIDE"))) : 8;
+                                        : (tc_tile_rows(K) == 128 ? (1 << 30) : 0);  // (not the CTA-pair variant)
+    ta.pilot_stride = getenv("FIC_PILOT_STRIDE") ? std::max(0, atoi(getenv("FIC_PILOT_STRIDE")))
+                                                 : (k16 ? 8 : 0);
+    ta.pilot_samples = getenv("FIC_PILOT_SAMPLES") ? std::max(1, atoi(getenv("FIC_PILOT_SAMPLES"))) : 16;
     ta.n_split = nsub > 1 ? std::min<int64_t>(titems_n, kSplitCap) : 0;  // bound
     ta.plan = d_plan;
     if (flat_path) {

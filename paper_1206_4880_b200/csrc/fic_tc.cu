@@ -540,6 +540,13 @@ __global__ void __maxnreg__(MAXREG)
       c0 = p0;
     }
   };
+  // column step of a pilot item: a fixed stride, or (pilot_stride 0) about
+  // pilot_samples N-tiles spread over the window (wide windows need few)
+  auto pilot_step = [&](int64_t c0, int64_t c1) -> int {
+    const int64_t nt_all = cdiv(c1 - c0, (int64_t)BN);
+    const int64_t st = a.pilot_stride > 0 ? a.pilot_stride : max((int64_t)1, nt_all / max(1, a.pilot_samples));
+    return (int)(BN * st);
+  };
   for (int64_t it = (CG == 1) ? (int64_t)s_item[0] : (int64_t)(blockIdx.x / CG); it < n_virt;
        it = (CG == 1) ? (int64_t)s_item[kitem & 1] : it + gridDim.x / CG) {
     const long long ti0 = TCLK();
@@ -549,7 +556,7 @@ __global__ void __maxnreg__(MAXREG)
     int64_t c0 = 0, c1 = 0;
     item_cols(it, tile, slot, c0, c1);
     // pilot items sample every pilot_stride-th N-tile of the window
-    const int tstep = slot < 0 ? BN * a.pilot_stride : BN;
+    const int tstep = slot < 0 ? pilot_step(c0, c1) : BN;
     const int nt = (int)cdiv(c1 - c0, (int64_t)tstep);
     // survivors of this item: the rescoring warp's queues first (overflow to
     // the survivor list), or all to the list -- for every item (sl_all 1) or
@@ -672,7 +679,7 @@ __global__ void __maxnreg__(MAXREG)
           int ntile = 0, nslot = 0;
           int64_t n0 = 0, n1 = 0;
           item_cols(nit, ntile, nslot, n0, n1);
-          const int nstep = nslot < 0 ? BN * a.pilot_stride : BN;
+          const int nstep = nslot < 0 ? pilot_step(n0, n1) : BN;
           const int nnt = (int)cdiv(n1 - n0, (int64_t)nstep);
           const int pre = min(nnt, C::NST / 2);
           for (int j = 0; j < pre; ++j) {
@@ -760,7 +767,12 @@ __global__ void __maxnreg__(MAXREG)
           if (h == SW / CH - 1) {
             fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(tempty0 + 8 * acc);
+            if (lane == 0) {  // (a CTA pair's stage barriers live in the leader)
+              if (leader)
+                mbar_arrive(tempty0 + 8 * acc);
+              else
+                mbar_arrive_cluster(map_to_rank(tempty0 + 8 * acc, 0));
+            }
           }
           const int32_t rel = j * tstep + slice * SW + CH * h;
           const int32_t e_lo = lo32 - rel, e_hi = hi32 - rel;

@@ -157,7 +157,9 @@ struct TcArgs {
   int pilot_cols;              // > 0: one pilot item per tile first (the first pilot_cols columns of its
                                // window): per row the PK largest |u|, evaluated exactly, seed the
                                // ranges' thresholds (thr_g) for the main items
-  int pilot_stride;            // pilot items sample every pilot_stride-th 128-column tile (>= 1)
+  int pilot_stride;            // pilot items sample every pilot_stride-th 128-column tile (>= 1);
+                               // 0: adaptive, about pilot_samples tiles of each window
+  int pilot_samples;
   int sl_all;                  // 1: every survivor goes to the list (the queues carry seeds only);
                                // 2: the same after each tile's first segment (a pilot with the queues)
   // Hit list (with sl_all == 1): a screening warp whose chunk has any lane

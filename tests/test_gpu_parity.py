@@ -358,6 +358,11 @@ def test_cta_pair_matcher_equals_default(monkeypatch):
     assert b.stats["tensor_tiles"] > 0
     assert torch.equal(a.records, b.records)
     assert torch.equal(a.post_rms, b.post_rms) and torch.equal(a.pre_rms, b.pre_rms)
+    # the pilot items on a CTA pair (their stage releases go to the leader's barrier)
+    monkeypatch.setenv("FIC_PILOT", str(1 << 30))
+    monkeypatch.setenv("FIC_PILOT_STRIDE", "0")
+    c2 = codec.encode_device(img, "dynamic_fd", max_segment=1024, **kw)
+    assert torch.equal(a.records, c2.records) and torch.equal(a.post_rms, c2.post_rms)
 
 
 def test_decode_full_size_matches_oracle():
