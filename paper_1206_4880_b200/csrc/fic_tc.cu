@@ -83,12 +83,21 @@ constexpr int CH = 64;        // TMEM columns per screening chunk (tcgen05.ld x3
 #ifndef FIC_TC_WIDE
 #define FIC_TC_WIDE 0
 #endif
-constexpr bool WIDE = FIC_TC_WIDE;  // load a whole stage before screening (needs ~170 registers)
+constexpr bool WIDE = FIC_TC_WIDE;
+#ifndef FIC_TC_F16ACC
+#define FIC_TC_F16ACC 0
+#endif
+// f16 accumulators for the main (non-pilot) items: a whole 128-column stage is
+// read back with ONE packed tcgen05.ld (64 registers, two columns each) and
+// screened with packed 3-input |x| max (VHMNMX); eps widens by the f16
+// roundings of the K/16 accumulation steps
+constexpr bool F16ACC = FIC_TC_F16ACC;
+static_assert(!F16ACC || (BN == 128 && NSPLIT == 1 && !WIDE), "f16 accumulators: one packed load per 128-column stage");  // load a whole stage before screening (needs ~170 registers)
 // Parity waits are only sound if a waiter can never be two phases ahead of a
 // barrier: a group must own fixed accumulator stages (NGRP divides NACC).
 static_assert(NACC % NGRP == 0, "screening groups must own whole accumulator stages");
 static_assert((BN / NSPLIT) % CH == 0 && CH % 32 == 0, "slices hold whole chunks of x32 loads");
-constexpr int QCAP = 32;      // survivor queue entries per (row, slice)
+constexpr int QCAP = NSLICE > 2 ? 16 : 32;  // survivor queue entries per (row, slice); the queues fit 227 KB
 constexpr uint32_t SLCH = 512;  // survivor-list entries per screening-warp chunk
 constexpr uint32_t HLCH = 256;  // hit-list entries per screening-warp chunk
 constexpr int PK = 8;         // pilot: |u| candidates kept per row and screening group (4x4 ranges)
@@ -190,25 +199,27 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t sbo, uint3
   return d;
 }
 
-// kind::f16 instruction descriptor: D f32, A/B f16, both K-major, M = 128*CG, N = BN.
+// kind::f16 instruction descriptor: D f32 (f16d: D f16, one value per 32-bit
+// TMEM column), A/B f16, both K-major, M = 128*CG, N = BN.
 template <int CG>
-__device__ __forceinline__ constexpr uint32_t idesc() {
-  return (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)((BM * CG) >> 4) << 24);
+__device__ __forceinline__ constexpr uint32_t idesc(bool f16d = false) {
+  return ((f16d ? 0u : 1u) << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)((BM * CG) >> 4) << 24);
 }
 
 template <int CG>
-__device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t acc) {
+__device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t acc,
+                                        uint32_t id) {
   if constexpr (CG == 1)
     asm volatile(
         "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
         " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
-        "l"(a), "l"(b), "r"(idesc<1>()), "r"(acc)
+        "l"(a), "l"(b), "r"(id), "r"(acc)
         : "memory");
   else
     asm volatile(
         "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
         " tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
-        "l"(a), "l"(b), "r"(idesc<2>()), "r"(acc)
+        "l"(a), "l"(b), "r"(id), "r"(acc)
         : "memory");
 }
 
@@ -282,6 +293,16 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
         "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
         "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
         "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr)
+      : "memory");
+}
+
+// 128 columns of f16 accumulators (D format f16: one value per 32-bit TMEM
+// column) as 64 registers, columns 2e | 2e+1 << 16 in register e
+__device__ __forceinline__ void tmem_ld64p(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x64.pack::16b.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32,%33,%34,%35,%36,%37,%38,%39,%40,%41,%42,%43,%44,%45,%46,%47,%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63}, [%64];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31]), "=r"(r[32]), "=r"(r[33]), "=r"(r[34]), "=r"(r[35]), "=r"(r[36]), "=r"(r[37]), "=r"(r[38]), "=r"(r[39]), "=r"(r[40]), "=r"(r[41]), "=r"(r[42]), "=r"(r[43]), "=r"(r[44]), "=r"(r[45]), "=r"(r[46]), "=r"(r[47]), "=r"(r[48]), "=r"(r[49]), "=r"(r[50]), "=r"(r[51]), "=r"(r[52]), "=r"(r[53]), "=r"(r[54]), "=r"(r[55]), "=r"(r[56]), "=r"(r[57]), "=r"(r[58]), "=r"(r[59]), "=r"(r[60]), "=r"(r[61]), "=r"(r[62]), "=r"(r[63])
       : "r"(taddr)
       : "memory");
 }
@@ -629,6 +650,10 @@ __global__ void __maxnreg__(MAXREG)
           double an = (double)((int64_t)srr - 2 * (int64_t)inf.rho * (int64_t)sr +
                                (int64_t)K * inf.rho * inf.rho);
           eps = (0x1p-11 + 0x1p-12 + 0x1p-13) * sqrt(an) + (double)K * 510.0 * 0x1p-24 + 1e-6;
+          // f16 accumulators: each of the K/16 steps returns an f16 neighbour of
+          // its sum (|sum| <= ||a|| ||B||, one ulp = 2^-10 relative; 2^-24 below
+          // the normal range), plus the final value's own rounding
+          if (F16ACC) eps += (double)(K / 16 + 1) * (0x1p-10 * (1.0 + 0x1p-10) * sqrt(an) + 0x1p-24);
         } else {
           rlo = rhi = 0;
         }
@@ -717,7 +742,7 @@ __global__ void __maxnreg__(MAXREG)
           const uint64_t bs = bdesc + (uint64_t)((stage * C::B_BYTES) >> 4);
 #pragma unroll
           for (int kk = 0; kk < K / 16; ++kk)
-            if (!(debug & 2)) mma_f16<CG>(d, adesc + 2 * kk, bs + 2 * kk, kk > 0 ? 1u : 0u);
+            if (!(debug & 2)) mma_f16<CG>(d, adesc + 2 * kk, bs + 2 * kk, kk > 0 ? 1u : 0u, idesc<CG>(F16ACC && !pil));
           mma_commit<CG>(empty0 + 8 * stage);
           mma_commit<CG>(tfull0 + 8 * acc);
         }
@@ -1078,7 +1103,56 @@ __global__ void __maxnreg__(MAXREG)
               mbar_arrive_cluster(map_to_rank(tempty0 + 8 * acc, 0));
           }
         };
-        if constexpr (WIDE) {
+        if (F16ACC && !pil) {
+          // f16 accumulators: the whole stage in 64 registers with one load
+          // and one wait, released at once; packed 3-input |x| max per
+          // 64-column chunk; a hit chunk is unpacked to fp32 for the hit path
+          uint32_t pk[BN / 2];
+          if (!(debug & 1)) tmem_ld64p(lane_base + acc * BN, pk);
+          tmem_wait_ld();
+          release();
+          if (debug & 1) continue;
+          auto chunk_max_h = [&](const uint32_t* r) {
+            auto hv = [&](int e) { return __habs2(*reinterpret_cast<const __half2*>(r + e)); };
+            __half2 m0 = __hmax2(__hmax2(hv(0), hv(1)), hv(2));
+            __half2 m1 = __hmax2(__hmax2(hv(3), hv(4)), hv(5));
+            __half2 m2 = __hmax2(__hmax2(hv(6), hv(7)), hv(8));
+            __half2 m3 = __hmax2(__hmax2(hv(9), hv(10)), hv(11));
+#pragma unroll
+            for (int e = 12; e < 28; e += 8) {
+              m0 = __hmax2(__hmax2(m0, hv(e)), hv(e + 1));
+              m1 = __hmax2(__hmax2(m1, hv(e + 2)), hv(e + 3));
+              m2 = __hmax2(__hmax2(m2, hv(e + 4)), hv(e + 5));
+              m3 = __hmax2(__hmax2(m3, hv(e + 6)), hv(e + 7));
+            }
+            m0 = __hmax2(__hmax2(m0, hv(28)), hv(29));
+            m1 = __hmax2(__hmax2(m1, hv(30)), hv(31));
+            const __half2 mm = __hmax2(__hmax2(m0, m1), __hmax2(m2, m3));
+            return fmaxf(__low2float(mm), __high2float(mm));
+          };
+          float mx[BN / CH];
+#pragma unroll
+          for (int h = 0; h < BN / CH; ++h) mx[h] = chunk_max_h(pk + (CH / 2) * h);
+#pragma unroll
+          for (int h = 0; h < BN / CH; ++h) {
+            const int32_t rel = j * BN + CH * h;
+            const int32_t e_lo = lo32 - rel, e_hi = hi32 - rel;
+            const bool in_window = (uint32_t)(e_hi - 1) < (uint32_t)(hi32 - lo32 + CH - 1);
+            const bool hit = !(debug & 8) & in_window & !rflat & (mx[h] >= s_r);
+            if (__any_sync(0xffffffffu, hit)) {
+              // (converting inside the hit path instead of this fp32 copy
+              // spilled in the screening loop: 5.65 -> 6.26 ms at cfg3)
+              float v[CH];
+#pragma unroll
+              for (int e = 0; e < CH / 2; ++e) {
+                const float2 f = __half22float2(*reinterpret_cast<const __half2*>(pk + (CH / 2) * h + e));
+                v[2 * e] = f.x;
+                v[2 * e + 1] = f.y;
+              }
+              on_hit(v, rel, e_lo, e_hi, hit);
+            }
+          }
+        } else if constexpr (WIDE) {
           // the whole stage in registers: loads, release, independent chunk maxima
           float v[SW];
           if (!(debug & 1)) {
