@@ -50,7 +50,7 @@ __device__ __forceinline__ void ld32(uint32_t taddr, uint32_t* r) {
 }
 
 // NACC stages of N columns; NGRP screening groups; LD: 0 no loads, 1 loads + max
-template <int N, int NACC, int NGRP, int LD, int SLEEP, int NMMA, int PROD, int RES, int EXTRA>
+template <int N, int NACC, int NGRP, int LD, int SLEEP, int NMMA, int PROD, int RES, int EXTRA, int KS>
 __global__ void k(int tiles, unsigned long long* out, float* sink) {
   extern __shared__ __align__(1024) uint8_t sm[];
   __shared__ uint32_t holder;
@@ -105,7 +105,7 @@ __global__ void k(int tiles, unsigned long long* out, float* sink) {
       if (elect_one()) {
         const uint64_t bs = bdesc + (uint64_t)(((j & 1) * N * 128 / 16) & 4095);
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk)
+        for (int kk = 0; kk < KS; ++kk)
           asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n"
                        ::"r"(tbase + s * N), "l"(adesc + 2 * kk), "l"(bs + 2 * kk), "r"(idesc), "r"(kk));
         if (PROD) asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(empty0 + 8 * (j & 7)));
@@ -180,10 +180,10 @@ __global__ void k(int tiles, unsigned long long* out, float* sink) {
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tbase));
 }
 
-template <int N, int NACC, int NGRP, int LD, int SLEEP, int NMMA, int PROD = 0, int RES = 0, int EXTRA = 0>
+template <int N, int NACC, int NGRP, int LD, int SLEEP, int NMMA, int PROD = 0, int RES = 0, int EXTRA = 0, int KS = 4>
 void run(int tiles, unsigned long long* d, float* sink) {
   const int smem = 1024 + 16384 + 65536;
-  auto fn = k<N, NACC, NGRP, LD, SLEEP, NMMA, PROD, RES, EXTRA>;
+  auto fn = k<N, NACC, NGRP, LD, SLEEP, NMMA, PROD, RES, EXTRA, KS>;
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const int threads = 32 * (3 + NMMA + 4 * NGRP);
   for (int rep = 0; rep < 2; ++rep) {
@@ -194,7 +194,7 @@ void run(int tiles, unsigned long long* d, float* sink) {
   unsigned long long cyc;
   cudaMemcpy(&cyc, d, 8, cudaMemcpyDeviceToHost);
   const double per_tile = (double)cyc / tiles;
-  printf("res=%d extra=%d prod=%d N=%3d nacc=%d ngrp=%d ld=%d %s nmma=%d: %7.1f cycles/tile (MMA %4d, %3.0f%%) per 128 cols %6.1f %s\n", RES, EXTRA, PROD, N, NACC,
+  printf("ksteps=%d res=%d extra=%d prod=%d N=%3d nacc=%d ngrp=%d ld=%d %s nmma=%d: %7.1f cycles/tile (MMA %4d, %3.0f%%) per 128 cols %6.1f %s\n", KS, RES, EXTRA, PROD, N, NACC,
          NGRP, LD, SLEEP ? "sleep" : "spin ", NMMA, per_tile, N * 2, 100.0 * N * 2 / per_tile, per_tile * 128 / N,
          cudaGetErrorString(cudaGetLastError()));
 }
@@ -205,10 +205,14 @@ int main(int argc, char** argv) {
   cudaMalloc(&d, 16);
   cudaMalloc(&sink, 148 * 1024 * 4);
   const int tiles = argc > 1 ? atoi(argv[1]) : 8000;
-  run<128, 4, 2, 1, 1, 2, 1>(tiles, d, sink);
-  run<128, 4, 2, 1, 1, 2, 1, 1>(tiles, d, sink);
   run<128, 4, 2, 1, 1, 2, 1, 0, 1>(tiles, d, sink);
-  run<128, 4, 2, 1, 1, 2, 1, 1, 1>(tiles, d, sink);
-  run<128, 4, 3, 1, 1, 2, 1, 1, 1>(tiles, d, sink);
+  // K = 16 (one MMA step per tile): screening groups 1 / 2 / 4, and without loads
+  run<128, 4, 1, 1, 1, 2, 1, 0, 1, 1>(tiles, d, sink);
+  run<128, 4, 2, 1, 1, 2, 1, 0, 1, 1>(tiles, d, sink);
+  run<128, 4, 4, 1, 1, 2, 1, 0, 1, 1>(tiles, d, sink);
+  run<128, 4, 2, 0, 1, 2, 1, 0, 1, 1>(tiles, d, sink);
+  run<128, 4, 4, 0, 1, 2, 1, 0, 1, 1>(tiles, d, sink);
+  run<64, 8, 4, 1, 1, 2, 1, 0, 1, 1>(tiles, d, sink);
+  run<64, 8, 8, 1, 1, 2, 1, 0, 1, 1>(tiles, d, sink);
   return 0;
 }
