@@ -87,6 +87,9 @@ constexpr bool WIDE = FIC_TC_WIDE;
 #ifndef FIC_TC_F16ACC
 #define FIC_TC_F16ACC 0
 #endif
+#ifndef FIC_TC_LEAN
+#define FIC_TC_LEAN 0  // 1: experiment, 4x4 main items without the slow path (hit list only)
+#endif
 // f16 accumulators for the main (non-pilot) items: a whole 128-column stage is
 // read back with ONE packed tcgen05.ld (64 registers, two columns each) and
 // screened with packed 3-input |x| max (VHMNMX); eps widens by the f16
@@ -1073,6 +1076,14 @@ __global__ void __maxnreg__(MAXREG)
         };
         auto on_hit = [&](const float* v, int32_t rel, int32_t e_lo, int32_t e_hi, bool hit) {
           // (4x4 ranges only: the 8x8 screeners keep their registers)
+#if FIC_TC_LEAN
+          // experiment: 4x4 main items append every hit chunk to the hit list
+          // (rows without a threshold hit on every chunk), no slow path
+          if (K == 16 && a.hl && !pil) {
+            hl_append(rel, hit);
+            return;
+          }
+#endif
           if (hl_ok(hit) && hl_append(rel, hit)) return;
           slow_path(v, rel, e_lo, e_hi, hit);
         };
