@@ -493,7 +493,8 @@ def run_ours(args):
     parity = _parity_vs_reference(recs.cpu().numpy(), pre.cpu().numpy(), post.cpu().numpy())
     # e2e through the public API: host image in, host records/RMS out
     e2e_times = []
-    for i in range(max(1, args.steps // 2) + 1):
+    e2e_warm = 3  # direct call, graph recording, first replay (the timing rules' W >= 3)
+    for i in range(max(1, args.steps // 2) + e2e_warm):
         barrier()
         t0 = time.perf_counter()
         if not dist_on:
@@ -503,7 +504,7 @@ def run_ours(args):
             recs, pre, post, pools, _ = encode_sharded(di, "dynamic_fd", **CFG)
             recs.cpu(), pre.cpu(), post.cpu(), pools.cpu()
         barrier()
-        if i:  # first call is a warm-up
+        if i >= e2e_warm:
             e2e_times.append(time.perf_counter() - t0)
     e2e_s = float(np.mean(e2e_times))
     if dist_on:

@@ -658,3 +658,53 @@ def test_graph_replay_rewrites_outputs_and_stats(cname):
     # arena grows on the second call), then recorded once and replayed
     assert modes[0] == 0 and modes[-2:] == [1, 2] or modes[-2:] == [2, 2], modes
     assert 1 in modes and modes[-1] == 2, modes
+
+
+@pytest.mark.parametrize("cname", ["cfg1", "cfg2", "cfg4"])
+def test_graph_replay_follows_image_content(cname):
+    """A replayed graph reads the image buffer anew: after the buffer's
+    content changes in place (another seed, a transposed image, an image with
+    flat areas, a constant image), the replay's records / RMS / pool sizes /
+    comparisons equal a direct (graph-free: any FIC_* variable set) encode
+    of a copy of that content."""
+    import os
+
+    import torch
+
+    c = synth.CONFIGS[cname]
+    base = c.make()
+    n_r = (base.shape[0] // c.range_size) * (base.shape[1] // c.range_size)
+    buf = torch.from_numpy(base).cuda()
+    out = codec.DeviceResult(torch.empty((n_r, 7), dtype=torch.uint8, device="cuda"),
+                             torch.empty(n_r, dtype=torch.float64, device="cuda"),
+                             torch.empty(n_r, dtype=torch.float64, device="cuda"),
+                             torch.empty(n_r, dtype=torch.int64, device="cuda"), {})
+    kw = dict(range_size=c.range_size, domain_size=c.domain_size, stride=c.stride,
+              isometries=True, delta=c.delta)
+    for _ in range(4):
+        r = codec.encode_device(buf, c.strategy, out=out, **kw)
+    torch.cuda.synchronize()
+    assert int(r.stats["graph"]) == 2
+    gen = {"cfg1": synth.cfg1_image, "cfg2": synth.cfg2_image, "cfg4": synth.cfg4_image}[cname]
+    half_flat = base.copy()
+    half_flat[: base.shape[0] // 2] = 97
+    variants = [gen(seed=77), np.ascontiguousarray(base.T), half_flat,
+                np.full_like(base, 200), base]
+    for v in variants:
+        buf.copy_(torch.from_numpy(v).cuda())
+        for t in (out.records, out.pre_rms, out.post_rms, out.pool_sizes):
+            t.zero_()
+        r = codec.encode_device(buf, c.strategy, out=out, **kw)
+        torch.cuda.synchronize()
+        assert int(r.stats["graph"]) == 2
+        os.environ["FIC_NO_GRAPH"] = "1"
+        try:
+            d = codec.encode_device(torch.from_numpy(v).cuda(), c.strategy, **kw)
+            torch.cuda.synchronize()
+        finally:
+            os.environ.pop("FIC_NO_GRAPH", None)
+        assert int(d.stats["graph"]) == 0
+        assert torch.equal(r.records, d.records)
+        assert torch.equal(r.pre_rms, d.pre_rms) and torch.equal(r.post_rms, d.post_rms)
+        assert torch.equal(r.pool_sizes, d.pool_sizes)
+        assert r.stats["comparisons"] == d.stats["comparisons"]
