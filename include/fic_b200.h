@@ -184,6 +184,16 @@ int fic_shard_pack_v1(const uint8_t* d_records, const double* d_pre_rms, const d
 int fic_shard_unpack_v1(const int64_t* d_buf, int64_t n, uint8_t* d_records, double* d_pre_rms,
                         double* d_post_rms, uint32_t* d_bad, void* stream);
 
+/* Diagnostic: with FIC_ARENA_GUARD set in the environment every scratch buffer
+ * of a call is followed by a red zone that is verified after the call's
+ * kernels (a write check for boxes without compute-sanitizer; the call fails
+ * with FIC_ECUDA and a message naming the buffer).  This entry exercises the
+ * check itself on the current device: a 1000-byte scratch buffer is filled
+ * with `overrun` extra bytes.  Returns FIC_OK when the zones are intact (or
+ * the guard is off), FIC_ECUDA when the overrun was caught.  No reference
+ * counterpart (the reference is pure numpy). */
+int fic_guard_selftest_v1(int32_t overrun);
+
 const char* fic_last_error(void);
 int fic_abi_version(void);
 /* Releases cached device workspaces of the calling thread's current device. */

@@ -77,8 +77,8 @@ class FicStats(ctypes.Structure):
 
 # every symbol include/fic_b200.h declares
 EXPORTS = ("fic_encode_v1", "fic_plan_v1", "fic_pool_v1", "fic_dbc_v1", "fic_decode_v1",
-           "fic_decode_step_v1", "fic_shard_pack_v1", "fic_shard_unpack_v1", "fic_last_error",
-           "fic_abi_version", "fic_release")
+           "fic_decode_step_v1", "fic_shard_pack_v1", "fic_shard_unpack_v1",
+           "fic_guard_selftest_v1", "fic_last_error", "fic_abi_version", "fic_release")
 
 _lib = None
 
@@ -108,6 +108,8 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     for name in ("fic_encode_v1", "fic_plan_v1", "fic_pool_v1", "fic_dbc_v1", "fic_decode_v1",
                  "fic_decode_step_v1", "fic_shard_pack_v1", "fic_shard_unpack_v1"):
         getattr(lib, name).restype = ctypes.c_int
+    lib.fic_guard_selftest_v1.argtypes = [i32]
+    lib.fic_guard_selftest_v1.restype = ctypes.c_int
     lib.fic_last_error.restype = ctypes.c_char_p
     lib.fic_last_error.argtypes = []
     lib.fic_abi_version.restype = ctypes.c_int

@@ -11,6 +11,7 @@
 #include <map>
 #include <mutex>
 #include <set>
+#include <stdexcept>
 #include <tuple>
 #include <vector>
 
@@ -57,7 +58,7 @@ static thread_local std::map<std::pair<int, cudaStream_t>, Arena> g_arenas;
 
 class Scratch {
  public:
-  explicit Scratch(cudaStream_t s) : s_(s) {
+  explicit Scratch(cudaStream_t s) : s_(s), guard_(getenv("FIC_ARENA_GUARD") != nullptr) {
     // keep freed blocks cached in the device's default pool (once per device)
     static std::mutex mu;
     static std::set<int> done;
@@ -110,24 +111,62 @@ class Scratch {
   template <class T>
   T* get(size_t n) {
     if (n == 0) n = 1;
-    const size_t bytes = align_up(n * sizeof(T), 256);
+    // FIC_ARENA_GUARD (a home-made write check; compute-sanitizer is not
+    // available on every box): each buffer is followed by a red zone -- its
+    // alignment slack plus GUARD bytes -- filled with a pattern that verify()
+    // expects to find intact after the call's kernels
+    const size_t bytes = align_up(n * sizeof(T), 256) + (guard_ ? GUARD : 0);
     used_ += bytes;
+    char* p = nullptr;
     if (arena_ && off_ + bytes <= arena_->cap) {
-      T* p = reinterpret_cast<T*>(arena_->base + off_);
+      p = arena_->base + off_;
       off_ += bytes;
-      return p;
+    } else {  // beyond the arena: a pool allocation freed at the end
+      FIC_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), bytes, s_));
+      ptrs_.push_back(p);
     }
-    void* p = nullptr;  // beyond the arena: a pool allocation freed at the end
-    FIC_CUDA(cudaMallocAsync(&p, bytes, s_));
-    ptrs_.push_back(p);
-    return static_cast<T*>(p);
+    if (guard_) {
+      const size_t live = align_up(n * sizeof(T), 16);  // vector stores may round a tail up to 16 B
+      FIC_CUDA(cudaMemsetAsync(p + live, 0xA5, bytes - live, s_));
+      zones_.push_back({p + live, bytes - live, n * sizeof(T)});
+    }
+    return reinterpret_cast<T*>(p);
   }
+  // FIC_ARENA_GUARD: every red zone still holds its pattern (call with the
+  // call's streams synchronised); throws naming the buffer otherwise
+  void verify(const char* what) {
+    if (!guard_) return;
+    std::vector<unsigned char> h;
+    for (size_t i = 0; i < zones_.size(); ++i) {
+      const Zone& z = zones_[i];
+      h.resize(z.len);
+      FIC_CUDA(cudaMemcpy(h.data(), z.at, z.len, cudaMemcpyDeviceToHost));
+      for (size_t k = 0; k < z.len; ++k)
+        if (h[k] != 0xA5) {
+          char msg[200];
+          snprintf(msg, sizeof(msg),
+                   "FIC_ARENA_GUARD: %s wrote past scratch buffer #%zu (%zu bytes): red-zone byte +%zu = 0x%02x",
+                   what, i, z.size, k, (unsigned)h[k]);
+          throw std::runtime_error(msg);
+        }
+    }
+    guard_checked_ += zones_.size();
+  }
+  size_t guard_checked() const { return guard_checked_; }
 
  private:
+  static constexpr size_t GUARD = 256;
+  struct Zone {
+    const char* at;
+    size_t len, size;
+  };
   cudaStream_t s_;
   Arena* arena_ = nullptr;
   size_t off_ = 0, used_ = 0;
   std::vector<void*> ptrs_;
+  bool guard_ = false;
+  std::vector<Zone> zones_;
+  size_t guard_checked_ = 0;
 };
 
 struct Timer {
@@ -1700,6 +1739,7 @@ static void encode_impl(const uint8_t* img, int H, int W, const fic_params_t& p,
     FIC_CUDA(cudaEventRecord(tm.ev[23], s));  // end of the flat fix-up (event 23: not a plan mark)
     FIC_CUDA(cudaStreamSynchronize(s));
   }
+  sc.verify("encode");
   if (ptime && pn == 15) {
     fprintf(stderr, "plan timing (ms): fd %.3f pool(side) %.3f | fork %.3f - %.3f classify..shard %.3f sync1 %.3f "
             "tiles..totals %.3f sync2 %.3f items %.3f | tensor %.3f exact %.3f merge %.3f readback %.3f | seed rounds %llu hit rounds %llu hit lanes %llu\n",
@@ -1808,6 +1848,7 @@ static void pool_impl(const uint8_t* img, int H, int W, const fic_params_t& p, i
   if (b_rows)
     FIC_CUDA(cudaMemcpyAsync(b_rows, pa.bh, (size_t)g.D * K * 2, cudaMemcpyDeviceToDevice, s));
   FIC_CUDA(cudaStreamSynchronize(s));
+  sc.verify("pool");
 }
 
 static void plan_impl(const uint8_t* img, int H, int W, const fic_params_t& p, double* fd_dom,
@@ -1840,6 +1881,7 @@ static void plan_impl(const uint8_t* img, int H, int W, const fic_params_t& p, d
   double hs[4];
   FIC_CUDA(cudaMemcpyAsync(hs, pb.scal, sizeof(hs), cudaMemcpyDeviceToHost, s));
   FIC_CUDA(cudaStreamSynchronize(s));
+  sc.verify("plan");
   if (st) {
     std::memset(st, 0, sizeof(*st));
     st->n_ranges = g.R;
@@ -1980,6 +2022,7 @@ static void decode_impl(const uint8_t* rec, int H, int W, int rs, int ds, int st
     std::swap(w0, w1);
   }
   FIC_CUDA(cudaStreamSynchronize(s));
+  sc.verify("decode");
 }
 
 static void decode_step_impl(const uint8_t* rec, int H, int W, int rs, int ds, int st,
@@ -2095,6 +2138,7 @@ extern "C" int fic_dbc_v1(const uint8_t* d_blocks, int64_t n, int32_t side, int3
     fa.fd = d_fd;
     launch_fd(fa, s);
     FIC_CUDA(cudaStreamSynchronize(s));
+    sc.verify("dbc");
   });
 }
 
@@ -2140,6 +2184,20 @@ extern "C" int fic_shard_unpack_v1(const int64_t* d_buf, int64_t n, uint8_t* d_r
     k_shard_unpack<<<(unsigned)cdiv(n, 256), 256, 0, as_stream(stream)>>>(
         reinterpret_cast<const unsigned long long*>(d_buf), n, d_records, d_pre_rms, d_post_rms, d_bad);
     FIC_CHECK_LAUNCH();
+  });
+}
+
+extern "C" int fic_guard_selftest_v1(int32_t overrun) {
+  return guarded([&] {
+    if (overrun < 0 || overrun > 64) invalid("overrun must be in [0, 64]");
+    cudaStream_t s = nullptr;
+    Scratch sc(s);
+    uint8_t* a = sc.get<uint8_t>(1000);
+    uint8_t* b = sc.get<uint8_t>(1000);
+    FIC_CUDA(cudaMemsetAsync(a, 1, 1000 + (size_t)(overrun > 0 ? 8 + overrun : 0), s));  // past the 16-byte tail slack
+    FIC_CUDA(cudaMemsetAsync(b, 2, 1000, s));
+    FIC_CUDA(cudaStreamSynchronize(s));
+    sc.verify("selftest");
   });
 }
 
