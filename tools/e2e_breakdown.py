@@ -44,4 +44,5 @@ for _ in range(20):
     t4 = time.perf_counter()
     P.append((t1 - t0, t2 - t1, t3 - t2, t4 - t3, res.stats["ms_total"] / 1e3))
 P = np.array(P).mean(0) * 1e3
-print("staging %.3f | encode_device %.3f (device %.3f) | D2H+sync %.3f | host copies %.3f ms" % tuple(P))
+print("staging %.3f | encode_device %.3f (device %.3f) | D2H+sync %.3f | host copies %.3f ms"
+      % (P[0], P[1], P[4], P[2], P[3]))
