@@ -154,6 +154,12 @@ int fic_pool_v1(const uint8_t* d_image, int32_t height, int32_t width,
 int fic_dbc_v1(const uint8_t* d_blocks, int64_t n, int32_t side, int32_t clamp,
                const double* h_ln_table, int32_t ln_len, const double* h_weights,
                int32_t n_weights, double* d_fd, void* stream);
+/* The same with the reference's gray_levels argument (fdim.py:45, 74: box
+ * height h = s * gray_levels / side); fic_dbc_v1 is gray_levels = 256. */
+int fic_dbc_v2(const uint8_t* d_blocks, int64_t n, int32_t side, int32_t gray_levels,
+               int32_t clamp,
+               const double* h_ln_table, int32_t ln_len, const double* h_weights,
+               int32_t n_weights, double* d_fd, void* stream);
 
 /* Replaces fic.codec.decode (codec.py:516-598): `iterations` passes from a
  * constant gray level `initial` (128 in the reference), or from d_initial

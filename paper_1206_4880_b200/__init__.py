@@ -3,7 +3,8 @@
 Public names mirror the reference package ``fic`` for the rebuilt path:
 ``encode``, ``decode``, ``decode_iterates``, ``serialize``, ``deserialize``,
 ``FractalCode``, ``EncodeStats``, ``FormatError``, ``RECORD_DTYPE``,
-``dbc_grid``, ``fit_transform``, ``quantize_so``, ``dequantize_so``.
+``dbc_grid``, ``dbc_dimension``, ``dbc_dimension_raw``, ``fd_stats``, ``FdStats``,
+``scale_set``, ``fit_transform``, ``quantize_so``, ``dequantize_so``.
 """
 
 from .codec import (  # noqa: F401
@@ -11,8 +12,11 @@ from .codec import (  # noqa: F401
     STRATEGIES,
     STRATEGY_IDS,
     EncodeStats,
+    FdStats,
     FormatError,
     FractalCode,
+    dbc_dimension,
+    dbc_dimension_raw,
     dbc_grid,
     decode,
     decode_iterates,
@@ -20,9 +24,11 @@ from .codec import (  # noqa: F401
     deserialize,
     encode,
     encode_device,
+    fd_stats,
     fit_transform,
     plan,
     quantize_so,
+    scale_set,
     serialize,
 )
 

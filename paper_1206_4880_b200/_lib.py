@@ -76,7 +76,7 @@ class FicStats(ctypes.Structure):
 
 
 # every symbol include/fic_b200.h declares
-EXPORTS = ("fic_encode_v1", "fic_plan_v1", "fic_pool_v1", "fic_dbc_v1", "fic_decode_v1",
+EXPORTS = ("fic_encode_v1", "fic_plan_v1", "fic_pool_v1", "fic_dbc_v1", "fic_dbc_v2", "fic_decode_v1",
            "fic_decode_step_v1", "fic_shard_pack_v1", "fic_shard_unpack_v1",
            "fic_guard_selftest_v1", "fic_last_error", "fic_abi_version", "fic_release")
 
@@ -100,6 +100,9 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.fic_plan_v1.argtypes = [vp, i32, i32, P(FicParams), vp, vp, vp, vp, vp, P(FicStats), vp]
     lib.fic_dbc_v1.argtypes = [vp, i64, i32, i32, P(ctypes.c_double), i32,
                                P(ctypes.c_double), i32, vp, vp]
+    lib.fic_dbc_v2.argtypes = [vp, i64, i32, i32, i32, P(ctypes.c_double), i32,
+                               P(ctypes.c_double), i32, vp, vp]
+    lib.fic_dbc_v2.restype = ctypes.c_int
     lib.fic_decode_v1.argtypes = [vp, i32, i32, i32, i32, i32, i32, ctypes.c_double, vp, vp, vp]
     lib.fic_pool_v1.argtypes = [vp, i32, i32, P(FicParams), vp, vp, vp, vp, vp, vp]
     lib.fic_decode_step_v1.argtypes = [vp, i32, i32, i32, i32, i32, vp, vp, vp, vp]

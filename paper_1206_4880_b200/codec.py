@@ -511,8 +511,9 @@ def dequantize_so(s_q: int, o_q: int) -> tuple[float, float]:
 # component entry points (used by parity tests)
 # ---------------------------------------------------------------------------
 
-def dbc_grid(blocks, clamp: bool = True) -> np.ndarray:
-    """Drop-in for ``fic.fdim.dbc_grid`` (fdim.py:44-80) on the GPU."""
+def dbc_grid(blocks, gray_levels: int = 256, clamp: bool = True) -> np.ndarray:
+    """Drop-in for ``fic.fdim.dbc_grid`` (fdim.py:44-80) on the GPU (uint8
+    blocks; the argument order is the reference's)."""
     torch = _torch()
     blocks = np.ascontiguousarray(blocks)
     if blocks.ndim != 3 or blocks.shape[1] != blocks.shape[2]:
@@ -520,14 +521,49 @@ def dbc_grid(blocks, clamp: bool = True) -> np.ndarray:
     n, side, _ = blocks.shape
     if len(dbc_scales(side)) < 2:
         raise ValueError(f"block side {side} too small: need at least two DBC scales")
-    d_blk = torch.from_numpy(blocks.astype(np.uint8)).cuda()
+    if blocks.dtype != np.uint8:
+        raise ValueError("the GPU path takes uint8 blocks")
+    if int(gray_levels) != gray_levels or gray_levels < 1:
+        raise ValueError("gray_levels must be a positive integer on the GPU path")
+    d_blk = torch.from_numpy(blocks).cuda()
     d_fd = torch.empty(n, dtype=torch.float64, device=d_blk.device)
     ln, wt = ln_table(), dbc_weights(side)
-    rc = _lib.load().fic_dbc_v1(ctypes.c_void_p(d_blk.data_ptr()), n, side, 1 if clamp else 0,
-                                _dptr(ln), len(ln), _dptr(wt), len(wt),
+    rc = _lib.load().fic_dbc_v2(ctypes.c_void_p(d_blk.data_ptr()), n, side, int(gray_levels),
+                                1 if clamp else 0, _dptr(ln), len(ln), _dptr(wt), len(wt),
                                 ctypes.c_void_p(d_fd.data_ptr()), _stream(torch, d_blk.device))
     _lib.check(rc)
     return d_fd.cpu().numpy()
+
+
+def dbc_dimension(block, gray_levels: int = 256) -> float:
+    """``fic.fdim.dbc_dimension`` (fdim.py:83-85): one block, clamped to [2, 3]."""
+    return float(dbc_grid(np.asarray(block)[None], gray_levels)[0])
+
+
+def dbc_dimension_raw(block, gray_levels: int = 256) -> float:
+    """``fic.fdim.dbc_dimension_raw`` (fdim.py:88-90): the unclamped slope."""
+    return float(dbc_grid(np.asarray(block)[None], gray_levels, clamp=False)[0])
+
+
+@dataclass(frozen=True)
+class FdStats:  # fdim.py:19-23
+    f_min: float
+    f_max: float
+    d_f: float  # fractal distance, (f_max - f_min) / 3
+
+
+def fd_stats(fds) -> FdStats:
+    """``fic.fdim.fd_stats`` (fdim.py:93-100) for a host array; the encoder
+    computes the same three numbers on the device (``k_slab_scalars``) and
+    returns them in ``EncodeStats.device`` / ``plan()``."""
+    arr = np.asarray(fds, dtype=np.float64)
+    if arr.size == 0:
+        raise ValueError("fd_stats requires a non-empty sequence")
+    f_min, f_max = float(arr.min()), float(arr.max())
+    return FdStats(f_min=f_min, f_max=f_max, d_f=(f_max - f_min) / 3.0)
+
+
+scale_set = dbc_scales  # fdim.py:26-34 under the reference's name
 
 
 def plan(image, strategy="dynamic_fd", *, range_size=8, domain_size=16, stride=1,

@@ -273,11 +273,11 @@ struct DbcTables {
 };
 
 static DbcTables make_dbc(Scratch& sc, cudaStream_t s, int side, const double* h_ln, int ln_len,
-                          const double* h_w, int n_w) {
+                          const double* h_w, int n_w, int gray_levels = 256) {
   DbcTables t;
   std::vector<uint16_t> q(7 * 256);
   int need = 0;
-  t.J = dbc_tables(side, q.data(), &t.smax, &need);
+  t.J = dbc_tables(side, q.data(), &t.smax, &need, gray_levels);
   if (t.J < 2)
     invalid("block side " + std::to_string(side) + " too small: need at least two DBC scales");
   // ln table: caller's numpy values if long enough, else C log()
@@ -320,7 +320,7 @@ static DbcTables make_dbc(Scratch& sc, cudaStream_t s, int side, const double* h
   static std::map<std::vector<double>, DbcTables> cache;
   int dev = 0;
   FIC_CUDA(cudaGetDevice(&dev));
-  std::vector<double> key{(double)dev, (double)side, (double)need};
+  std::vector<double> key{(double)dev, (double)side, (double)need, (double)gray_levels};
   key.insert(key.end(), w.begin(), w.end());
   key.insert(key.end(), ln.begin(), ln.end());
   std::lock_guard<std::mutex> lock(mu);
@@ -2116,13 +2116,14 @@ extern "C" int fic_pool_v1(const uint8_t* d_image, int32_t height, int32_t width
   });
 }
 
-extern "C" int fic_dbc_v1(const uint8_t* d_blocks, int64_t n, int32_t side, int32_t clamp,
+extern "C" int fic_dbc_v2(const uint8_t* d_blocks, int64_t n, int32_t side, int32_t gray_levels, int32_t clamp,
                           const double* h_ln_table, int32_t ln_len, const double* h_weights,
                           int32_t n_weights, double* d_fd, void* stream) {
   return guarded([&] {
+    if (gray_levels < 1 || gray_levels > (1 << 20)) invalid("gray_levels must be in [1, 2^20]");
     cudaStream_t s = as_stream(stream);
     Scratch sc(s);
-    DbcTables t = make_dbc(sc, s, side, h_ln_table, ln_len, h_weights, n_weights);
+    DbcTables t = make_dbc(sc, s, side, h_ln_table, ln_len, h_weights, n_weights, gray_levels);
     FdArgs fa{};
     fa.src = d_blocks;
     fa.side = side;
@@ -2140,6 +2141,12 @@ extern "C" int fic_dbc_v1(const uint8_t* d_blocks, int64_t n, int32_t side, int3
     FIC_CUDA(cudaStreamSynchronize(s));
     sc.verify("dbc");
   });
+}
+
+extern "C" int fic_dbc_v1(const uint8_t* d_blocks, int64_t n, int32_t side, int32_t clamp,
+                          const double* h_ln_table, int32_t ln_len, const double* h_weights,
+                          int32_t n_weights, double* d_fd, void* stream) {
+  return fic_dbc_v2(d_blocks, n, side, 256, clamp, h_ln_table, ln_len, h_weights, n_weights, d_fd, stream);
 }
 
 extern "C" int fic_decode_v1(const uint8_t* d_records, int32_t height, int32_t width,

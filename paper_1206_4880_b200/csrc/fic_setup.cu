@@ -23,7 +23,7 @@ namespace fic {
 // fp64 division numpy performs, so any block side is bit-exact.
 // ============================================================================
 
-int dbc_tables(int side, uint16_t* quot, int* smax, int* ln_needed) {
+int dbc_tables(int side, uint16_t* quot, int* smax, int* ln_needed, int gray_levels) {
   std::vector<int> scales;
   for (int s = 2; s <= side / 2; s *= 2)
     if (side % s == 0) scales.push_back(s);
@@ -32,7 +32,8 @@ int dbc_tables(int side, uint16_t* quot, int* smax, int* ln_needed) {
   if (J > 7) invalid("block side too large for the DBC kernel (max 7 scales)");
   int need = 0;
   for (int j = 0; j < J; ++j) {
-    double h = (double)(scales[j] * 256) / (double)side;  // fdim.py:74
+    double h = (double)(scales[j] * gray_levels) / (double)side;  // fdim.py:74 (s * gray_levels is exact)
+    if (std::floor(255.0 / h) > 65535.0) invalid("gray_levels too small for this block side on the GPU path");
     for (int v = 0; v < 256; ++v) quot[j * 256 + v] = (uint16_t)std::floor((double)v / h);
     int k = side / scales[j];
     need = std::max(need, k * k * (quot[j * 256 + 255] - quot[j * 256 + 0]) + k * k);

@@ -35,7 +35,7 @@ struct FdArgs {
 };
 // Builds host-side tables for block side `side` into `quot` (J*256), returns
 // J and the coarsest scale and the ln-table length required.
-int dbc_tables(int side, uint16_t* quot, int* smax, int* ln_needed);
+int dbc_tables(int side, uint16_t* quot, int* smax, int* ln_needed, int gray_levels = 256);
 void launch_fd(const FdArgs& a, cudaStream_t s);
 
 // ---- K3: FD index + slabs (avltree.py:150-189, codec.py:343-375) ------------
