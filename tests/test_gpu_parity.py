@@ -572,7 +572,12 @@ def test_kernels_with_per_call_shared_memory_any_size_order():
 
 def _sweep_cases(n=150, seed=2026):
     """Seeded random small encodes: strategy, range size (domain = 2x),
-    stride, isometries, delta, fd_source, matcher and forced tensor routing."""
+    stride, isometries, delta, fd_source, matcher and forced tensor routing.
+    SWEEP_N / SWEEP_SEED in the environment run a larger one-off campaign
+    (profiles/r02e_sweep_campaign.md)."""
+    import os
+    n = int(os.environ.get("SWEEP_N", n))
+    seed = int(os.environ.get("SWEEP_SEED", seed))
     rng = np.random.default_rng(seed)
     out = []
     for i in range(n):
@@ -708,3 +713,64 @@ def test_graph_replay_follows_image_content(cname):
         assert torch.equal(r.pre_rms, d.pre_rms) and torch.equal(r.post_rms, d.post_rms)
         assert torch.equal(r.pool_sizes, d.pool_sizes)
         assert r.stats["comparisons"] == d.stats["comparisons"]
+
+
+def _mid_cases(n=4, seed=4242):
+    """Seeded mid-size encodes (128-320 px sides, 8x8 and 4x4 ranges, strides
+    1-4): big enough for the tensor matcher's multi-tile windows, segments,
+    pilot and hit list, small enough for the oracle.  Image kinds stress the
+    screen: low contrast (two or three grey levels: ties everywhere),
+    gradients with faint noise (near-flat ranges), textures, flat areas.
+    SWEEP_MID_N / SWEEP_SEED in the environment run a larger campaign."""
+    import os
+    n = int(os.environ.get("SWEEP_MID_N", n))
+    rng = np.random.default_rng(int(os.environ.get("SWEEP_SEED", seed)))
+    out = []
+    for i in range(n):
+        rs = int(rng.choice([4, 8]))
+        stride = int(rng.choice([1, 2, 4]) if rs == 4 else rng.choice([2, 4]))
+        h, w = int(rng.integers(8, 21)) * 16, int(rng.integers(8, 21)) * 16
+        # keep the oracle's work (R x D x 8 matches at ~1.3e7/s) under ~20 s
+        while (h // rs) * (w // rs) * ((h - 2 * rs) // stride + 1) * ((w - 2 * rs) // stride + 1) * 8 > 2.5e8:
+            h, w = max(64, h // 2 // 16 * 16), max(64, w // 2 // 16 * 16)
+        out.append(dict(i=i, rs=rs, h=h, w=w, stride=stride, small_pool=int(rng.choice([0, 1])),
+                        strategy=str(rng.choice(["exhaustive", "dynamic_fd"]) if rs == 8 else "exhaustive"),
+                        delta=[None, 0.05, 0.2][int(rng.integers(0, 3))],
+                        kind=str(rng.choice(["lowcontrast", "gradient", "texture", "flatmix"])),
+                        seed=int(rng.integers(1 << 30))))
+    return out
+
+
+def _mid_image(c):
+    rng = np.random.default_rng(c["seed"])
+    h, w = c["h"], c["w"]
+    if c["kind"] == "lowcontrast":
+        return (100 + rng.integers(0, int(rng.integers(2, 4)), (h, w))).astype(np.uint8)
+    if c["kind"] == "gradient":
+        g = np.add.outer(np.arange(h) * rng.uniform(0.05, 0.6), np.arange(w) * rng.uniform(0.05, 0.6))
+        return np.clip(g + rng.normal(0, rng.choice([0.3, 1.0, 3.0]), (h, w)), 0, 255).astype(np.uint8)
+    if c["kind"] == "texture":
+        return synth.to_u8(synth.fbm(max(h, w), float(rng.uniform(0.2, 0.8)), rng))[:h, :w].copy()
+    img = rng.integers(0, 256, (h, w)).astype(np.uint8)
+    img[: h // 2, : w // 2] = 37
+    img[h // 2:, w // 2:] = (200 + rng.integers(0, 2, (h - h // 2, w - w // 2))).astype(np.uint8)
+    return img
+
+
+@pytest.mark.parametrize("case", _mid_cases(), ids=lambda c: f"mid{c['i']}")
+def test_random_mid_size_encodes_match_oracle(case):
+    import torch
+
+    c = case
+    img = _mid_image(c)
+    kw = dict(range_size=c["rs"], domain_size=2 * c["rs"], stride=c["stride"], isometries=True)
+    delta = c["delta"] if c["strategy"] == "dynamic_fd" else None
+    ref = orc.encode(img, c["strategy"], delta=delta, **kw)
+    res = codec.encode_device(torch.from_numpy(img).cuda(), c["strategy"], delta=delta,
+                              small_pool=c["small_pool"], **kw)
+    if c["small_pool"] == 1:
+        assert res.stats["tensor_tiles"] > 0, c
+    assert np.array_equal(_recs(res.records.cpu().numpy()), ref.records), c
+    assert np.array_equal(res.pre_rms.cpu().numpy(), ref.pre_rms), c
+    assert np.array_equal(res.post_rms.cpu().numpy(), ref.post_rms), c
+    assert res.stats["comparisons"] == ref.comparisons
