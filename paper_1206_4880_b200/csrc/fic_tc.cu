@@ -87,6 +87,9 @@ constexpr bool WIDE = FIC_TC_WIDE;
 #ifndef FIC_TC_F16ACC
 #define FIC_TC_F16ACC 0
 #endif
+#ifndef FIC_TC_DUMP
+#define FIC_TC_DUMP 1  // 8x8 main items hand a hit row's 64 accumulator values to the rescoring warp (hit ring); 0: per-row survivor queues
+#endif
 #ifndef FIC_TC_LEAN
 #define FIC_TC_LEAN 0  // 1: experiment, 4x4 main items without the slow path (hit list only)
 #endif
@@ -394,6 +397,21 @@ __global__ void __maxnreg__(MAXREG)
   volatile uint32_t* qtail = qbuf + BM * NSLICE * QCAP;        // [BM][NSLICE] (screener-owned)
   volatile uint32_t* qhead = qtail + BM * NSLICE;              // [BM][NSLICE] (rescorer-owned)
   volatile uint32_t* edone = qhead + BM * NSLICE;              // screening warps done
+  // hit ring (FIC_TC_DUMP, 8x8 main items; aliases the survivor queues it
+  // replaces): a hit lane copies its chunk's 64 accumulator values and the
+  // row / column / window of the chunk into the next of NSLOT slots -- no
+  // mask, no seeding, no per-survivor push on the screening warp, whose
+  // stall would hold up the whole accumulator ring -- and the rescoring warp
+  // filters them against the row's freshest threshold, 32 lanes per slot
+  constexpr bool DUMP = FIC_TC_DUMP && K == 64;
+  constexpr int NSLOT = 64, SLOTW = CH + 5, SLOTB = SLOTW * 4;  // odd word stride: lane-per-slot reads hit distinct banks
+  static_assert(NSLOT * SLOTB + NSLOT * 4 + 16 + BM * 16 <= BM * NSLICE * QCAP * 4, "hit ring fits the queues");
+  uint8_t* ring = reinterpret_cast<uint8_t*>(qbuf);                               // [NSLOT][SLOTB]
+  volatile uint32_t* ring_flag = reinterpret_cast<uint32_t*>(ring + NSLOT * SLOTB);  // [NSLOT]: ticket + 1 when filled
+  volatile uint32_t* ring_ticket = ring_flag + NSLOT;                              // next ticket (screeners)
+  volatile uint32_t* ring_head = ring_ticket + 1;                                  // slots consumed (rescorer)
+  double* rowV = reinterpret_cast<double*>(const_cast<uint32_t*>(ring_ticket) + 4);  // [BM] V of each row
+  double* rowEps = rowV + BM;                                                       // [BM] screen slack
   struct RowState { double err, pre, sr, srr; uint32_t dom; uint8_t sq, oq, iso, valid; };
   RowState* rstate = reinterpret_cast<RowState*>(
       reinterpret_cast<uint8_t*>(const_cast<uint32_t*>(edone)) + 16);  // [BM]
@@ -660,6 +678,10 @@ __global__ void __maxnreg__(MAXREG)
         } else {
           rlo = rhi = 0;
         }
+        if (DUMP && group == 0 && slice == 0) {
+          rowV[row] = rvalid ? V : 0.0;
+          rowEps[row] = rvalid ? eps : 0.0;
+        }
       }
       prev_tile = tile;
     }
@@ -675,6 +697,13 @@ __global__ void __maxnreg__(MAXREG)
       qhead[i] = 0;
     }
     if (threadIdx.x == 0) *edone = 0;
+    if (DUMP) {
+      if (threadIdx.x < NSLOT) ring_flag[threadIdx.x] = 0;
+      if (threadIdx.x == 0) {
+        *ring_ticket = 0;
+        *ring_head = 0;
+      }
+    }
     cta_sync<CG>();
     tsetup += TCLK() - ti0;
     const long long ti1 = TCLK();
@@ -1075,6 +1104,27 @@ __global__ void __maxnreg__(MAXREG)
           return true;
         };
         auto on_hit = [&](const float* v, int32_t rel, int32_t e_lo, int32_t e_hi, bool hit) {
+          if constexpr (DUMP) {
+            if (FIC_TC_PROF) {
+              ++hit_rounds;
+              hit_lanes += hit ? 1 : 0;
+            }
+            if (hit) {
+              const long long ts0 = TCLK();
+              const uint32_t t = atomicAdd(const_cast<uint32_t*>(ring_ticket), 1u);
+              while (t - *ring_head >= (uint32_t)NSLOT) __nanosleep(32);
+              uint32_t* dst = reinterpret_cast<uint32_t*>(ring + (t % NSLOT) * SLOTB);
+#pragma unroll
+              for (int e = 0; e < CH; ++e) dst[e] = __float_as_uint(v[e]);
+              dst[CH] = (uint32_t)row;
+              dst[CH + 1] = (uint32_t)rel;
+              dst[CH + 2] = (uint32_t)max(e_lo, 0) | ((uint32_t)min(e_hi, CH) << 8);
+              __threadfence_block();
+              ring_flag[t % NSLOT] = t + 1;
+              tw4 += TCLK() - ts0;
+            }
+            return;
+          }
           // (4x4 ranges only: the 8x8 screeners keep their registers)
 #if FIC_TC_LEAN
           // experiment: 4x4 main items append every hit chunk to the hit list
@@ -1258,6 +1308,152 @@ __global__ void __maxnreg__(MAXREG)
         }
       };
       constexpr int NE = 4;  // candidates per lane and pass
+      if constexpr (DUMP) {
+        // hit ring consumer: up to 32 slots per pass, in ticket order (the
+        // ready prefix of the next 32 tickets), the warp's lanes split evenly
+        // over the pass's slots: they filter the chunk's 64 values against
+        // the row's freshest threshold (a row without one first evaluates
+        // the chunk's best |u|), the slots are handed back, the survivors
+        // are evaluated exactly and the lanes' results merged per row
+        // (lowest lane of each row)
+        constexpr unsigned long long INF_BITS = 0x7ff0000000000000ull;
+        uint32_t next = 0;
+        while (true) {
+          const uint32_t myt = next + (uint32_t)t, sl = myt % NSLOT;
+          const unsigned rb = __ballot_sync(0xffffffffu, ring_flag[sl] == myt + 1);
+          const int n = rb == 0xffffffffu ? 32 : __ffs((int)~rb) - 1;
+          if (n == 0) {
+            if (*edone == (uint32_t)NEPI) {
+              __threadfence_block();
+              if (*ring_ticket == next) break;  // every ticket taken has been consumed
+            } else {
+              __nanosleep(512);
+            }
+            continue;
+          }
+          __threadfence_block();  // the slots' data behind their flags
+          // L lanes per slot (a power of two, 32 for one slot .. 1 for 17-32
+          // slots), each CH / L columns... the usual pass has one or two slots,
+          // and a single lane sweeping 64 values would cost the warp (and the
+          // screening warps sharing its scheduler) 64 iterations of issue slots
+          int lg = 0;  // log2(slots rounded up to a power of two)
+          while ((1 << lg) < n) ++lg;
+          const int L = 32 >> lg, cpl = CH / L;  // lanes per slot, columns per lane (2 .. 64)
+          const int si = t >> (5 - lg), sub = t & (L - 1);
+          const bool act = si < n;
+          const uint32_t* sw = reinterpret_cast<const uint32_t*>(ring + ((next + (uint32_t)si) % NSLOT) * SLOTB);
+          int r = 0, wl = 0, wh = 0;
+          int32_t rel = 0;
+          if (act) {
+            r = (int)sw[CH];
+            rel = (int32_t)sw[CH + 1];
+            wl = (int)(sw[CH + 2] & 255u);
+            wh = (int)(sw[CH + 2] >> 8);
+          }
+          const int k = r / n_iso;
+          const double e_sr = rstate[r].sr, e_srr = rstate[r].srr, Vr = rowV[r], er = rowEps[r];
+          unsigned long long tb = thr_s[k];
+          double b_err = INFINITY, b_pre = INFINITY;
+          uint32_t b_dom = 0xffffffffu, b_q = 0;
+          auto take = [&](int c) {  // exact evaluation of column c of the chunk into the lane's best
+            const int64_t p = c0 + rel + c;
+            const uint32_t id = pool_id(P, p);
+            const Cand cd = exact(p, id, r, e_sr, e_srr);
+            b_pre = fmin(b_pre, cd.pre);
+            if (better(cd.err, id, 0, b_err, b_dom, 0)) {
+              b_err = cd.err;
+              b_dom = id;
+              b_q = (uint32_t)cd.sq | ((uint32_t)cd.oq << 8);
+            }
+            ++evals;
+          };
+          auto s_of = [&](unsigned long long bits) -> float {
+            const double cth = Vr - __longlong_as_double((long long)bits) - 1e-5;
+            return (bits != INF_BITS && cth > 0.0) ? __double2float_rd(sqrt(cth) * (1.0 - 1e-9) - er) : -1.0f;
+          };
+          float s_r = s_of(tb);
+          const int q0 = sub * cpl;
+          uint64_t mask = 0;  // bit q - q0: column q survives
+          float bestv = -1.0f;
+          int bestc = -1;
+          if (act) {
+            for (int q = q0; q < q0 + cpl; ++q) {
+              const float v = fabsf(__uint_as_float(sw[q]));
+              const bool inw = q >= wl && q < wh;
+              if (inw && v > bestv) {
+                bestv = v;
+                bestc = q;
+              }
+              mask |= (inw && v >= s_r) ? (1ull << (q - q0)) : 0ull;
+            }
+          }
+          if (__any_sync(0xffffffffu, act && tb == INF_BITS)) {
+            // a range without a threshold: the chunk's best |u| (over the
+            // slot's L lanes) is evaluated first, the rest filtered against it
+            float gv = bestv;
+            for (int m = 1; m < L; m <<= 1) gv = fmaxf(gv, __shfl_xor_sync(0xffffffffu, gv, m));
+            const bool noth = act && tb == INF_BITS && gv >= 0.0f;
+            // the slot's lowest lane holding the maximum evaluates it
+            const unsigned cand = __ballot_sync(0xffffffffu, noth && bestv == gv);
+            const unsigned mine = cand & (L == 32 ? 0xffffffffu : (((1u << L) - 1u) << (t & ~(L - 1))));
+            const int first = __ffs((int)mine) - 1;
+            double e0 = INFINITY;
+            if (noth && t == first) {
+              take(bestc);
+              e0 = b_err;
+            }
+            e0 = __shfl_sync(0xffffffffu, e0, first < 0 ? 0 : first);
+            if (noth) {
+              tb = (unsigned long long)__double_as_longlong(fmax(e0, 0.0));
+              s_r = s_of(tb);
+              mask = 0;
+              for (int q = q0; q < q0 + cpl; ++q) {
+                const float v = fabsf(__uint_as_float(sw[q]));
+                mask |= (q >= wl && q < wh && !(t == first && q == bestc) && v >= s_r) ? (1ull << (q - q0)) : 0ull;
+              }
+            }
+          }
+          __syncwarp();
+          next += (uint32_t)n;
+          if (t == 0) *ring_head = next;  // the slots of this pass are free again
+          while (mask) {
+            const int c = __ffsll((long long)mask) - 1;
+            mask &= mask - 1;
+            take(q0 + c);
+          }
+          // merge per row: the lowest lane of each row applies its lanes' results
+          const bool has = act && b_dom != 0xffffffffu;
+          if (!__any_sync(0xffffffffu, has)) continue;
+          s_cerr[t] = b_err;
+          s_cpre[t] = b_pre;
+          s_cdom[t] = b_dom;
+          s_csqoq[t] = b_q;
+          __syncwarp();
+          const unsigned grp = __match_any_sync(0xffffffffu, has ? (uint32_t)r : (0x80000000u | (uint32_t)t));
+          if (has && t == __ffs((int)grp) - 1) {
+            RowState st = rstate[r];
+            unsigned g2 = grp;
+            while (g2) {
+              const int j = __ffs((int)g2) - 1;
+              g2 &= g2 - 1;
+              st.pre = fmin(st.pre, s_cpre[j]);
+              if (better(s_cerr[j], s_cdom[j], st.iso, st.err, st.dom, st.iso)) {
+                st.err = s_cerr[j];
+                st.dom = s_cdom[j];
+                st.sq = (uint8_t)(s_csqoq[j] & 255u);
+                st.oq = (uint8_t)(s_csqoq[j] >> 8);
+              }
+            }
+            rstate[r] = st;
+            const unsigned long long eb = (unsigned long long)__double_as_longlong(fmax(st.err, 0.0));
+            if (eb < thr_s[k]) {  // an improvement: publish to the screeners and the other segments
+              atomicMin(thr_s + k, eb);
+              atomicMin(a.thr_g + s_rid[k], eb);
+            }
+          }
+          __syncwarp();
+        }
+      } else {
 #if FIC_TC_BAL
       // Balanced drain: the warp is the single consumer of all 2 x 128
       // queues; each pass takes up to 32 x NE pending entries from any rows
@@ -1433,6 +1629,7 @@ __global__ void __maxnreg__(MAXREG)
         }
       }
 #endif
+      }
       __syncwarp();
       // combine the n_iso rows of each range: lexicographic (err, dom, iso)
 #pragma unroll
