@@ -90,6 +90,12 @@ constexpr bool WIDE = FIC_TC_WIDE;
 #ifndef FIC_TC_DUMP
 #define FIC_TC_DUMP 1  // 8x8 main items hand a hit row's 64 accumulator values to the rescoring warp (hit ring); 0: per-row survivor queues
 #endif
+#ifndef FIC_TC_RES_SLEEP
+#define FIC_TC_RES_SLEEP 512  // ns the rescoring warp sleeps when the hit ring is empty
+#endif
+#ifndef FIC_TC_RES_DIRECT
+#define FIC_TC_RES_DIRECT 0  // 1: a pass whose results sit in one lane skips the per-row merge staging
+#endif
 #ifndef FIC_TC_LEAN
 #define FIC_TC_LEAN 0  // 1: experiment, 4x4 main items without the slow path (hit list only)
 #endif
@@ -1327,7 +1333,7 @@ __global__ void __maxnreg__(MAXREG)
               __threadfence_block();
               if (*ring_ticket == next) break;  // every ticket taken has been consumed
             } else {
-              __nanosleep(512);
+              __nanosleep(FIC_TC_RES_SLEEP);
             }
             continue;
           }
@@ -1423,7 +1429,28 @@ __global__ void __maxnreg__(MAXREG)
           }
           // merge per row: the lowest lane of each row applies its lanes' results
           const bool has = act && b_dom != 0xffffffffu;
-          if (!__any_sync(0xffffffffu, has)) continue;
+          const unsigned hb = __ballot_sync(0xffffffffu, has);
+          if (!hb) continue;
+          if (FIC_TC_RES_DIRECT && (hb & (hb - 1)) == 0) {  // one lane holds the pass's only results
+            if (has) {
+              RowState st = rstate[r];
+              st.pre = fmin(st.pre, b_pre);
+              if (better(b_err, b_dom, st.iso, st.err, st.dom, st.iso)) {
+                st.err = b_err;
+                st.dom = b_dom;
+                st.sq = (uint8_t)(b_q & 255u);
+                st.oq = (uint8_t)(b_q >> 8);
+              }
+              rstate[r] = st;
+              const unsigned long long eb = (unsigned long long)__double_as_longlong(fmax(st.err, 0.0));
+              if (eb < thr_s[k]) {
+                atomicMin(thr_s + k, eb);
+                atomicMin(a.thr_g + s_rid[k], eb);
+              }
+            }
+            __syncwarp();
+            continue;
+          }
           s_cerr[t] = b_err;
           s_cpre[t] = b_pre;
           s_cdom[t] = b_dom;
