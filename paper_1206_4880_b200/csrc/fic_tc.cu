@@ -68,7 +68,10 @@ constexpr int BM = 128;       // rows per tile (TMEM lanes)
 constexpr int BN = FIC_TC_BN;  // columns per N-tile (one TMEM accumulator stage)
 constexpr int NACC = 512 / BN;  // TMEM accumulator stages (NACC * BN = 512 columns)
 #ifndef FIC_TC_NGRP
-#define FIC_TC_NGRP 2
+// four groups of four screening warps (20 warps, 96 registers): pays since the hit
+// ring took the hit path off the screeners (cfg3 5.59 -> 5.30 ms, cfg4 16.4 -> 15.4 ms;
+// with the survivor queues it was slower than two groups at 168 registers)
+#define FIC_TC_NGRP 4
 #endif
 #ifndef FIC_TC_NSPLIT
 #define FIC_TC_NSPLIT 1
@@ -89,6 +92,9 @@ constexpr bool WIDE = FIC_TC_WIDE;
 #endif
 #ifndef FIC_TC_DUMP
 #define FIC_TC_DUMP 1  // 8x8 main items hand a hit row's 64 accumulator values to the rescoring warp (hit ring); 0: per-row survivor queues
+#endif
+#ifndef FIC_TC_SLOTW
+#define FIC_TC_SLOTW 68  // hit-ring slot stride in 32-bit words (64 values + row, column, window)
 #endif
 #ifndef FIC_TC_RES_SLEEP
 #define FIC_TC_RES_SLEEP 512  // ns the rescoring warp sleeps when the hit ring is empty
@@ -410,7 +416,9 @@ __global__ void __maxnreg__(MAXREG)
   // stall would hold up the whole accumulator ring -- and the rescoring warp
   // filters them against the row's freshest threshold, 32 lanes per slot
   constexpr bool DUMP = FIC_TC_DUMP && K == 64;
-  constexpr int NSLOT = 64, SLOTW = CH + 5, SLOTB = SLOTW * 4;  // odd word stride: lane-per-slot reads hit distinct banks
+  // slot stride in words: CH + 5 (odd: lanes reading different slots hit distinct
+  // banks, scalar stores) or CH + 4 (16-byte aligned: the copy is 17 128-bit stores)
+  constexpr int NSLOT = 64, SLOTW = FIC_TC_SLOTW, SLOTB = SLOTW * 4;
   static_assert(NSLOT * SLOTB + NSLOT * 4 + 16 + BM * 16 <= BM * NSLICE * QCAP * 4, "hit ring fits the queues");
   uint8_t* ring = reinterpret_cast<uint8_t*>(qbuf);                               // [NSLOT][SLOTB]
   volatile uint32_t* ring_flag = reinterpret_cast<uint32_t*>(ring + NSLOT * SLOTB);  // [NSLOT]: ticket + 1 when filled
@@ -425,13 +433,14 @@ __global__ void __maxnreg__(MAXREG)
   // count, per (lane, owned queue) pending count and head, per lane one
   // evaluated candidate
   uint32_t* s_incl = reinterpret_cast<uint32_t*>(rstate + BM);     // [32]
-  uint32_t* s_pend = s_incl + 32;                                   // [32][RROWS * NSLICE]
-  uint32_t* s_hd = s_pend + 32 * RROWS * NSLICE;                    // [32][RROWS * NSLICE]
-  uint32_t* s_crow = s_hd + 32 * RROWS * NSLICE;                    // [32]
+  uint32_t* s_crow = s_incl + 32;                                   // [32]
   uint32_t* s_cdom = s_crow + 32;                                   // [32]
   uint32_t* s_csqoq = s_cdom + 32;                                  // [32]
   double* s_cerr = reinterpret_cast<double*>(s_csqoq + 32);         // [32]
-  [[maybe_unused]] double* s_cpre = s_cerr + 32;                                     // [32]
+  [[maybe_unused]] double* s_cpre = s_cerr + 32;                    // [32]
+  // (balanced drain only, FIC_TC_BAL; with more than two slices they would not fit RS_BYTES)
+  [[maybe_unused]] uint32_t* s_pend = reinterpret_cast<uint32_t*>(s_cpre + 32);  // [32][RROWS * NSLICE]
+  [[maybe_unused]] uint32_t* s_hd = s_pend + 32 * RROWS * NSLICE;                 // [32][RROWS * NSLICE]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   auto full_bar = [&](int s) { return smem_u32(bars + s); };
@@ -1120,11 +1129,19 @@ __global__ void __maxnreg__(MAXREG)
               const uint32_t t = atomicAdd(const_cast<uint32_t*>(ring_ticket), 1u);
               while (t - *ring_head >= (uint32_t)NSLOT) __nanosleep(32);
               uint32_t* dst = reinterpret_cast<uint32_t*>(ring + (t % NSLOT) * SLOTB);
+              const uint32_t win = (uint32_t)max(e_lo, 0) | ((uint32_t)min(e_hi, CH) << 8);
+              if constexpr (SLOTW % 4 == 0) {
+                float4* d4 = reinterpret_cast<float4*>(dst);
 #pragma unroll
-              for (int e = 0; e < CH; ++e) dst[e] = __float_as_uint(v[e]);
-              dst[CH] = (uint32_t)row;
-              dst[CH + 1] = (uint32_t)rel;
-              dst[CH + 2] = (uint32_t)max(e_lo, 0) | ((uint32_t)min(e_hi, CH) << 8);
+                for (int e = 0; e < CH / 4; ++e) d4[e] = make_float4(v[4 * e], v[4 * e + 1], v[4 * e + 2], v[4 * e + 3]);
+                *reinterpret_cast<uint4*>(dst + CH) = make_uint4((uint32_t)row, (uint32_t)rel, win, 0u);
+              } else {
+#pragma unroll
+                for (int e = 0; e < CH; ++e) dst[e] = __float_as_uint(v[e]);
+                dst[CH] = (uint32_t)row;
+                dst[CH + 1] = (uint32_t)rel;
+                dst[CH + 2] = win;
+              }
               __threadfence_block();
               ring_flag[t % NSLOT] = t + 1;
               tw4 += TCLK() - ts0;
