@@ -574,7 +574,7 @@ def _sweep_cases(n=150, seed=2026):
     """Seeded random small encodes: strategy, range size (domain = 2x),
     stride, isometries, delta, fd_source, matcher and forced tensor routing.
     SWEEP_N / SWEEP_SEED in the environment run a larger one-off campaign
-    (profiles/r02e_sweep_campaign.md)."""
+    (profiles/r02_sweep_campaigns.md)."""
     import os
     n = int(os.environ.get("SWEEP_N", n))
     seed = int(os.environ.get("SWEEP_SEED", seed))
