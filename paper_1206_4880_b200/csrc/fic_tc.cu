@@ -93,6 +93,9 @@ constexpr bool WIDE = FIC_TC_WIDE;
 #ifndef FIC_TC_DUMP
 #define FIC_TC_DUMP 1  // 8x8 main items hand a hit row's 64 accumulator values to the rescoring warp (hit ring); 0: per-row survivor queues
 #endif
+#ifndef FIC_TC_DUMP_WAIT
+#define FIC_TC_DUMP_WAIT 0  // 1: a screening lane without a threshold waits for the one its hit-ring slot seeds (measured: cfg3 5.28 -> 5.38 ms; without the pilot 6.23 -> 6.14)
+#endif
 #ifndef FIC_TC_SLOTW
 #define FIC_TC_SLOTW 68  // hit-ring slot stride in 32-bit words (64 values + row, column, window)
 #endif
@@ -1144,6 +1147,19 @@ __global__ void __maxnreg__(MAXREG)
               }
               __threadfence_block();
               ring_flag[t % NSLOT] = t + 1;
+              if (FIC_TC_DUMP_WAIT && thr_bits == 0x7ff0000000000000ull) {
+                // a row without a threshold would copy every chunk of its
+                // window until the rescoring warp has seeded it (it does so
+                // from this very slot: the chunk has a column of the row's
+                // window); waiting here once costs less than that flood
+                volatile unsigned long long* tp = thr_s + rk;
+                unsigned long long tb = *tp;
+                while (tb == 0x7ff0000000000000ull) {
+                  __nanosleep(64);
+                  tb = *tp;
+                }
+                set_threshold(tb);
+              }
               tw4 += TCLK() - ts0;
             }
             return;
