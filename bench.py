@@ -438,6 +438,15 @@ def run_ours(args):
         local = 0
     torch.cuda.set_device(local)
     if dist_on:
+        if "RANK" not in os.environ:  # FIC_BENCH_DIST=1 started without torchrun: a one-rank group
+            import socket
+            sock = socket.socket()
+            sock.bind(("127.0.0.1", 0))
+            port = sock.getsockname()[1]
+            sock.close()
+            os.environ.update(RANK="0", WORLD_SIZE="1", LOCAL_RANK="0")
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", str(port))
         if one_gpu:
             dist.init_process_group("gloo")
         else:
